@@ -1,0 +1,221 @@
+"""CPU oracle for the NDGI tile decode (arXiv 2604.12625) -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference`` arm) may import this package.
+The product path (``paper_2604_12625_b200``) never imports it and shares no
+code with it; see ``oracle/ndgi_oracle.c`` for the definition and the
+citations of every step.
+
+This module is a thin ctypes wrapper: argument marshalling only, all
+arithmetic lives in ``ndgi_oracle.c``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ndgi_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+FMT = {"bc7": 0, "u8": 1, "f16": 2}
+GELU = {"erf": 0, "tanh": 1}
+BORDER = {"mirror": 0, "eval_clamp": 1}
+
+
+def build(force: bool = False) -> str:
+    """Compile ndgi_oracle.c to liboracle.so (plain gcc, -O2, fp-contract off)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-ffp-contract=off", "-fPIC", "-shared",
+             "-o", _LIB, _SRC, "-lm", "-lpthread"])
+    return _LIB
+
+
+class Layout(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "num_tiles", "atlases", "tiles_x", "tiles_y", "core", "border", "uv_res", "uvt_res",
+        "uvt_depth", "line_res", "line_t", "hidden", "fmt_uv", "fmt_uvt", "fmt_line", "gelu",
+        "border_mode")]
+
+
+class Maps(C.Structure):
+    _fields_ = [("uv", C.c_void_p), ("uvt", C.c_void_p), ("ut", C.c_void_p), ("vt", C.c_void_p),
+                ("mlp", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P, D, I, U32 = C.c_void_p, C.c_double, C.c_int, C.c_uint32
+        sig = {
+            "oracle_half_to_double": (D, [C.c_uint16]),
+            "oracle_bc7_decode_block": (I, [P, P]),
+            "oracle_bc7_decode_image": (None, [P, I, I, P]),
+            "oracle_bc7_weight": (I, [I, I]),
+            "oracle_bc7_subset": (I, [I, I, I]),
+            "oracle_bc7_anchor": (I, [I, I, I]),
+            "oracle_sample2d": (None, [P, I, I, I, I, D, D, P]),
+            "oracle_sample_uvt": (None, [P, P, D, D, D, P]),
+            "oracle_gamma": (None, [D, P]),
+            "oracle_features": (None, [P, P, I, D, D, D, P]),
+            "oracle_gelu": (D, [D, I]),
+            "oracle_mlp": (None, [I, P, P, I, P]),
+            "oracle_texel": (None, [P, P, I, I, I, D, P]),
+            "oracle_decode_tiles": (I, [P, P, P, U32, D, P, I]),
+            "oracle_decode_full": (I, [P, P, D, P, I]),
+            "oracle_quantize_rgba8_f64": (None, [P, C.c_size_t, P]),
+            "oracle_quantize_rgba8_f32": (None, [P, C.c_size_t, C.c_size_t, P]),
+            "oracle_mlp_params": (C.c_size_t, [I]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(_lib, name)
+            f.restype = res
+            f.argtypes = args
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------- BC7
+def bc7_decode_block(block: bytes | np.ndarray) -> tuple[np.ndarray, int]:
+    """One 16-byte block -> (16x4 RGBA8 texels, bits consumed)."""
+    b = np.ascontiguousarray(np.frombuffer(bytes(block), np.uint8))
+    out = np.zeros(64, np.uint8)
+    n = lib().oracle_bc7_decode_block(_ptr(b), _ptr(out))
+    return out.reshape(16, 4), n
+
+
+def bc7_decode_image(blocks: np.ndarray, w: int, h: int) -> np.ndarray:
+    """Row-major BC7 blocks of a w x h image -> [h][w][4] RGBA8."""
+    b = np.ascontiguousarray(blocks, dtype=np.uint8)
+    out = np.zeros((h, w, 4), np.uint8)
+    lib().oracle_bc7_decode_image(_ptr(b), w, h, _ptr(out))
+    return out
+
+
+def bc7_weight(bits: int, index: int) -> int:
+    return lib().oracle_bc7_weight(bits, index)
+
+
+def bc7_subset(ns: int, part: int, texel: int) -> int:
+    return lib().oracle_bc7_subset(ns, part, texel)
+
+
+def bc7_anchor(ns: int, part: int, subset: int) -> int:
+    return lib().oracle_bc7_anchor(ns, part, subset)
+
+
+# ---------------------------------------------------------------- sampling / MLP
+def sample2d(data: np.ndarray, fmt: str, rx: int, ry: int, nc: int, a: float, b: float) -> np.ndarray:
+    d = np.ascontiguousarray(data)
+    out = np.zeros(4, np.float64)
+    lib().oracle_sample2d(_ptr(d), FMT[fmt], rx, ry, nc, float(a), float(b), _ptr(out))
+    return out[:nc]
+
+
+def make_layout(lay: dict) -> Layout:
+    return Layout(
+        num_tiles=lay["num_tiles"], atlases=lay["atlases"], tiles_x=lay["tiles_x"],
+        tiles_y=lay["tiles_y"], core=lay["core"], border=lay["border"], uv_res=lay["uv_res"],
+        uvt_res=lay["uvt_res"], uvt_depth=lay["uvt_depth"], line_res=lay["line_res"],
+        line_t=lay["line_t"], hidden=lay["hidden"], fmt_uv=FMT[lay["fmt_uv"]],
+        fmt_uvt=FMT[lay["fmt_uvt"]], fmt_line=FMT[lay["fmt_line"]], gelu=GELU[lay["gelu"]],
+        border_mode=BORDER[lay["border_mode"]])
+
+
+class Model:
+    """Holds a layout + Theta arrays (numpy, host) and calls the C oracle."""
+
+    def __init__(self, lay: dict, theta: dict):
+        self.lay = dict(lay)
+        self.L = make_layout(lay)
+        self.arrs = {k: np.ascontiguousarray(theta[k]) for k in ("uv", "uvt", "ut", "vt", "mlp")}
+        assert self.arrs["mlp"].dtype == np.uint16
+        self.M = Maps(*(self.arrs[k].ctypes.data for k in ("uv", "uvt", "ut", "vt", "mlp")))
+
+    @property
+    def padded(self) -> int:
+        return self.lay["core"] + 2 * self.lay["border"]
+
+    def features(self, k: int, u: float, v: float, t: float) -> np.ndarray:
+        x = np.zeros(16, np.float64)
+        lib().oracle_features(C.byref(self.L), C.byref(self.M), k, u, v, t, _ptr(x))
+        return x
+
+    def sample_uvt(self, k: int, u: float, v: float, t: float) -> np.ndarray:
+        per = self.arrs["uvt"].reshape(self.lay["num_tiles"], -1)[k]
+        per = np.ascontiguousarray(per)
+        out = np.zeros(4, np.float64)
+        lib().oracle_sample_uvt(C.byref(self.L), _ptr(per), u, v, t, _ptr(out))
+        return out
+
+    def texel(self, k: int, x: int, y: int, t: float) -> np.ndarray:
+        out = np.zeros(3, np.float64)
+        lib().oracle_texel(C.byref(self.L), C.byref(self.M), k, x, y, t, _ptr(out))
+        return out
+
+    def decode_tiles(self, ids, t: float, nthreads: int = 1) -> np.ndarray:
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint32))
+        P = self.padded
+        out = np.zeros((len(ids), P, P, 3), np.float64)
+        rc = lib().oracle_decode_tiles(C.byref(self.L), C.byref(self.M), _ptr(ids), len(ids),
+                                       float(t), _ptr(out), int(nthreads))
+        if rc != 0:
+            raise ValueError("oracle_decode_tiles: tile id out of range")
+        return out
+
+    def decode_full(self, t: float, nthreads: int = 1) -> np.ndarray:
+        L = self.lay
+        C_ = L["core"]
+        out = np.zeros((L["atlases"], L["tiles_y"] * C_, L["tiles_x"] * C_, 3), np.float64)
+        lib().oracle_decode_full(C.byref(self.L), C.byref(self.M), float(t), _ptr(out), int(nthreads))
+        return out
+
+
+def gamma(t: float) -> np.ndarray:
+    g = np.zeros(4, np.float64)
+    lib().oracle_gamma(float(t), _ptr(g))
+    return g
+
+
+def gelu(z: float, variant: str = "erf") -> float:
+    return lib().oracle_gelu(float(z), GELU[variant])
+
+
+def mlp(h: int, w_f16bits: np.ndarray, x: np.ndarray, variant: str = "erf") -> np.ndarray:
+    w = np.ascontiguousarray(w_f16bits, dtype=np.uint16)
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros(3, np.float64)
+    lib().oracle_mlp(h, _ptr(w), _ptr(xx), GELU[variant], _ptr(y))
+    return y
+
+
+def mlp_params(h: int) -> int:
+    return lib().oracle_mlp_params(h)
+
+
+def quantize_rgba8(y3: np.ndarray) -> np.ndarray:
+    """RN-even(clamp(y,0,1)*255), A=255; precision follows y's dtype (f64 or f32)."""
+    if y3.dtype == np.float32:
+        y = np.ascontiguousarray(y3)
+        stride = y.shape[-1]
+        n = y.size // stride
+        out = np.zeros(y.shape[:-1] + (4,), np.uint8)
+        lib().oracle_quantize_rgba8_f32(_ptr(y), stride, n, _ptr(out))
+        return out
+    y = np.ascontiguousarray(y3, dtype=np.float64)
+    assert y.shape[-1] == 3
+    n = y.size // 3
+    out = np.zeros(y.shape[:-1] + (4,), np.uint8)
+    lib().oracle_quantize_rgba8_f64(_ptr(y), n, _ptr(out))
+    return out

@@ -1,0 +1,552 @@
+/*
+ * ndgi_oracle.c -- plain, slow, obviously-correct CPU oracle for the NDGI
+ * tile-decode hot path (arXiv 2604.12625).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant generator with the CUDA
+ * path under paper_2604_12625_b200/ and includes nothing from it.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n.  Readings R1..R20
+ * are listed in DESIGN.md section "Readings of the paper".
+ *
+ * What it computes (Eq. 3/4):
+ *   I(u,v,t) = G_Phi(V_uvt, V_uv, V_ut, V_vt, gamma(t))
+ * with every feature fetched from its stored format (BC7 blocks decoded
+ * from scratch on every tap), sampled bilinearly at
+ * texel centres with clamp (R1), trilinearly for F_uvt (R4), an fp64 MLP
+ * with GELU on the hidden layers and a linear output, weights
+ * stored as f16 (R11).
+ *
+ * Pins (tests/test_oracle_*.py): BC7 against Pillow's independent BCn
+ * decoder and hand vectors; samplers against torch grid_sample; MLP against
+ * torch F.linear/F.gelu in fp64; gamma against closed forms;
+ * border against torch F.pad(mode="reflect"); the whole pipeline against a
+ * composition of those library routines.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+/* ------------------------------------------------------------------ */
+/* Layout (the oracle's own struct; mirrors the meaning, not the code, of
+ * include/ndgi.h).                                                     */
+/* ------------------------------------------------------------------ */
+enum { OR_FMT_BC7 = 0, OR_FMT_U8 = 1, OR_FMT_F16 = 2 };
+enum { OR_GELU_ERF = 0, OR_GELU_TANH = 1 };
+enum { OR_BORDER_MIRROR = 0, OR_BORDER_EVAL_CLAMP = 1 };
+
+typedef struct {
+    int32_t num_tiles, atlases, tiles_x, tiles_y;
+    int32_t core, border;
+    int32_t uv_res, uvt_res, uvt_depth, line_res, line_t;
+    int32_t hidden;
+    int32_t fmt_uv, fmt_uvt, fmt_line;
+    int32_t gelu, border_mode;
+} oracle_layout;
+
+typedef struct {
+    const uint8_t *uv, *uvt, *ut, *vt; /* raw bytes, per-tile dense */
+    const uint16_t *mlp;               /* f16 bit patterns */
+} oracle_maps;
+
+/* ------------------------------------------------------------------ */
+/* f16 -> double, exact (IEEE 754 binary16).                           */
+/* ------------------------------------------------------------------ */
+double oracle_half_to_double(uint16_t h)
+{
+    int s = (h >> 15) & 1, e = (h >> 10) & 31, m = h & 1023;
+    double v;
+    if (e == 0)       v = ldexp((double)m, -24);               /* subnormal */
+    else if (e == 31) v = m ? NAN : INFINITY;
+    else              v = ldexp((double)(m + 1024), e - 25);
+    return s ? -v : v;
+}
+
+/* ------------------------------------------------------------------ */
+/* BC7 (BPTC) block decoder.  Definition: D3D11 functional spec, BC7
+ * section / Khronos Data Format spec, BPTC.  The paper stores F_uv and
+ * every t-slice of F_uvt as BC7 and describes the per-block
+ * endpoint interpolation c_p = (1-w_p) e1 + w_p e2 with multi-partition
+ * modes.                                                   */
+/* ------------------------------------------------------------------ */
+
+/* per-mode parameters: subsets, partition bits, rotation bits, index
+ * selection bits, colour bits, alpha bits, per-endpoint p-bits, shared
+ * (per-subset) p-bits, primary index bits, secondary index bits        */
+typedef struct { int ns, pb, rb, isb, cb, ab, epb, spb, ib, ib2; } bc7_mode_info;
+static const bc7_mode_info BC7_MODES[8] = {
+    {3, 4, 0, 0, 4, 0, 1, 0, 3, 0},
+    {2, 6, 0, 0, 6, 0, 0, 1, 3, 0},
+    {3, 6, 0, 0, 5, 0, 0, 0, 2, 0},
+    {2, 6, 0, 0, 7, 0, 1, 0, 2, 0},
+    {1, 0, 2, 1, 5, 6, 0, 0, 2, 3},
+    {1, 0, 2, 0, 7, 8, 0, 0, 2, 2},
+    {1, 0, 0, 0, 7, 7, 1, 0, 4, 0},
+    {2, 6, 0, 0, 5, 5, 1, 0, 2, 0},
+};
+
+/* Two-subset partitions, written as in the D3D11 spec: one digit per texel
+ * in raster order (texel 0 first), the digit is the subset.             */
+static const char *const BC7_P2[64] = {
+    "0011001100110011", "0001000100010001", "0111011101110111", "0001001100110111",
+    "0000000100010011", "0011011101111111", "0001001101111111", "0000000100110111",
+    "0000000000010011", "0011011111111111", "0000000101111111", "0000000000010111",
+    "0001011111111111", "0000000011111111", "0000111111111111", "0000000000001111",
+    "0000100011101111", "0111000100000000", "0000000010001110", "0111001100010000",
+    "0011000100000000", "0000100011001110", "0000000010001100", "0111001100110001",
+    "0011000100010000", "0000100010001100", "0110011001100110", "0011011001101100",
+    "0001011111101000", "0000111111110000", "0111000110001110", "0011100110011100",
+    "0101010101010101", "0000111100001111", "0101101001011010", "0011001111001100",
+    "0011110000111100", "0101010110101010", "0110100101101001", "0101101010100101",
+    "0111001111001110", "0001001111001000", "0011001001001100", "0011101111011100",
+    "0110100110010110", "0011110011000011", "0110011010011001", "0000011001100000",
+    "0100111001000000", "0010011100100000", "0000001001110010", "0000010011100100",
+    "0110110010010011", "0011011011001001", "0110001110011100", "0011100111000110",
+    "0110110011001001", "0110001100111001", "0111111010000001", "0001100011100111",
+    "0000111100110011", "0011001111110000", "0010001011101110", "0100010001110111",
+};
+
+/* Three-subset partitions, same notation. */
+static const char *const BC7_P3[64] = {
+    "0011001102212222", "0001001122112221", "0000200122112211", "0222002200110111",
+    "0000000011221122", "0011001100220022", "0022002211111111", "0011001122112211",
+    "0000000011112222", "0000111111112222", "0000111122222222", "0012001200120012",
+    "0112011201120112", "0122012201220122", "0011011211221222", "0011200122002220",
+    "0001001101121122", "0111001120012200", "0000112211221122", "0022002200221111",
+    "0111011102220222", "0001000122212221", "0000001101220122", "0000110022102210",
+    "0122012200110000", "0012001211222222", "0110122112210110", "0000011012211221",
+    "0022110211020022", "0110011020022222", "0011012201220011", "0000200022112221",
+    "0000000211221222", "0222002200120011", "0011001200220222", "0120012001200120",
+    "0000111122220000", "0120120120120120", "0120201212010120", "0011220011220011",
+    "0011112222000011", "0101010122222222", "0000000021212121", "0022112200221122",
+    "0022001100220011", "0220122102201221", "0101222222220101", "0000212121212121",
+    "0101010101012222", "0222011102220111", "0002111200021112", "0000211221122112",
+    "0222011101110222", "0002111211120002", "0110011001102222", "0000000021122112",
+    "0110011022222222", "0022001100110022", "0022112211220022", "0000000000002112",
+    "0002000100020001", "0222122202221222", "0101222222222222", "0111201122012220",
+};
+
+/* Anchor ("fix-up") texels.  Subset 0's anchor is texel 0. */
+static const int BC7_A2[64] = {
+    15,15,15,15,15,15,15,15, 15,15,15,15,15,15,15,15,
+    15, 2, 8, 2, 2, 8, 8,15,  2, 8, 2, 2, 8, 8, 2, 2,
+    15,15, 6, 8, 2, 8,15,15,  2, 8, 2, 2, 2,15,15, 6,
+     6, 2, 6, 8,15,15, 2, 2, 15,15,15,15,15, 2, 2,15,
+};
+static const int BC7_A3a[64] = {
+     3, 3,15,15, 8, 3,15,15,  8, 8, 6, 6, 6, 5, 3, 3,
+     3, 3, 8,15, 3, 3, 6,10,  5, 8, 8, 6, 8, 5,15,15,
+     8,15, 3, 5, 6,10, 8,15, 15, 3,15, 5,15,15,15,15,
+     3,15, 5, 5, 5, 8, 5,10,  5,10, 8,13,15,12, 3, 3,
+};
+static const int BC7_A3b[64] = {
+    15, 8, 8, 3,15,15, 3, 8, 15,15,15,15,15,15,15, 8,
+    15, 8,15, 3,15, 8,15, 8,  3,15, 6,10,15,15,10, 8,
+    15, 3,15,10,10, 8, 9,10,  6,15, 8,15, 3, 6, 6, 8,
+    15, 3,15,15,15,15,15,15, 15,15,15,15, 3,15,15, 8,
+};
+
+/* Interpolation weights, D3D11 spec aWeight2/3/4. */
+static const int BC7_W2[4]  = {0, 21, 43, 64};
+static const int BC7_W3[8]  = {0, 9, 18, 27, 37, 46, 55, 64};
+static const int BC7_W4[16] = {0, 4, 9, 13, 17, 21, 26, 30, 34, 38, 43, 47, 51, 55, 60, 64};
+
+int oracle_bc7_weight(int bits, int index)
+{
+    if (bits == 2) return BC7_W2[index & 3];
+    if (bits == 3) return BC7_W3[index & 7];
+    if (bits == 4) return BC7_W4[index & 15];
+    return -1;
+}
+
+/* partition table digit for (number of subsets, partition, texel) */
+int oracle_bc7_subset(int ns, int part, int texel)
+{
+    if (ns == 1) return 0;
+    if (ns == 2) return BC7_P2[part][texel] - '0';
+    return BC7_P3[part][texel] - '0';
+}
+
+int oracle_bc7_anchor(int ns, int part, int subset)
+{
+    if (subset == 0) return 0;
+    if (ns == 2) return BC7_A2[part];
+    return subset == 1 ? BC7_A3a[part] : BC7_A3b[part];
+}
+
+/* LSB-first bit reader over the 16-byte block */
+typedef struct { const uint8_t *b; int pos; } bitreader;
+static int take(bitreader *r, int n)
+{
+    int v = 0;
+    for (int i = 0; i < n; ++i) {
+        int bit = (r->b[r->pos >> 3] >> (r->pos & 7)) & 1;
+        v |= bit << i;
+        r->pos++;
+    }
+    return v;
+}
+
+/* expand an n-bit endpoint component to 8 bits by bit replication */
+static int expand8(int v, int n)
+{
+    if (n >= 8) return v;
+    v <<= (8 - n);
+    return v | (v >> n);
+}
+
+static int interp(int e0, int e1, int w) { return ((64 - w) * e0 + w * e1 + 32) >> 6; }
+
+/* Decodes one 128-bit block into 16 RGBA8 texels (texel = 4*row + col).
+ * Returns the number of bits consumed (128 for modes 0..7, 8 for the
+ * reserved mode-8 encoding, which decodes to all zeros, reading R9).   */
+int oracle_bc7_decode_block(const uint8_t blk[16], uint8_t out[64])
+{
+    bitreader r = {blk, 0};
+    int mode = 0;
+    while (mode < 8 && take(&r, 1) == 0) mode++;
+    if (mode == 8) { memset(out, 0, 64); return r.pos; }
+    const bc7_mode_info *mi = &BC7_MODES[mode];
+    int part = take(&r, mi->pb);
+    int rot = take(&r, mi->rb);
+    int isel = take(&r, mi->isb);
+
+    int ep[3][2][4];        /* [subset][endpoint][channel] raw field value */
+    int nbits[4];           /* bits per channel before p-bit */
+    int ne = mi->ns * 2;
+    for (int c = 0; c < 3; ++c) {
+        nbits[c] = mi->cb;
+        for (int e = 0; e < ne; ++e) ep[e / 2][e % 2][c] = take(&r, mi->cb);
+    }
+    if (mi->ab > 0) {
+        nbits[3] = mi->ab;
+        for (int e = 0; e < ne; ++e) ep[e / 2][e % 2][3] = take(&r, mi->ab);
+    } else {
+        nbits[3] = 0;
+    }
+    /* p-bits: appended as the LSB of every channel of the endpoint */
+    int pbit[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    int has_p = 0;
+    if (mi->epb) {
+        has_p = 1;
+        for (int e = 0; e < ne; ++e) pbit[e / 2][e % 2] = take(&r, 1);
+    } else if (mi->spb) {
+        has_p = 1;
+        for (int s = 0; s < mi->ns; ++s) { int p = take(&r, 1); pbit[s][0] = p; pbit[s][1] = p; }
+    }
+    int col[3][2][4];       /* expanded 8-bit endpoints */
+    for (int s = 0; s < mi->ns; ++s)
+        for (int e = 0; e < 2; ++e)
+            for (int c = 0; c < 4; ++c) {
+                if (c == 3 && nbits[3] == 0) { col[s][e][c] = 255; continue; }
+                int v = ep[s][e][c], n = nbits[c];
+                if (has_p) { v = (v << 1) | pbit[s][e]; n += 1; }
+                col[s][e][c] = expand8(v, n);
+            }
+    /* primary indices */
+    int idx1[16], idx2[16];
+    for (int i = 0; i < 16; ++i) {
+        int s = oracle_bc7_subset(mi->ns, part, i);
+        int n = mi->ib - (i == oracle_bc7_anchor(mi->ns, part, s) ? 1 : 0);
+        idx1[i] = take(&r, n);
+    }
+    /* secondary indices (modes 4 and 5); anchor = texel 0 */
+    if (mi->ib2 > 0)
+        for (int i = 0; i < 16; ++i) idx2[i] = take(&r, mi->ib2 - (i == 0 ? 1 : 0));
+
+    for (int i = 0; i < 16; ++i) {
+        int s = oracle_bc7_subset(mi->ns, part, i);
+        int rgba[4];
+        if (mi->ib2 == 0) {
+            int w = oracle_bc7_weight(mi->ib, idx1[i]);
+            for (int c = 0; c < 4; ++c) rgba[c] = interp(col[s][0][c], col[s][1][c], w);
+        } else {
+            /* mode 4: index-selection bit swaps which array drives colour */
+            int cbits = mi->ib, abits = mi->ib2, ci = idx1[i], ai = idx2[i];
+            if (isel) { cbits = mi->ib2; abits = mi->ib; ci = idx2[i]; ai = idx1[i]; }
+            int wc = oracle_bc7_weight(cbits, ci), wa = oracle_bc7_weight(abits, ai);
+            for (int c = 0; c < 3; ++c) rgba[c] = interp(col[0][0][c], col[0][1][c], wc);
+            rgba[3] = interp(col[0][0][3], col[0][1][3], wa);
+        }
+        if (rot) { int t = rgba[3]; rgba[3] = rgba[rot - 1]; rgba[rot - 1] = t; }
+        for (int c = 0; c < 4; ++c) out[4 * i + c] = (uint8_t)rgba[c];
+    }
+    return r.pos;
+}
+
+/* Decodes a (w x h)-texel BC7 image (blocks row-major) to RGBA8. */
+void oracle_bc7_decode_image(const uint8_t *blocks, int w, int h, uint8_t *rgba)
+{
+    int bw = w / 4, bh = h / 4;
+    uint8_t tex[64];
+    for (int by = 0; by < bh; ++by)
+        for (int bx = 0; bx < bw; ++bx) {
+            oracle_bc7_decode_block(blocks + 16 * (by * bw + bx), tex);
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c)
+                    memcpy(rgba + 4 * ((by * 4 + r) * w + bx * 4 + c), tex + 4 * (4 * r + c), 4);
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* Feature fetch and sampling (readings R1, R2, R4, R5, R8).    */
+/* ------------------------------------------------------------------ */
+
+/* A 2D feature map of rx x ry texels with nc channels, stored in fmt.
+ * BC7 maps are always 4 channels (RGBA).                               */
+typedef struct { const uint8_t *base; int fmt, rx, ry, nc; } map2d;
+
+/* Dequantised texel value (R8: q/255 for BC7 and U8; the stored value for
+ * F16).  BC7: the whole block is decoded for every fetch.             */
+static double fetch(const map2d *m, int a, int b, int c)
+{
+    if (m->fmt == OR_FMT_BC7) {
+        uint8_t tex[64];
+        const uint8_t *blk = m->base + 16 * ((b / 4) * (m->rx / 4) + (a / 4));
+        oracle_bc7_decode_block(blk, tex);
+        return tex[4 * (4 * (b % 4) + (a % 4)) + c] / 255.0;
+    }
+    size_t k = ((size_t)b * m->rx + a) * m->nc + c;
+    if (m->fmt == OR_FMT_U8) return m->base[k] / 255.0;
+    uint16_t h;
+    memcpy(&h, m->base + 2 * k, 2);
+    return oracle_half_to_double(h);
+}
+
+static int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+/* Bilinear sample at normalised coordinates (a, b): texel centres at
+ * (i+0.5)/R, clamp-to-edge addressing (R1).                            */
+static void bilinear(const map2d *m, double a, double b, double *out)
+{
+    double sx = a * m->rx - 0.5, sy = b * m->ry - 0.5;
+    double fx0 = floor(sx), fy0 = floor(sy);
+    double fx = sx - fx0, fy = sy - fy0;
+    int x0 = clampi((int)fx0, 0, m->rx - 1), x1 = clampi((int)fx0 + 1, 0, m->rx - 1);
+    int y0 = clampi((int)fy0, 0, m->ry - 1), y1 = clampi((int)fy0 + 1, 0, m->ry - 1);
+    for (int c = 0; c < m->nc; ++c)
+        out[c] = (1 - fx) * (1 - fy) * fetch(m, x0, y0, c) + fx * (1 - fy) * fetch(m, x1, y0, c)
+               + (1 - fx) * fy * fetch(m, x0, y1, c) + fx * fy * fetch(m, x1, y1, c);
+}
+
+/* exported for the sampler pins: one 2D map without tile offsets */
+void oracle_sample2d(const uint8_t *base, int fmt, int rx, int ry, int nc, double a, double b, double *out)
+{
+    map2d m = {base, fmt, rx, ry, nc};
+    bilinear(&m, a, b, out);
+}
+
+static size_t bytes_2d(int fmt, int rx, int ry, int nc)
+{
+    if (fmt == OR_FMT_BC7) return (size_t)(rx / 4) * (ry / 4) * 16;
+    return (size_t)rx * ry * nc * (fmt == OR_FMT_U8 ? 1 : 2);
+}
+
+size_t oracle_tile_bytes_uv(const oracle_layout *L)  { return bytes_2d(L->fmt_uv, L->uv_res, L->uv_res, 4); }
+size_t oracle_tile_bytes_uvt(const oracle_layout *L) { return (size_t)L->uvt_depth * bytes_2d(L->fmt_uvt, L->uvt_res, L->uvt_res, 4); }
+size_t oracle_tile_bytes_line(const oracle_layout *L){ return bytes_2d(L->fmt_line, L->line_res, L->line_t, 2); }
+size_t oracle_mlp_params(int h) { return (size_t)16 * h + h + (size_t)h * h + h + 3 * (size_t)h + 3; }
+
+/* Trilinear sample of the D-deep volume (R4): s = t*D - 0.5, texel-centre
+ * convention along depth, clamp, then bilinear in each slice.          */
+static void trilinear_uvt(const oracle_layout *L, const uint8_t *vol, double u, double v, double t, double *out)
+{
+    size_t slice = bytes_2d(L->fmt_uvt, L->uvt_res, L->uvt_res, 4);
+    double s = t * L->uvt_depth - 0.5;
+    double k0d = floor(s), tau = s - k0d;
+    int k0 = clampi((int)k0d, 0, L->uvt_depth - 1), k1 = clampi((int)k0d + 1, 0, L->uvt_depth - 1);
+    map2d m0 = {vol + slice * k0, L->fmt_uvt, L->uvt_res, L->uvt_res, 4};
+    map2d m1 = {vol + slice * k1, L->fmt_uvt, L->uvt_res, L->uvt_res, 4};
+    double a[4], b[4];
+    bilinear(&m0, u, v, a);
+    bilinear(&m1, u, v, b);
+    for (int c = 0; c < 4; ++c) out[c] = (1 - tau) * a[c] + tau * b[c];
+}
+
+void oracle_sample_uvt(const oracle_layout *L, const uint8_t *vol, double u, double v, double t, double *out)
+{
+    trilinear_uvt(L, vol, u, v, t, out);
+}
+
+/* gamma(t) = [sin(2^0 pi t), cos(2^0 pi t), sin(2^1 pi t), cos(2^1 pi t)]  (Eq. 4) */
+void oracle_gamma(double t, double g[4])
+{
+    g[0] = sin(M_PI * t);
+    g[1] = cos(M_PI * t);
+    g[2] = sin(2.0 * M_PI * t);
+    g[3] = cos(2.0 * M_PI * t);
+}
+
+/* Eq. 4 input vector x = [V_uvt, V_uv, V_ut, V_vt, gamma(t)] (R6) for
+ * tile k at normalised (u, v) and time t.                              */
+void oracle_features(const oracle_layout *L, const oracle_maps *M, int k, double u, double v, double t, double x[16])
+{
+    map2d uv = {M->uv + oracle_tile_bytes_uv(L) * k, L->fmt_uv, L->uv_res, L->uv_res, 4};
+    map2d ut = {M->ut + oracle_tile_bytes_line(L) * k, L->fmt_line, L->line_res, L->line_t, 2};
+    map2d vt = {M->vt + oracle_tile_bytes_line(L) * k, L->fmt_line, L->line_res, L->line_t, 2};
+    trilinear_uvt(L, M->uvt + oracle_tile_bytes_uvt(L) * k, u, v, t, x + 0);   /* V_uvt */
+    bilinear(&uv, u, v, x + 4);                                                  /* V_uv  */
+    bilinear(&ut, u, t, x + 8);                                                  /* V_ut: axes (u, t) */
+    bilinear(&vt, v, t, x + 10);                                                 /* V_vt: axes (v, t) */
+    oracle_gamma(t, x + 12);
+}
+
+/* ------------------------------------------------------------------ */
+/* Decoder MLP G_Phi: 16 -> h -> h -> 3, GELU on hidden layers, linear
+ * output.  Weights f16, PyTorch [out][in] order (R11).         */
+/* ------------------------------------------------------------------ */
+double oracle_gelu(double z, int variant)
+{
+    if (variant == OR_GELU_TANH)
+        return 0.5 * z * (1.0 + tanh(sqrt(2.0 / M_PI) * (z + 0.044715 * z * z * z)));
+    return 0.5 * z * (1.0 + erf(z / sqrt(2.0)));
+}
+
+static void linear(const uint16_t *W, const uint16_t *b, int nout, int nin, const double *in, double *out)
+{
+    for (int o = 0; o < nout; ++o) {
+        double acc = oracle_half_to_double(b[o]);
+        for (int i = 0; i < nin; ++i) acc += oracle_half_to_double(W[o * nin + i]) * in[i];
+        out[o] = acc;
+    }
+}
+
+void oracle_mlp(int h, const uint16_t *w, const double x[16], int gelu, double y[3])
+{
+    double h1[256], h2[256];
+    const uint16_t *W1 = w, *b1 = W1 + 16 * h, *W2 = b1 + h, *b2 = W2 + h * h, *W3 = b2 + h, *b3 = W3 + 3 * h;
+    linear(W1, b1, h, 16, x, h1);
+    for (int i = 0; i < h; ++i) h1[i] = oracle_gelu(h1[i], gelu);
+    linear(W2, b2, h, h, h1, h2);
+    for (int i = 0; i < h; ++i) h2[i] = oracle_gelu(h2[i], gelu);
+    linear(W3, b3, 3, h, h2, y);
+}
+
+/* ------------------------------------------------------------------ */
+/* Tile decode (readings R2, R3, R12, R16).               */
+/* ------------------------------------------------------------------ */
+
+/* mirror a core coordinate without repeating the edge (R3) */
+static int mirror(int i, int C)
+{
+    if (i < 0) i = -i;
+    if (i >= C) i = 2 * (C - 1) - i;
+    return i;
+}
+
+/* I(u,v,t) for padded texel (x, y) of tile k -> y3 (fp64, pre-clamp) */
+void oracle_texel(const oracle_layout *L, const oracle_maps *M, int k, int x, int y, double t, double out[3])
+{
+    int C = L->core, i = x - L->border, j = y - L->border;
+    if (L->border_mode == OR_BORDER_MIRROR) { i = mirror(i, C); j = mirror(j, C); }
+    double u = (i + 0.5) / C, v = (j + 0.5) / C;
+    double feat[16];
+    oracle_features(L, M, k, u, v, t, feat);
+    oracle_mlp(L->hidden, M->mlp + oracle_mlp_params(L->hidden) * k, feat, L->gelu, out);
+}
+
+typedef struct {
+    const oracle_layout *L; const oracle_maps *M; const uint32_t *ids; uint32_t n; double t;
+    double *out; int full; int next_row; pthread_mutex_t *mu;
+} job;
+
+static void do_row(job *J, int row)
+{
+    const oracle_layout *L = J->L;
+    int C = L->core, P = C + 2 * L->border;
+    if (!J->full) {
+        int r = row / P, y = row % P;
+        int k = (int)J->ids[r];
+        for (int x = 0; x < P; ++x)
+            oracle_texel(L, J->M, k, x, y, J->t, J->out + 3 * (((size_t)r * P + y) * P + x));
+    } else {
+        /* decode_full: core texels only, atlas placement
+         * tile id k = (a*tiles_y + ty)*tiles_x + tx                        */
+        int k = row / C, j = row % C;
+        int tx = k % L->tiles_x, ty = (k / L->tiles_x) % L->tiles_y, a = k / (L->tiles_x * L->tiles_y);
+        size_t W = (size_t)L->tiles_x * C, Hh = (size_t)L->tiles_y * C;
+        for (int i = 0; i < C; ++i)
+            oracle_texel(L, J->M, k, i + L->border, j + L->border, J->t,
+                         J->out + 3 * ((size_t)a * Hh * W + ((size_t)ty * C + j) * W + (size_t)tx * C + i));
+    }
+}
+
+static void *worker(void *arg)
+{
+    job *J = (job *)arg;
+    int C = J->L->core, P = C + 2 * J->L->border;
+    int rows = J->full ? J->L->num_tiles * C : (int)J->n * P;
+    for (;;) {
+        pthread_mutex_lock(J->mu);
+        int row = J->next_row++;
+        pthread_mutex_unlock(J->mu);
+        if (row >= rows) break;
+        do_row(J, row);
+    }
+    return NULL;
+}
+
+static int run(job *J, int nthreads)
+{
+    pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
+    J->mu = &mu;
+    J->next_row = 0;
+    if (nthreads <= 1) { worker(J); return 0; }
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * nthreads);
+    for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, worker, J);
+    for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+    free(th);
+    return 0;
+}
+
+static int check_ids(const oracle_layout *L, const uint32_t *ids, uint32_t n)
+{
+    for (uint32_t r = 0; r < n; ++r) if (ids[r] >= (uint32_t)L->num_tiles) return -1;
+    return 0;
+}
+
+/* y_out: [n][P][P][3] fp64 (padded tile, mirrored border) */
+int oracle_decode_tiles(const oracle_layout *L, const oracle_maps *M, const uint32_t *ids, uint32_t n,
+                        double t, double *y_out, int nthreads)
+{
+    if (check_ids(L, ids, n)) return -1;
+    job J = {L, M, ids, n, t, y_out, 0, 0, NULL};
+    return run(&J, nthreads);
+}
+
+/* y_out: [atlases][tiles_y*C][tiles_x*C][3] fp64 (core texels only) */
+int oracle_decode_full(const oracle_layout *L, const oracle_maps *M, double t, double *y_out, int nthreads)
+{
+    job J = {L, M, NULL, 0, t, y_out, 1, 0, NULL};
+    return run(&J, nthreads);
+}
+
+/* Output quantisation to RGBA8 (R12): RN-even(clamp(y,0,1)*255), A = 255.
+ * Two precisions so that the decision is taken in the precision of the
+ * y being quantised (fp64 oracle y, or a kernel's fp32 y).             */
+void oracle_quantize_rgba8_f64(const double *y3, size_t n, uint8_t *out)
+{
+    for (size_t i = 0; i < n; ++i) {
+        for (int c = 0; c < 3; ++c) {
+            double v = y3[3 * i + c];
+            v = fmin(fmax(v, 0.0), 1.0);   /* NaN -> 0, as fmaxf does */
+            out[4 * i + c] = (uint8_t)nearbyint(v * 255.0);
+        }
+        out[4 * i + 3] = 255;
+    }
+}
+
+void oracle_quantize_rgba8_f32(const float *y, size_t stride, size_t n, uint8_t *out)
+{
+    for (size_t i = 0; i < n; ++i) {
+        for (int c = 0; c < 3; ++c) {
+            float v = y[stride * i + c];
+            v = fminf(fmaxf(v, 0.0f), 1.0f);
+            out[4 * i + c] = (uint8_t)nearbyintf(v * 255.0f);
+        }
+        out[4 * i + 3] = 255;
+    }
+}
