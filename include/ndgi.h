@@ -1,0 +1,231 @@
+/*
+ * ndgi.h -- C ABI of the B200-native NDGI tile decoder (libndgi.so).
+ *
+ * Operation (Neural Dynamic GI, arXiv 2604.12625; "P:n" = PAPER.md line n):
+ *   I(u, v, t) = H_Theta(u, v, t)                                  Eq. 3
+ *   I(u, v, t) = G_Phi(V_uvt, V_uv, V_ut, V_vt, gamma(t)),
+ *   gamma(t)   = [sin(pi t), cos(pi t), sin(2 pi t), cos(2 pi t)]  Eq. 4
+ *   Theta = {F3D_uvt, F2D_uv, F2D_ut, F2D_vt, Phi}, one per tile   Eq. 5
+ * F_uv and every t-slice of F_uvt are BC7; F_ut/F_vt are 8-bit;
+ * G_Phi is 16 -> h -> h -> 3 with GELU on the hidden layers (Table 3).
+ * The decoded tiles are written into a virtual-texturing page cache as
+ * 8-bit RGBA with a mirrored border.
+ * Every reading the paper leaves open (R1..R20) is listed in DESIGN.md.
+ *
+ * Conventions
+ * -----------
+ * - Every call returns an ndgi_status; nothing aborts or throws.
+ * - Pointers documented "device" are CUDA device pointers on the context's
+ *   device; "host" pointers are CPU memory.  Input buffers are BORROWED: the
+ *   caller keeps them alive (and unchanged) for the context's lifetime.
+ * - Decode calls are stream-ordered and asynchronous on the given
+ *   cudaStream_t (passed as void*; NULL = legacy default stream) unless
+ *   documented otherwise.  They never synchronise.
+ * - Outputs are bit-deterministic for identical inputs (no data atomics).
+ * - Host-detectable argument errors are reported synchronously; a tile id
+ *   >= num_tiles or a slot >= num_slots is detected on the device: that
+ *   request is skipped and the context's error counter is incremented
+ *   (read it with ndgi_device_error).
+ * - Thread safety: one context may be used from several host threads on
+ *   different streams; the context is read-only after ndgi_load except for
+ *   its device error counter.
+ */
+#ifndef NDGI_H
+#define NDGI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NDGI_ABI_VERSION 1u
+
+#if defined(__GNUC__)
+#define NDGI_API __attribute__((visibility("default")))
+#else
+#define NDGI_API
+#endif
+
+typedef struct ndgi_ctx ndgi_ctx; /* opaque; one per device */
+
+typedef enum {
+    NDGI_OK = 0,
+    NDGI_ERR_ARG = 1,         /* null pointer, malformed layout, bad enum       */
+    NDGI_ERR_RANGE = 2,       /* t not finite or outside [0,1]; n too large     */
+    NDGI_ERR_UNSUPPORTED = 3, /* valid layout the chosen mode does not support  */
+    NDGI_ERR_CUDA = 4,        /* CUDA runtime error; see ndgi_last_error        */
+    NDGI_ERR_NOMEM = 5,       /* device or host allocation failed               */
+    NDGI_ERR_DEVICE = 6       /* device is not an sm_100 part / not present     */
+} ndgi_status;
+
+/* storage format of a feature map (reading R8) */
+typedef enum {
+    NDGI_FMT_BC7 = 0, /* 16-byte BC7 blocks, UNORM, value = q/255            */
+    NDGI_FMT_U8 = 1,  /* raw 8-bit texels, value = q/255                     */
+    NDGI_FMT_F16 = 2  /* IEEE binary16 texels, value as stored               */
+} ndgi_feat_fmt;
+
+/* page-cache texel format (reading R12) */
+typedef enum {
+    NDGI_OUT_RGBA8 = 0,   /* RN-even(clamp(y,0,1)*255), A = 255 (4 B/texel)  */
+    NDGI_OUT_RGBA16F = 1, /* (fp16(y), 1.0)                       (8 B/texel)  */
+    NDGI_OUT_RGBA32F = 2  /* (y, 1.0)                            (16 B/texel) */
+} ndgi_out_fmt;
+
+typedef enum { NDGI_GELU_ERF = 0, NDGI_GELU_TANH = 1 } ndgi_gelu;           /* R7 */
+typedef enum { NDGI_BORDER_MIRROR = 0, NDGI_BORDER_EVAL_CLAMP = 1 } ndgi_border; /* R3 */
+
+typedef enum {
+    /* fused tensor-core kernel: BC7 -> smem, fp16 MMA operands (tcgen05, fp32
+     * accumulation in TMEM), tanh-form GELU.  Parity bar vs the fp64 oracle:
+     * max-abs <= 2e-2, mean-abs <= 2e-3 (BASELINE.json north_star).          */
+    NDGI_MODE_FAST = 0,
+    /* scalar fp32 reference kernel, accurate erff/tanhf GELU per layout.gelu;
+     * parity bar: max-abs <= 1e-5.                                            */
+    NDGI_MODE_REF_FP32 = 1
+} ndgi_mode;
+
+/*
+ * Layout of every tile's Theta (the "BC layout" of ndgi_load).
+ * C = core, B = border, P = C + 2B (padded tile side).
+ * Tile id k <-> atlas placement for decode_full:
+ *   k = (a * tiles_y + ty) * tiles_x + tx,  num_tiles = atlases*tiles_y*tiles_x.
+ * Constraints (NDGI_ERR_ARG otherwise): abi_version == NDGI_ABI_VERSION;
+ *   num_tiles >= 1; core >= 4, core % 4 == 0; border < core;
+ *   BC7 maps need resolutions that are multiples of 4; all resolutions >= 1;
+ *   uvt_depth, line_t >= 1; 1 <= hidden <= 256; fmt_line is U8 or F16.
+ * NDGI_MODE_FAST additionally needs (NDGI_ERR_UNSUPPORTED otherwise):
+ *   core in {128, 256}, uv_res == core (R2), hidden in {16, 64}
+ *   (Table 3), border_mode == MIRROR, uvt_res <= 64, line_res <= 256.
+ */
+typedef struct ndgi_layout {
+    uint32_t abi_version;            /* = NDGI_ABI_VERSION                     */
+    uint32_t num_tiles;
+    uint32_t atlases, tiles_x, tiles_y;
+    uint32_t core;                   /* C: core texels per tile side (128)     */
+    uint32_t border;                 /* B: border texels per edge (4)          */
+    uint32_t uv_res;                 /* R_uv: F_uv side (= C, R2)              */
+    uint32_t uvt_res;                /* R3: F_uvt side (16/32/64, Table 3)     */
+    uint32_t uvt_depth;              /* D: F_uvt slices along t (12, Table 1)  */
+    uint32_t line_res;               /* U: spatial texels of F_ut/F_vt (64)    */
+    uint32_t line_t;                 /* T: temporal rows of F_ut/F_vt (24)     */
+    uint32_t hidden;                 /* h: MLP width (16 or 64, Table 3)       */
+    uint32_t fmt_uv, fmt_uvt, fmt_line; /* ndgi_feat_fmt                       */
+    uint32_t gelu;                   /* ndgi_gelu                              */
+    uint32_t border_mode;            /* ndgi_border                            */
+} ndgi_layout;
+
+/*
+ * Theta buffers, DEVICE pointers, dense, tile-major (tile k's data at
+ * k * per_tile_bytes), borrowed for the context's lifetime:
+ *   uv : BC7 [tile][R_uv/4][R_uv/4][16 B]  |  U8/F16 [tile][R_uv][R_uv][4]
+ *   uvt: BC7 [tile][D][R3/4][R3/4][16 B]   |  U8/F16 [tile][D][R3][R3][4]
+ *   ut, vt: [tile][T][U][2] (U8 or F16; row = time, reading R5)
+ *   mlp: [tile][W1 h*16 | b1 h | W2 h*h | b2 h | W3 3*h | b3 3] binary16,
+ *        PyTorch [out][in] order (R11)
+ * BC7 block (bx, by) of a map is at (by * (R/4) + bx) * 16; texel (x, y) of a
+ * block is texel 4*y + x of the BC7 block.  All pointers 16-byte aligned.
+ */
+typedef struct ndgi_params {
+    const void* uv;
+    const void* uvt;
+    const void* ut;
+    const void* vt;
+    const uint16_t* mlp;
+} ndgi_params;
+
+/*
+ * Creates a context on CUDA device `device` for the given layout and Theta.
+ * Validates the layout (synchronously), queries the device (must be an
+ * sm_100 part for decode), repacks nothing from Theta (zero-copy), uploads
+ * the small per-context state and synchronises once.  *out is set only on
+ * NDGI_OK.  Errors: ARG (null/invalid layout), DEVICE, CUDA, NOMEM.
+ */
+NDGI_API ndgi_status ndgi_load(const ndgi_layout* layout, const ndgi_params* params, int device, ndgi_ctx** out);
+
+/*
+ * Decodes n requested tiles at time t into the page cache.
+ *   tile_ids : DEVICE u32[n], tile id per request
+ *   slots    : DEVICE u32[n], destination slot per request, or NULL (slot = i)
+ *   out_cache: DEVICE [num_slots][P][P][texel], texel per `fmt`; slot s holds
+ *              the padded tile, core at rows/cols [B, B+C), border = mirror
+ *              of the core (R3).  Written texels: n * P * P.
+ * Errors (synchronous): ARG (null ctx/tile_ids/out_cache, bad enum, n == 0),
+ *   RANGE (t not finite or outside [0,1]; n > 2^24), UNSUPPORTED (mode/layout),
+ *   CUDA (launch failure).  Invalid ids/slots: device error counter.
+ */
+NDGI_API ndgi_status ndgi_decode_tiles(ndgi_ctx* ctx, const uint32_t* tile_ids, const uint32_t* slots, uint32_t n,
+                              uint32_t num_slots, float t, void* out_cache, ndgi_out_fmt fmt, ndgi_mode mode,
+                              void* stream);
+
+/*
+ * Decodes every tile's core at time t into atlas images:
+ *   out: DEVICE [atlases][tiles_y*C][tiles_x*C][texel]; tile k's core texel
+ *        (i, j) lands at row ty*C + j, column tx*C + i of atlas a.
+ * Written texels: num_tiles * C * C.  Errors as ndgi_decode_tiles.
+ */
+NDGI_API ndgi_status ndgi_decode_full(ndgi_ctx* ctx, float t, void* out, ndgi_out_fmt fmt, ndgi_mode mode, void* stream);
+
+/*
+ * Batched ndgi_decode_full over n_t query times t[0..n_t) (HOST array of
+ * floats, read during the call): out receives n_t consecutive atlas sets
+ * (n_t * num_tiles * C * C texels).  One launch per 32 times, so small
+ * lightmaps and many times still fill the GPU.  Errors as ndgi_decode_tiles.
+ */
+NDGI_API ndgi_status ndgi_decode_full_batch(ndgi_ctx* ctx, const float* t, uint32_t n_t, void* out, ndgi_out_fmt fmt,
+                                   ndgi_mode mode, void* stream);
+
+/*
+ * Host-buffer variant of ndgi_decode_full for end-to-end use: decodes the
+ * n_t times t[0..n_t) (HOST array) into out_host (HOST memory, ideally
+ * pinned), n_t consecutive atlas images.  Device staging buffers are owned by
+ * the context; decode of time i+1 overlaps the device->host copy of time i.
+ * SYNCHRONOUS: returns when out_host holds every result.
+ */
+NDGI_API ndgi_status ndgi_decode_full_host(ndgi_ctx* ctx, const float* t, uint32_t n_t, void* out_host, ndgi_out_fmt fmt,
+                                  ndgi_mode mode);
+
+/* Written-texel and byte sizes helpers (host, no CUDA). */
+NDGI_API uint64_t ndgi_full_texels(const ndgi_layout* layout);
+NDGI_API size_t ndgi_texel_bytes(ndgi_out_fmt fmt);
+
+/*
+ * Synchronises the context's device and returns the number of rejected
+ * requests (bad tile id or slot) since load or the last reset; resets the
+ * counter when `reset` != 0.
+ */
+NDGI_API ndgi_status ndgi_device_error(ndgi_ctx* ctx, uint32_t* bad_requests, int reset);
+
+NDGI_API const char* ndgi_status_string(ndgi_status s);
+/* detail of the last failing call on this host thread ("" if none) */
+NDGI_API const char* ndgi_last_error(void);
+NDGI_API ndgi_status ndgi_free(ndgi_ctx* ctx);
+
+/* Validates a layout without touching CUDA (same rules as ndgi_load; FAST-mode
+ * support reported through *fast_supported if non-NULL). */
+NDGI_API ndgi_status ndgi_validate_layout(const ndgi_layout* layout, int* fast_supported);
+
+/* ---------------- test hooks (not the product path) ---------------- */
+
+/* Bit-exact BC7 map decode: blocks (DEVICE, (w/4)*(h/4) blocks row-major) ->
+ * rgba (DEVICE, [h][w][4] u8).  w, h multiples of 4.  Same device decoder as
+ * the fused kernel. */
+NDGI_API ndgi_status ndgi_debug_bc7_decode(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, void* stream);
+
+/* Same map decoded by the GPU texture unit (cudaArray of BC7 with
+ * cudaChannelFormatKindUnsignedBlockCompressed7, point sampling): an
+ * independent hardware decoder for the cross-check.  Synchronous. */
+NDGI_API ndgi_status ndgi_debug_bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
+
+/* GELU-rate microbenchmark for the ALU roofline: runs the fused kernel's
+ * GELU formulation (f16x2, tanh.approx) on `iters` x (grid*256*8) pairs and
+ * returns the elapsed device milliseconds and activations evaluated.
+ * Synchronous. */
+NDGI_API ndgi_status ndgi_debug_gelu_rate(uint32_t iters, float* ms, double* activations);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NDGI_H */

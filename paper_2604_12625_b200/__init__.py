@@ -1,0 +1,231 @@
+"""Python binding of libndgi.so -- the B200-native NDGI tile decoder.
+
+Argument marshalling only: every step of the decode runs in the CUDA kernels
+behind the C ABI declared in ``include/ndgi.h`` (functions of the same names
+below).  PyTorch is used only to hold device memory and streams.  There is no
+CPU fallback: importing this package without the built library raises.
+
+    import paper_2604_12625_b200 as ndgi
+    ctx = ndgi.ndgi_load(layout_dict, theta_tensors_on_cuda, device=0)
+    ndgi.ndgi_decode_tiles(ctx, ids, None, n, num_slots, t, out_cache)
+    ndgi.ndgi_decode_full(ctx, t, out)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libndgi.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python paper_2604_12625_b200/build.py` "
+        "(or __graft_entry__.build()); there is no fallback implementation")
+
+_lib = C.CDLL(LIB_PATH)
+
+ABI_VERSION = 1
+OK, ERR_ARG, ERR_RANGE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NOMEM, ERR_DEVICE = range(7)
+FMT = {"bc7": 0, "u8": 1, "f16": 2}
+OUT = {"rgba8": 0, "rgba16f": 1, "rgba32f": 2}
+GELU = {"erf": 0, "tanh": 1}
+BORDER = {"mirror": 0, "eval_clamp": 1}
+MODE = {"fast": 0, "ref_fp32": 1}
+TEXEL_BYTES = {"rgba8": 4, "rgba16f": 8, "rgba32f": 16}
+
+
+class ndgi_layout(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in (
+        "abi_version", "num_tiles", "atlases", "tiles_x", "tiles_y", "core", "border", "uv_res",
+        "uvt_res", "uvt_depth", "line_res", "line_t", "hidden", "fmt_uv", "fmt_uvt", "fmt_line",
+        "gelu", "border_mode")]
+
+
+class ndgi_params(C.Structure):
+    _fields_ = [("uv", C.c_void_p), ("uvt", C.c_void_p), ("ut", C.c_void_p), ("vt", C.c_void_p),
+                ("mlp", C.c_void_p)]
+
+
+_P, _U32, _I, _F = C.c_void_p, C.c_uint32, C.c_int, C.c_float
+_SIGS = {
+    "ndgi_load": (_I, [C.POINTER(ndgi_layout), C.POINTER(ndgi_params), _I, C.POINTER(C.c_void_p)]),
+    "ndgi_decode_tiles": (_I, [_P, _P, _P, _U32, _U32, _F, _P, _I, _I, _P]),
+    "ndgi_decode_full": (_I, [_P, _F, _P, _I, _I, _P]),
+    "ndgi_decode_full_batch": (_I, [_P, C.POINTER(_F), _U32, _P, _I, _I, _P]),
+    "ndgi_decode_full_host": (_I, [_P, C.POINTER(_F), _U32, _P, _I, _I]),
+    "ndgi_full_texels": (C.c_uint64, [C.POINTER(ndgi_layout)]),
+    "ndgi_texel_bytes": (C.c_size_t, [_I]),
+    "ndgi_device_error": (_I, [_P, C.POINTER(_U32), _I]),
+    "ndgi_status_string": (C.c_char_p, [_I]),
+    "ndgi_last_error": (C.c_char_p, []),
+    "ndgi_free": (_I, [_P]),
+    "ndgi_validate_layout": (_I, [C.POINTER(ndgi_layout), C.POINTER(_I)]),
+    "ndgi_debug_bc7_decode": (_I, [_P, _U32, _U32, _P, _P]),
+    "ndgi_debug_bc7_decode_hw": (_I, [_P, _U32, _U32, _P]),
+    "ndgi_debug_gelu_rate": (_I, [_U32, C.POINTER(_F), C.POINTER(C.c_double)]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class NdgiError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.ndgi_status_string(status).decode()
+        detail = _lib.ndgi_last_error().decode()
+        super().__init__(f"{where}: {msg}" + (f" ({detail})" if detail else ""))
+
+
+def _check(status: int, where: str) -> None:
+    if status != OK:
+        raise NdgiError(status, where)
+
+
+def make_layout(lay: dict) -> ndgi_layout:
+    """dict (ndgi_synth.layout keys) -> ndgi_layout."""
+    return ndgi_layout(
+        ABI_VERSION, lay["num_tiles"], lay["atlases"], lay["tiles_x"], lay["tiles_y"], lay["core"],
+        lay["border"], lay["uv_res"], lay["uvt_res"], lay["uvt_depth"], lay["line_res"], lay["line_t"],
+        lay["hidden"], FMT[lay["fmt_uv"]], FMT[lay["fmt_uvt"]], FMT[lay["fmt_line"]], GELU[lay["gelu"]],
+        BORDER[lay["border_mode"]])
+
+
+def ndgi_validate_layout(lay) -> tuple[int, bool]:
+    L = lay if isinstance(lay, ndgi_layout) else make_layout(lay)
+    fast = C.c_int(0)
+    st = _lib.ndgi_validate_layout(C.byref(L), C.byref(fast))
+    return st, bool(fast.value)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Context:
+    """An ndgi_ctx plus references to the (borrowed) Theta tensors."""
+
+    def __init__(self, handle: C.c_void_p, lay: dict, theta: dict, device: int):
+        self.handle = handle
+        self.lay = dict(lay)
+        self.theta = theta      # keeps the borrowed device buffers alive
+        self.device = device
+        self.layout = make_layout(lay)
+
+    @property
+    def padded(self) -> int:
+        return self.lay["core"] + 2 * self.lay["border"]
+
+    def full_texels(self) -> int:
+        return int(_lib.ndgi_full_texels(C.byref(self.layout)))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.ndgi_free(self.handle)
+            self.handle = None
+
+
+def ndgi_load(lay: dict, theta: dict, device: int = 0) -> Context:
+    """theta: dict of CUDA tensors uv, uvt, ut, vt (uint8/float16) and mlp (int16/uint16 f16 bits)."""
+    for k in ("uv", "uvt", "ut", "vt", "mlp"):
+        t = theta[k]
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"theta[{k!r}] must be a contiguous CUDA tensor")
+    L = make_layout(lay)
+    P = ndgi_params(*(theta[k].data_ptr() for k in ("uv", "uvt", "ut", "vt", "mlp")))
+    h = C.c_void_p()
+    _check(_lib.ndgi_load(C.byref(L), C.byref(P), int(device), C.byref(h)), "ndgi_load")
+    return Context(h, lay, theta, device)
+
+
+def ndgi_decode_tiles(ctx: Context, tile_ids, slots, n: int, num_slots: int, t: float, out_cache,
+                      fmt: str = "rgba8", mode: str = "fast", stream=None) -> None:
+    """tile_ids/slots: CUDA int32/uint32 tensors (slots may be None); out_cache: CUDA tensor."""
+    st = _lib.ndgi_decode_tiles(ctx.handle, C.c_void_p(tile_ids.data_ptr()),
+                                C.c_void_p(slots.data_ptr()) if slots is not None else None,
+                                int(n), int(num_slots), float(t), C.c_void_p(out_cache.data_ptr()),
+                                OUT[fmt], MODE[mode], _stream_ptr(stream))
+    _check(st, "ndgi_decode_tiles")
+
+
+def ndgi_decode_full(ctx: Context, t: float, out, fmt: str = "rgba8", mode: str = "fast", stream=None) -> None:
+    st = _lib.ndgi_decode_full(ctx.handle, float(t), C.c_void_p(out.data_ptr()), OUT[fmt], MODE[mode],
+                               _stream_ptr(stream))
+    _check(st, "ndgi_decode_full")
+
+
+def ndgi_decode_full_batch(ctx: Context, ts, out, fmt: str = "rgba8", mode: str = "fast", stream=None) -> None:
+    arr = (C.c_float * len(ts))(*[float(x) for x in ts])
+    st = _lib.ndgi_decode_full_batch(ctx.handle, arr, len(ts), C.c_void_p(out.data_ptr()), OUT[fmt],
+                                     MODE[mode], _stream_ptr(stream))
+    _check(st, "ndgi_decode_full_batch")
+
+
+def ndgi_decode_full_host(ctx: Context, ts, out_host, fmt: str = "rgba8", mode: str = "fast") -> None:
+    """out_host: CPU tensor (pinned for overlap) of n_t * full_texels texels."""
+    arr = (C.c_float * len(ts))(*[float(x) for x in ts])
+    st = _lib.ndgi_decode_full_host(ctx.handle, arr, len(ts), C.c_void_p(out_host.data_ptr()), OUT[fmt],
+                                    MODE[mode])
+    _check(st, "ndgi_decode_full_host")
+
+
+def ndgi_device_error(ctx: Context, reset: bool = False) -> int:
+    v = C.c_uint32(0)
+    _check(_lib.ndgi_device_error(ctx.handle, C.byref(v), int(reset)), "ndgi_device_error")
+    return int(v.value)
+
+
+def ndgi_free(ctx: Context) -> None:
+    if ctx.handle:
+        _check(_lib.ndgi_free(ctx.handle), "ndgi_free")
+        ctx.handle = None
+
+
+def ndgi_status_string(status: int) -> str:
+    return _lib.ndgi_status_string(status).decode()
+
+
+def ndgi_debug_bc7_decode(blocks, w: int, h: int, rgba, stream=None) -> None:
+    _check(_lib.ndgi_debug_bc7_decode(C.c_void_p(blocks.data_ptr()), w, h, C.c_void_p(rgba.data_ptr()),
+                                      _stream_ptr(stream)), "ndgi_debug_bc7_decode")
+
+
+def ndgi_debug_bc7_decode_hw(blocks, w: int, h: int, rgba) -> None:
+    _check(_lib.ndgi_debug_bc7_decode_hw(C.c_void_p(blocks.data_ptr()), w, h, C.c_void_p(rgba.data_ptr())),
+           "ndgi_debug_bc7_decode_hw")
+
+
+def ndgi_debug_gelu_rate(iters: int = 4096) -> tuple[float, float]:
+    """-> (milliseconds, activations) of the f16x2 GELU microbenchmark."""
+    ms, acts = C.c_float(0), C.c_double(0)
+    _check(_lib.ndgi_debug_gelu_rate(iters, C.byref(ms), C.byref(acts)), "ndgi_debug_gelu_rate")
+    return float(ms.value), float(acts.value)
+
+
+def raw_call(name: str, *args) -> int:
+    """Direct C call for contract tests (status codes instead of exceptions)."""
+    return getattr(_lib, name)(*args)
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def upload_theta(theta: dict, device: int = 0) -> dict:
+    """numpy Theta (ndgi_synth.make_theta) -> contiguous CUDA tensors (plumbing only)."""
+    import numpy as np
+    import torch
+    out = {}
+    for k, v in theta.items():
+        a = np.ascontiguousarray(v)
+        if a.dtype == np.uint16:
+            a = a.view(np.int16)
+        out[k] = torch.from_numpy(a).to(f"cuda:{device}")
+    return out

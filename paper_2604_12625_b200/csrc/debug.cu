@@ -1,0 +1,111 @@
+// debug.cu -- test hooks of libndgi.so (not the product path):
+//  * BC7 map decode with the fused kernel's device decoder (bit-exact check);
+//  * the same map through the B200 texture unit (independent hardware decoder);
+//  * a GELU-rate microbenchmark of the fused kernel's f16x2 GELU, which is the
+//    measured denominator of the ALU roofline (T_alu).
+#include <cuda_runtime.h>
+
+#include "bc7_device.cuh"
+#include "ndgi_common.cuh"
+
+namespace ndgi {
+
+// one thread per block; texel (x, y) of block (bx, by) -> rgba[(4by+y)*w + 4bx+x]
+__global__ void bc7_map_kernel(const uint4* __restrict__ blocks, uint32_t bw, uint32_t bh, uint32_t* __restrict__ rgba) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= bw * bh) return;
+    const uint32_t bx = b % bw, by = b / bw, w = bw * 4;
+    const uint4 raw = __ldg(blocks + b);
+    bc7_decode(raw, [&](int i, uint32_t v) { rgba[(size_t)(4 * by + (i >> 2)) * w + 4 * bx + (i & 3)] = v; });
+}
+
+cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, cudaStream_t s) {
+    const uint32_t n = (w / 4) * (h / 4);
+    bc7_map_kernel<<<(n + 127) / 128, 128, 0, s>>>(reinterpret_cast<const uint4*>(blocks), w / 4, h / 4,
+                                                   reinterpret_cast<uint32_t*>(rgba));
+    return cudaGetLastError();
+}
+
+__global__ void tex_fetch_kernel(cudaTextureObject_t tex, uint32_t w, uint32_t h, uint32_t* rgba) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= w * h) return;
+    const uint32_t x = i % w, y = i / w;
+    const float4 v = tex2D<float4>(tex, (float)x + 0.5f, (float)y + 0.5f);
+    rgba[i] = (uint32_t)__float2int_rn(v.x * 255.f) | ((uint32_t)__float2int_rn(v.y * 255.f) << 8) |
+              ((uint32_t)__float2int_rn(v.z * 255.f) << 16) | ((uint32_t)__float2int_rn(v.w * 255.f) << 24);
+}
+
+cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba) {
+    cudaArray_t arr = nullptr;
+    cudaTextureObject_t tex = 0;
+    cudaChannelFormatDesc cd = cudaCreateChannelDesc(32, 32, 32, 32, cudaChannelFormatKindUnsigned);
+    cudaError_t e = cudaMallocArray(&arr, &cd, w / 4, h / 4);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy2DToArray(arr, 0, 0, blocks, (w / 4) * 16, (w / 4) * 16, h / 4, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) {
+        cudaResourceDesc rd = {};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = arr;
+        cudaTextureDesc td = {};
+        td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeNormalizedFloat;
+        td.normalizedCoords = 0;
+        cudaResourceViewDesc vd = {};
+        vd.format = cudaResViewFormatUnsignedBlockCompressed7;
+        vd.width = w;
+        vd.height = h;
+        vd.depth = 0;
+        e = cudaCreateTextureObject(&tex, &rd, &td, &vd);
+        if (e == cudaSuccess) {
+            tex_fetch_kernel<<<(w * h + 255) / 256, 256>>>(tex, w, h, reinterpret_cast<uint32_t*>(rgba));
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            cudaDestroyTextureObject(tex);
+        }
+    }
+    cudaFreeArray(arr);
+    return e;
+}
+
+// 8 independent f16x2 GELU chains per thread
+__global__ void __launch_bounds__(256) gelu_rate_kernel(uint32_t iters, uint32_t* sink) {
+    uint32_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = pack_f16x2(0.25f + 0.01f * (threadIdx.x & 7) + 0.1f * q, -0.5f - 0.02f * q);
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = gelu_scaled_f16x2(v[q]);
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc ^= v[q];
+    if (acc == 0x12345678u) sink[0] = acc;  // keep the chains alive
+}
+
+cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t* sink = nullptr;
+    cudaError_t e = cudaMalloc(&sink, 4);
+    if (e != cudaSuccess) return e;
+    const int grid = sms * 8;
+    gelu_rate_kernel<<<grid, 256>>>(16, sink);  // warm-up
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    gelu_rate_kernel<<<grid, 256>>>(iters, sink);
+    cudaEventRecord(b);
+    e = cudaEventSynchronize(b);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaEventElapsedTime(ms, a, b);
+    *acts = (double)grid * 256.0 * 8.0 * 2.0 * (double)iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    return e;
+}
+
+}  // namespace ndgi

@@ -1,0 +1,451 @@
+// fused_kernel.cu -- NDGI_MODE_FAST: the fused tile-decode kernel for sm_100a.
+//
+// One persistent kernel does the whole hot path of SURVEY.md §8(a):
+//   a1  work units (query time, request, strip of core rows); call constants
+//       gamma(t), k0/k1/tau, r0/r1/rho come precomputed from the host
+//   a2  per unit: the tile's f16 MLP, the two BC7 t-slices of F_uvt, the line
+//       maps at t, and (per 2048-texel chunk) the BC7 F_uv blocks
+//   a3  BC7 decode (bc7_device.cuh) -- one block per thread -> shared memory
+//   a4  V_uvt: tau-blended slice (f16, smem) sampled bilinearly (f16x2 math);
+//       V_uv: the texel itself (R2); V_ut per column / V_vt per row (f16x2)
+//   a5  gamma(t): folded into layer-1's bias column (R6)
+//   a6  the 16-wide Eq. 4 input row of each texel -> TMEM (tcgen05.st)
+//   a7  G_Phi on the 5th-gen tensor cores: per 128-texel block three
+//       tcgen05.mma (kind::f16, M=128) with A in TMEM, B (weights) in smem,
+//       fp32 accumulators in TMEM; biases ride in an extra K chunk (A column
+//       of ones); GELU in the epilogue on packed f16x2 (tanh.approx), its
+//       constants folded into the next layer's weights
+//   a8  RGBA8 (or 16F/32F) page-cache writer: core + mirrored border (R3)
+//
+// CTA = 128 threads = 4 warps; thread t owns TMEM lane t = texel t of the
+// current 128-texel block (warp w may only touch lanes 32w..32w+31).  Several
+// CTAs per SM (TMEM: 64 columns per CTA for h = 16, 128 for h = 64) hide the
+// MMA round-trip latency of each other.
+#include <cuda_runtime.h>
+
+#include "bc7_device.cuh"
+#include "ndgi_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace ndgi {
+
+constexpr int kThreads = 128;
+constexpr int kChunkTexels = 2048;  // F_uv texels decoded per chunk (128 BC7 blocks)
+
+template <int H>
+struct FusedCfg {
+    static constexpr int K2 = H + 16;                   // layer 2/3 K incl. bias chunk
+    static constexpr uint32_t TM_A1 = 0;                // 8 columns  (K = 16 f16)
+    static constexpr uint32_t TM_A23 = 8;               // K2/2 columns
+    static constexpr uint32_t TM_D = H == 16 ? 32 : 64; // H columns (fp32 accumulators)
+    static constexpr uint32_t TM_COLS = H == 16 ? 64 : 128;
+    static constexpr int B1_BYTES = H * 16 * 2;
+    static constexpr int B2_BYTES = H * K2 * 2;
+    static constexpr int B3_BYTES = 16 * K2 * 2;
+    static constexpr int B_BYTES = B1_BYTES + B2_BYTES + B3_BYTES;
+    static_assert(TM_A23 + K2 / 2 <= TM_D, "TMEM layout");
+    static_assert(TM_D + H <= TM_COLS, "TMEM layout");
+};
+
+// element (n, k) of a K-major no-swizzle operand with Kt columns:
+// [n/8][k/8][n%8][k%8] halves -> LBO = 128 B, SBO = Kt/8 * 128 B
+__device__ __forceinline__ int bofs(int n, int k, int Kt) {
+    return (((n >> 3) * (Kt >> 3) + (k >> 3)) << 6) + ((n & 7) << 3) + (k & 7);
+}
+
+__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+// a + f (b - a), packed
+__device__ __forceinline__ uint32_t hlerp2(uint32_t a, uint32_t b, uint32_t f2) { return hfma2(f2, hsub2(b, a), a); }
+
+// 4 u8 channels -> two f16x2 holding the integers 0..255 exactly
+__device__ __forceinline__ void u8x4_to_h2(uint32_t q, uint32_t& rg, uint32_t& ba) {
+    const uint32_t k1024 = 0x64006400u;  // f16x2(1024, 1024); 0x64XX = 1024 + XX
+    rg = hsub2(__byte_perm(q, 0x64646464u, 0x5140u), k1024);
+    ba = hsub2(__byte_perm(q, 0x64646464u, 0x7362u), k1024);
+}
+
+struct FusedSmem {
+    // offsets in bytes from the dynamic smem base
+    uint32_t b1, b2, b3, uvt, uvc, utcol, vtrow, bar, tmem_slot, total;
+};
+
+template <int H>
+__host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
+    using Cfg = FusedCfg<H>;
+    FusedSmem s{};
+    uint32_t o = 0;
+    s.b1 = o; o += Cfg::B1_BYTES;
+    s.b2 = o; o += Cfg::B2_BYTES;
+    s.b3 = o; o += Cfg::B3_BYTES;
+    o = (o + 127) & ~127u;
+    s.uvt = o; o += (uint32_t)(R3 * R3 * 8);         // blended slice, f16x4 per texel
+    s.uvc = o; o += kChunkTexels * 4;                 // decoded F_uv chunk, RGBA8
+    s.utcol = o; o += (uint32_t)(C * 4);              // V_ut per column, f16x2
+    s.vtrow = o; o += (uint32_t)(C * 4);              // V_vt per row, f16x2
+    o = (o + 15) & ~15u;
+    s.bar = o; o += 8;
+    s.tmem_slot = o; o += 8;
+    s.total = o;
+    return s;
+}
+
+template <int H, int FMT_UV>
+__global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(const __grid_constant__ KParams p) {
+    using Cfg = FusedCfg<H>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const FusedSmem L = fused_smem_layout<H>(p.C, p.R3);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bar = ptx::smem_addr(smem + L.bar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
+    __half* sB1 = reinterpret_cast<__half*>(smem + L.b1);
+    __half* sB2 = reinterpret_cast<__half*>(smem + L.b2);
+    __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
+    uint2* sUvt = reinterpret_cast<uint2*>(smem + L.uvt);
+    uint32_t* sUvc = reinterpret_cast<uint32_t*>(smem + L.uvc);
+    uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
+    uint32_t* sVt = reinterpret_cast<uint32_t*>(smem + L.vtrow);
+
+    // ---- one-time setup: mbarrier, TMEM allocation --------------------------
+    if (tid == 0) {
+        ptx::mbar_init(bar, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<Cfg::TM_COLS>(ptx::smem_addr(tmem_slot));
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
+
+    // constant part of the layer-2/3 A operand: the bias chunk [1, 0, ..., 0]
+    {
+        uint32_t c[8] = {0x00003C00u, 0, 0, 0, 0, 0, 0, 0};
+        ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A23 + H / 2, c);
+        ptx::tmem_wait_st();
+    }
+
+    const int C = p.C, B = p.B, P = p.P, R3 = p.R3;
+    const int chunk_rows = kChunkTexels / C;
+    const int blocks_per_row = C / kThreads;
+    const uint32_t idesc1 = ptx::idesc_f16_f32(128, H);
+    const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
+    const uint32_t sb1 = ptx::smem_addr(sB1), sb2 = ptx::smem_addr(sB2), sb3 = ptx::smem_addr(sB3);
+    uint32_t phase = 0;
+
+    // issue one layer (K steps of 16) and wait for it; all threads participate
+    auto run_layer = [&](uint32_t a_col, uint32_t b_saddr, int kt, uint32_t idesc) {
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            ptx::tc_fence_after();
+            const uint32_t sbo = (uint32_t)(kt >> 3) * 128u;
+            for (int s = 0; s < kt / 16; ++s)
+                ptx::mma_f16_ts(tmem + Cfg::TM_D, tmem + a_col + 8u * s,
+                                ptx::smem_desc_kmajor(b_saddr + 256u * s, 128u, sbo), idesc, s > 0);
+            ptx::mma_commit(bar);
+        }
+        ptx::mbar_wait(bar, phase);
+        phase ^= 1u;
+        ptx::tc_fence_after();
+    };
+
+    for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
+        const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
+        const uint32_t rq = unit / (uint32_t)p.strips_per_tile;
+        const int ti = (int)(rq / p.n_req);
+        const uint32_t r = rq % p.n_req;
+        const TConst& tc = p.tc[ti];
+        int k;
+        size_t out_base;  // texel index of core texel (0,0)
+        size_t row_pitch; // texels between rows
+        if (p.full) {
+            k = (int)r;
+            const int tx = k % p.tiles_x, ty = (k / p.tiles_x) % p.tiles_y, a = k / (p.tiles_x * p.tiles_y);
+            row_pitch = (size_t)p.tiles_x * C;
+            out_base = (size_t)ti * p.out_t_stride + (size_t)a * p.tiles_y * C * row_pitch +
+                       (size_t)ty * C * row_pitch + (size_t)tx * C;
+        } else {
+            const uint32_t id = __ldg(p.tile_ids + r);
+            const uint32_t slot = p.slots ? __ldg(p.slots + r) : r;
+            if (id >= (uint32_t)p.num_tiles || slot >= p.num_slots) {
+                if (strip == 0 && tid == 0) atomicAdd(p.err, 1u);
+                continue;  // uniform across the CTA
+            }
+            k = (int)id;
+            row_pitch = (size_t)P;
+            out_base = ((size_t)slot * P + B) * P + B;
+        }
+
+        // ---- a2: tile parameters -> shared memory ---------------------------------
+        __syncthreads();  // previous unit's smem readers are done
+        {
+            const uint16_t* w = p.mlp + p.mlp_tile_elems * k;
+            const uint16_t *W1 = w, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
+            const float a = kGeluA;
+            const float s_uv = FMT_UV == FMT_F16 ? a : a / 255.0f;   // F_uv enters in q units (R8)
+            // layer 1: [H][16]: k 0..11 = Eq. 4 features, 12 = bias (gamma(t) folded), 13..15 = 0
+            for (int e = tid; e < H * 16; e += kThreads) {
+                const int n = e >> 4, kk = e & 15;
+                float v = 0.f;
+                if (kk < 12) {
+                    const float wv = half_bits_to_float(__ldg(W1 + n * 16 + kk));
+                    v = wv * ((kk >= 4 && kk < 8) ? s_uv : a);
+                } else if (kk == 12) {
+                    float acc = half_bits_to_float(__ldg(b1 + n));
+                    for (int g = 0; g < 4; ++g) acc = fmaf(half_bits_to_float(__ldg(W1 + n * 16 + 12 + g)), tc.gamma[g], acc);
+                    v = a * acc;
+                }
+                sB1[bofs(n, kk, 16)] = __float2half_rn(v);
+            }
+            // layer 2: [H][H+16]: 0.5*W2 (absorbs 1/(2a) of GELU and a of the next pre-scale), bias a*b2
+            for (int e = tid; e < H * Cfg::K2; e += kThreads) {
+                const int n = e / Cfg::K2, kk = e % Cfg::K2;
+                float v = 0.f;
+                if (kk < H) v = 0.5f * half_bits_to_float(__ldg(W2 + n * H + kk));
+                else if (kk == H) v = a * half_bits_to_float(__ldg(b2 + n));
+                sB2[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
+            }
+            // layer 3: [16][H+16]: rows 0..2 = W3/(2a), bias b3 (exact); rows 3..15 = 0
+            for (int e = tid; e < 16 * Cfg::K2; e += kThreads) {
+                const int n = e / Cfg::K2, kk = e % Cfg::K2;
+                float v = 0.f;
+                if (n < 3) {
+                    if (kk < H) v = half_bits_to_float(__ldg(W3 + n * H + kk)) * (0.5f / a);
+                    else if (kk == H) v = half_bits_to_float(__ldg(b3 + n));
+                }
+                sB3[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
+            }
+            // F_uvt slices k0, k1 blended with tau (R4, R17) -> f16x4 [R3][R3], values in [0,1]
+            const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
+            const float tau = tc.tau, omt = 1.0f - tau;
+            if (p.fmt_uvt == FMT_BC7) {
+                const int nbx = R3 >> 2, nb = nbx * nbx;
+                const uint4* s0 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k0);
+                const uint4* s1 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k1);
+                for (int bi = tid; bi < nb; bi += kThreads) {
+                    uint32_t t0[16], t1[16];
+                    bc7_decode(__ldg(s0 + bi), [&](int i, uint32_t v) { t0[i] = v; });
+                    bc7_decode(__ldg(s1 + bi), [&](int i, uint32_t v) { t1[i] = v; });
+                    const int bx = bi % nbx, by = bi / nbx;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float c[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            c[q] = (omt * (float)((t0[i] >> (8 * q)) & 0xffu) + tau * (float)((t1[i] >> (8 * q)) & 0xffu)) *
+                                   (1.0f / 255.0f);
+                        sUvt[(by * 4 + (i >> 2)) * R3 + bx * 4 + (i & 3)] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+                    }
+                }
+            } else {
+                const int ntex = R3 * R3;
+                for (int e = tid; e < ntex; e += kThreads) {
+                    float c[4];
+                    if (p.fmt_uvt == FMT_U8) {
+                        const uint32_t q0 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k0) + e);
+                        const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + e);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            c[q] = (omt * (float)((q0 >> (8 * q)) & 0xffu) + tau * (float)((q1 >> (8 * q)) & 0xffu)) * (1.0f / 255.0f);
+                    } else {
+                        const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * e;
+                        const uint16_t* h1 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k1) + 4 * e;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            c[q] = omt * half_bits_to_float(__ldg(h0 + q)) + tau * half_bits_to_float(__ldg(h1 + q));
+                    }
+                    sUvt[e] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+                }
+            }
+            // line maps (R5): V_ut(u_i) per core column i, V_vt(v_j) per core row j
+            const uint8_t* ut = p.ut + p.line_tile_bytes * k;
+            const uint8_t* vt = p.vt + p.line_tile_bytes * k;
+            const float rho = tc.rho, omr = 1.0f - rho;
+            for (int e = tid; e < 2 * C; e += kThreads) {
+                const int i = e % C;
+                const uint8_t* m = e < C ? ut : vt;
+                const float sx = ((float)i + 0.5f) / (float)C * (float)p.U - 0.5f;
+                const float fl = floorf(sx), fx = sx - fl;
+                const int x0 = clampi((int)fl, 0, p.U - 1), x1 = clampi((int)fl + 1, 0, p.U - 1);
+                float c[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    float v00, v10, v01, v11;
+                    if (p.fmt_line == FMT_U8) {
+                        v00 = (float)__ldg(m + (tc.r0 * p.U + x0) * 2 + q);
+                        v10 = (float)__ldg(m + (tc.r0 * p.U + x1) * 2 + q);
+                        v01 = (float)__ldg(m + (tc.r1 * p.U + x0) * 2 + q);
+                        v11 = (float)__ldg(m + (tc.r1 * p.U + x1) * 2 + q);
+                    } else {
+                        const uint16_t* mh = reinterpret_cast<const uint16_t*>(m);
+                        v00 = half_bits_to_float(__ldg(mh + (tc.r0 * p.U + x0) * 2 + q));
+                        v10 = half_bits_to_float(__ldg(mh + (tc.r0 * p.U + x1) * 2 + q));
+                        v01 = half_bits_to_float(__ldg(mh + (tc.r1 * p.U + x0) * 2 + q));
+                        v11 = half_bits_to_float(__ldg(mh + (tc.r1 * p.U + x1) * 2 + q));
+                    }
+                    float v = (1.f - fx) * omr * v00 + fx * omr * v10 + (1.f - fx) * rho * v01 + fx * rho * v11;
+                    c[q] = p.fmt_line == FMT_U8 ? v * (1.0f / 255.0f) : v;
+                }
+                (e < C ? sUt : sVt)[i] = pack_f16x2(c[0], c[1]);
+            }
+        }
+        ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
+        __syncthreads();
+
+        // ---- rows of this strip ------------------------------------------------------
+        const int j_begin = strip * p.strip_rows, j_end = j_begin + p.strip_rows;
+        const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
+        for (int jc = j_begin; jc < j_end; jc += chunk_rows) {
+            if (FMT_UV == FMT_BC7) {
+                // a3: 128 BC7 blocks of F_uv (rows jc .. jc+chunk_rows) -> smem RGBA8
+                const int bpr = C >> 2;
+                const int brow = tid / bpr, bcol = tid % bpr;
+                const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + brow) * bpr + bcol);
+                uint32_t* dst = sUvc + (brow * 4) * C + bcol * 4;
+                uint32_t rowv[4];
+                bc7_decode(raw, [&](int i, uint32_t v) {
+                    rowv[i & 3] = v;
+                    if ((i & 3) == 3) *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
+                });
+                __syncthreads();
+            }
+            for (int jr = 0; jr < chunk_rows; ++jr) {
+                const int j = jc + jr;
+                // per-row constants (uniform): uvt y taps
+                const float sy = ((float)j + 0.5f) / (float)C * (float)R3 - 0.5f;
+                const float fly = floorf(sy);
+                const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
+                const uint32_t fy2 = pack_f16x2(sy - fly, sy - fly);
+                const uint32_t vtv = sVt[j];
+                for (int blk = 0; blk < blocks_per_row; ++blk) {
+                    const int i = blk * kThreads + tid;
+                    // ---- a4/a6: gather the Eq. 4 input row of texel (i, j) ----
+                    const float sx = ((float)i + 0.5f) / (float)C * (float)R3 - 0.5f;
+                    const float flx = floorf(sx);
+                    const int x0 = clampi((int)flx, 0, R3 - 1), x1 = clampi((int)flx + 1, 0, R3 - 1);
+                    const uint32_t fx2 = pack_f16x2(sx - flx, sx - flx);
+                    const uint2 t00 = sUvt[y0 * R3 + x0], t10 = sUvt[y0 * R3 + x1];
+                    const uint2 t01 = sUvt[y1 * R3 + x0], t11 = sUvt[y1 * R3 + x1];
+                    uint32_t a1[8];
+                    a1[0] = hlerp2(hlerp2(t00.x, t10.x, fx2), hlerp2(t01.x, t11.x, fx2), fy2);
+                    a1[1] = hlerp2(hlerp2(t00.y, t10.y, fx2), hlerp2(t01.y, t11.y, fx2), fy2);
+                    if (FMT_UV == FMT_BC7) {
+                        u8x4_to_h2(sUvc[jr * C + i], a1[2], a1[3]);
+                    } else if (FMT_UV == FMT_U8) {
+                        u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)j * C + i), a1[2], a1[3]);
+                    } else {
+                        const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)j * C + i);
+                        a1[2] = hv.x;
+                        a1[3] = hv.y;
+                    }
+                    a1[4] = sUt[i];
+                    a1[5] = vtv;
+                    a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
+                    a1[7] = 0u;
+                    ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A1, a1);
+
+                    // ---- a7: layer 1 ----
+                    run_layer(Cfg::TM_A1, sb1, 16, idesc1);
+                    // epilogue 1: GELU -> A23
+#pragma unroll
+                    for (int c0 = 0; c0 < H; c0 += 16) {
+                        uint32_t d[16], g[8];
+                        ptx::tmem_ld_x16(tmem + lane_base + Cfg::TM_D + c0, d);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
+                        ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A23 + c0 / 2, g);
+                    }
+                    // ---- layer 2 ----
+                    run_layer(Cfg::TM_A23, sb2, Cfg::K2, idesc1);
+#pragma unroll
+                    for (int c0 = 0; c0 < H; c0 += 16) {
+                        uint32_t d[16], g[8];
+                        ptx::tmem_ld_x16(tmem + lane_base + Cfg::TM_D + c0, d);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
+                        ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A23 + c0 / 2, g);
+                    }
+                    // ---- layer 3 ----
+                    run_layer(Cfg::TM_A23, sb3, Cfg::K2, idesc3);
+                    uint32_t yv[4];
+                    ptx::tmem_ld_x4(tmem + lane_base + Cfg::TM_D, yv);
+                    ptx::tmem_wait_ld();
+                    const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
+
+                    // ---- a8: page-cache writer (core + mirrored border, R3) ----
+                    const size_t o = out_base + (size_t)j * row_pitch + i;
+                    store_texel(p.out, o, p.out_fmt, y0f, y1f, y2f);
+                    if (!p.full && B > 0) {
+                        const bool bx = (i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2);
+                        const bool by = (j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2);
+                        if (bx || by) {
+                            // mirrored positions: core i -> padded-core offsets -i and 2(C-1)-i
+                            const int xm = i <= B ? -i : 2 * (C - 1) - i;
+                            const int ym = j <= B ? -j : 2 * (C - 1) - j;
+                            const ptrdiff_t base = (ptrdiff_t)out_base;
+                            const ptrdiff_t rp = (ptrdiff_t)row_pitch;
+                            if (bx) store_texel(p.out, (size_t)(base + (ptrdiff_t)j * rp + xm), p.out_fmt, y0f, y1f, y2f);
+                            if (by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + i), p.out_fmt, y0f, y1f, y2f);
+                            if (bx && by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + xm), p.out_fmt, y0f, y1f, y2f);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- teardown --------------------------------------------------------------------
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<Cfg::TM_COLS>(tmem);
+}
+
+// ---- host-side launch helpers ---------------------------------------------------
+template <int H, int FMT_UV>
+static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s, int* ctas_per_sm_out) {
+    const FusedSmem L = fused_smem_layout<H>(p.C, p.R3);
+    auto kern = ndgi_fused_kernel<H, FMT_UV>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, L.total);
+    if (e != cudaSuccess) return e;
+    const int tmem_cap = 512 / (int)FusedCfg<H>::TM_COLS;
+    if (occ > tmem_cap) occ = tmem_cap;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (ctas_per_sm_out) *ctas_per_sm_out = occ;
+    const uint32_t cap = (uint32_t)(num_sms * occ);
+    const uint32_t grid = p.units < cap ? p.units : cap;
+    kern<<<grid, kThreads, L.total, s>>>(p);
+    return cudaGetLastError();
+}
+
+int fused_ctas_per_sm(int H) { return H == 16 ? 8 : 4; }
+
+cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s) {
+    int occ = 0;
+    if (p.H == 16) {
+        if (p.fmt_uv == FMT_BC7) return launch_fused_t<16, FMT_BC7>(p, num_sms, s, &occ);
+        if (p.fmt_uv == FMT_U8) return launch_fused_t<16, FMT_U8>(p, num_sms, s, &occ);
+        return launch_fused_t<16, FMT_F16>(p, num_sms, s, &occ);
+    }
+    if (p.fmt_uv == FMT_BC7) return launch_fused_t<64, FMT_BC7>(p, num_sms, s, &occ);
+    if (p.fmt_uv == FMT_U8) return launch_fused_t<64, FMT_U8>(p, num_sms, s, &occ);
+    return launch_fused_t<64, FMT_F16>(p, num_sms, s, &occ);
+}
+
+}  // namespace ndgi

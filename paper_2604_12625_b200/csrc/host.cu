@@ -1,0 +1,415 @@
+// host.cu -- the C ABI of libndgi.so (include/ndgi.h): validation, context,
+// call setup and kernel launches.  No torch types cross
+// this boundary; every entry point returns an ndgi_status and never throws.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ndgi.h"
+#include "ndgi_common.cuh"
+
+namespace ndgi {
+cudaError_t launch_ref(const KParams& p, cudaStream_t stream);
+cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s);
+int fused_ctas_per_sm(int H);
+cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, cudaStream_t s);
+cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
+cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts);
+}  // namespace ndgi
+
+struct ndgi_ctx {
+    ndgi_layout L;
+    ndgi_params P;
+    int device;
+    int num_sms;
+    uint32_t* d_err;
+    // host-buffer path
+    cudaStream_t hstream[2];
+    cudaEvent_t hevent[2];
+    void* stage[2];
+    size_t stage_bytes;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ndgi_status fail(ndgi_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+ndgi_status cuda_fail(cudaError_t e, const char* where) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return NDGI_ERR_CUDA;
+}
+
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+size_t map2d_bytes(uint32_t fmt, uint32_t rx, uint32_t ry, uint32_t nc) {
+    if (fmt == NDGI_FMT_BC7) return (size_t)(rx / 4) * (ry / 4) * 16;
+    return (size_t)rx * ry * nc * (fmt == NDGI_FMT_U8 ? 1 : 2);
+}
+
+size_t mlp_elems(uint32_t h) { return (size_t)16 * h + h + (size_t)h * h + h + 3 * (size_t)h + 3; }
+
+bool fmt_ok(uint32_t f) { return f <= NDGI_FMT_F16; }
+
+ndgi_status validate(const ndgi_layout* L, int* fast) {
+    if (!L) return fail(NDGI_ERR_ARG, "layout is NULL");
+    if (L->abi_version != NDGI_ABI_VERSION) return fail(NDGI_ERR_ARG, "abi_version mismatch");
+    if (L->num_tiles == 0) return fail(NDGI_ERR_ARG, "num_tiles == 0");
+    if ((uint64_t)L->atlases * L->tiles_x * L->tiles_y != L->num_tiles)
+        return fail(NDGI_ERR_ARG, "num_tiles != atlases*tiles_y*tiles_x");
+    if (L->core < 4 || L->core % 4 != 0) return fail(NDGI_ERR_ARG, "core must be a multiple of 4, >= 4");
+    if (L->border >= L->core) return fail(NDGI_ERR_ARG, "border must be < core");
+    if (L->uv_res == 0 || L->uvt_res == 0 || L->uvt_depth == 0 || L->line_res == 0 || L->line_t == 0)
+        return fail(NDGI_ERR_ARG, "zero resolution");
+    if (!fmt_ok(L->fmt_uv) || !fmt_ok(L->fmt_uvt)) return fail(NDGI_ERR_ARG, "bad feature format");
+    if (L->fmt_line != NDGI_FMT_U8 && L->fmt_line != NDGI_FMT_F16) return fail(NDGI_ERR_ARG, "fmt_line must be U8 or F16");
+    if (L->fmt_uv == NDGI_FMT_BC7 && L->uv_res % 4) return fail(NDGI_ERR_ARG, "BC7 F_uv resolution must be a multiple of 4");
+    if (L->fmt_uvt == NDGI_FMT_BC7 && L->uvt_res % 4) return fail(NDGI_ERR_ARG, "BC7 F_uvt resolution must be a multiple of 4");
+    if (L->hidden < 1 || L->hidden > 256) return fail(NDGI_ERR_ARG, "hidden must be in [1, 256]");
+    if (L->gelu > NDGI_GELU_TANH) return fail(NDGI_ERR_ARG, "bad gelu");
+    if (L->border_mode > NDGI_BORDER_EVAL_CLAMP) return fail(NDGI_ERR_ARG, "bad border_mode");
+    if (fast) {
+        *fast = (L->core == 128 || L->core == 256) && L->uv_res == L->core && (L->hidden == 16 || L->hidden == 64) &&
+                L->border_mode == NDGI_BORDER_MIRROR && L->uvt_res <= 64 && L->line_res <= 256 &&
+                L->uvt_res >= 4;
+    }
+    return NDGI_OK;
+}
+
+// call setup (a1): gamma(t), slice and row indices, in fp64 (R4, R5, Eq. 4)
+ndgi::TConst make_tconst(const ndgi_layout& L, double t) {
+    ndgi::TConst c{};
+    c.t = (float)t;
+    c.gamma[0] = (float)std::sin(M_PI * t);
+    c.gamma[1] = (float)std::cos(M_PI * t);
+    c.gamma[2] = (float)std::sin(2.0 * M_PI * t);
+    c.gamma[3] = (float)std::cos(2.0 * M_PI * t);
+    auto axis = [](double s, int n, int& i0, int& i1, float& f) {
+        const double fl = std::floor(s);
+        f = (float)(s - fl);
+        const int a = (int)fl;
+        i0 = a < 0 ? 0 : (a > n - 1 ? n - 1 : a);
+        i1 = a + 1 < 0 ? 0 : (a + 1 > n - 1 ? n - 1 : a + 1);
+    };
+    axis(t * L.uvt_depth - 0.5, (int)L.uvt_depth, c.k0, c.k1, c.tau);
+    axis(t * L.line_t - 0.5, (int)L.line_t, c.r0, c.r1, c.rho);
+    return c;
+}
+
+void fill_common(const ndgi_ctx* ctx, ndgi::KParams& p) {
+    const ndgi_layout& L = ctx->L;
+    memset(&p, 0, sizeof(p));
+    p.C = (int)L.core;
+    p.B = (int)L.border;
+    p.P = (int)(L.core + 2 * L.border);
+    p.R_uv = (int)L.uv_res;
+    p.R3 = (int)L.uvt_res;
+    p.D = (int)L.uvt_depth;
+    p.U = (int)L.line_res;
+    p.T = (int)L.line_t;
+    p.H = (int)L.hidden;
+    p.fmt_uv = (int)L.fmt_uv;
+    p.fmt_uvt = (int)L.fmt_uvt;
+    p.fmt_line = (int)L.fmt_line;
+    p.gelu = (int)L.gelu;
+    p.border_mode = (int)L.border_mode;
+    p.atlases = (int)L.atlases;
+    p.tiles_x = (int)L.tiles_x;
+    p.tiles_y = (int)L.tiles_y;
+    p.num_tiles = (int)L.num_tiles;
+    p.uv = static_cast<const uint8_t*>(ctx->P.uv);
+    p.uvt = static_cast<const uint8_t*>(ctx->P.uvt);
+    p.ut = static_cast<const uint8_t*>(ctx->P.ut);
+    p.vt = static_cast<const uint8_t*>(ctx->P.vt);
+    p.mlp = ctx->P.mlp;
+    p.uv_tile_bytes = map2d_bytes(L.fmt_uv, L.uv_res, L.uv_res, 4);
+    p.uvt_slice_bytes = map2d_bytes(L.fmt_uvt, L.uvt_res, L.uvt_res, 4);
+    p.uvt_tile_bytes = p.uvt_slice_bytes * L.uvt_depth;
+    p.line_tile_bytes = map2d_bytes(L.fmt_line, L.line_res, L.line_t, 2);
+    p.mlp_tile_elems = mlp_elems(L.hidden);
+    p.err = ctx->d_err;
+}
+
+ndgi_status check_t(float t) {
+    if (!std::isfinite(t) || t < 0.0f || t > 1.0f) return fail(NDGI_ERR_RANGE, "t must be finite and in [0, 1]");
+    return NDGI_OK;
+}
+
+// work decomposition of the fused kernel: smallest number of strips per tile
+// that still gives >= 2 waves of work units (VT batches), rows multiple of
+// the 2048-texel F_uv chunk
+void choose_strips(ndgi::KParams& p, int num_sms) {
+    const int C = p.C;
+    const int chunk_rows = 2048 / C;
+    const int max_strips = C / chunk_rows;
+    const uint64_t target = 2ull * num_sms * ndgi::fused_ctas_per_sm(p.H);
+    int s = 1;
+    while (s < max_strips && (uint64_t)p.nt * p.n_req * s < target) s *= 2;
+    p.strips_per_tile = s;
+    p.strip_rows = C / s;
+    p.units = (uint32_t)((uint64_t)p.nt * p.n_req * s);
+}
+
+ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t s) {
+    int fast = 0;
+    validate(&ctx->L, &fast);
+    cudaError_t e;
+    if (mode == NDGI_MODE_FAST) {
+        if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
+        choose_strips(p, ctx->num_sms);
+        e = ndgi::launch_fused(p, ctx->num_sms, s);
+    } else {
+        e = ndgi::launch_ref(p, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    return NDGI_OK;
+}
+
+bool mode_ok(int m) { return m == NDGI_MODE_FAST || m == NDGI_MODE_REF_FP32; }
+bool out_ok(int f) { return f >= NDGI_OUT_RGBA8 && f <= NDGI_OUT_RGBA32F; }
+
+ndgi_status decode_full_async(ndgi_ctx* ctx, const float* ts, uint32_t nt, void* out, ndgi_out_fmt fmt,
+                              ndgi_mode mode, cudaStream_t stream) {
+    const size_t per_t = ndgi_full_texels(&ctx->L);
+    for (uint32_t t0 = 0; t0 < nt; t0 += ndgi::kMaxT) {
+        const uint32_t n = nt - t0 < (uint32_t)ndgi::kMaxT ? nt - t0 : (uint32_t)ndgi::kMaxT;
+        ndgi::KParams p;
+        fill_common(ctx, p);
+        p.nt = (int)n;
+        for (uint32_t i = 0; i < n; ++i) p.tc[i] = make_tconst(ctx->L, (double)ts[t0 + i]);
+        p.out_t_stride = per_t;
+        p.full = 1;
+        p.n_req = ctx->L.num_tiles;
+        p.num_slots = 0;
+        p.out = static_cast<uint8_t*>(out) + (size_t)t0 * per_t * ndgi_texel_bytes(fmt);
+        p.out_fmt = (int)fmt;
+        ndgi_status st = launch(ctx, p, mode, stream);
+        if (st != NDGI_OK) return st;
+    }
+    return NDGI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ndgi_status_string(ndgi_status s) {
+    switch (s) {
+        case NDGI_OK: return "NDGI_OK";
+        case NDGI_ERR_ARG: return "NDGI_ERR_ARG";
+        case NDGI_ERR_RANGE: return "NDGI_ERR_RANGE";
+        case NDGI_ERR_UNSUPPORTED: return "NDGI_ERR_UNSUPPORTED";
+        case NDGI_ERR_CUDA: return "NDGI_ERR_CUDA";
+        case NDGI_ERR_NOMEM: return "NDGI_ERR_NOMEM";
+        case NDGI_ERR_DEVICE: return "NDGI_ERR_DEVICE";
+    }
+    return "NDGI_ERR_UNKNOWN";
+}
+
+const char* ndgi_last_error(void) { return g_last_error.c_str(); }
+
+ndgi_status ndgi_validate_layout(const ndgi_layout* layout, int* fast_supported) {
+    return validate(layout, fast_supported);
+}
+
+uint64_t ndgi_full_texels(const ndgi_layout* L) {
+    return L ? (uint64_t)L->num_tiles * L->core * L->core : 0;
+}
+
+size_t ndgi_texel_bytes(ndgi_out_fmt fmt) {
+    return fmt == NDGI_OUT_RGBA8 ? 4 : (fmt == NDGI_OUT_RGBA16F ? 8 : (fmt == NDGI_OUT_RGBA32F ? 16 : 0));
+}
+
+ndgi_status ndgi_load(const ndgi_layout* layout, const ndgi_params* params, int device, ndgi_ctx** out) {
+    if (!out) return fail(NDGI_ERR_ARG, "out is NULL");
+    ndgi_status st = validate(layout, nullptr);
+    if (st != NDGI_OK) return st;
+    if (!params || !params->uv || !params->uvt || !params->ut || !params->vt || !params->mlp)
+        return fail(NDGI_ERR_ARG, "params or one of its pointers is NULL");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || device < 0 || device >= ndev) return fail(NDGI_ERR_DEVICE, "no such CUDA device");
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(NDGI_ERR_DEVICE, "libndgi.so is built for sm_100a (B200); device is sm_" +
+                                         std::to_string(prop.major) + std::to_string(prop.minor));
+    DeviceGuard g(device);
+    ndgi_ctx* c = new (std::nothrow) ndgi_ctx();
+    if (!c) return fail(NDGI_ERR_NOMEM, "host allocation");
+    c->L = *layout;
+    c->P = *params;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    e = cudaMalloc(&c->d_err, sizeof(uint32_t));
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaMalloc(error counter)");
+    }
+    cudaMemset(c->d_err, 0, sizeof(uint32_t));
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(c->d_err);
+        delete c;
+        return cuda_fail(e, "ndgi_load sync");
+    }
+    *out = c;
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_decode_tiles(ndgi_ctx* ctx, const uint32_t* tile_ids, const uint32_t* slots, uint32_t n,
+                              uint32_t num_slots, float t, void* out_cache, ndgi_out_fmt fmt, ndgi_mode mode,
+                              void* stream) {
+    if (!ctx || !tile_ids || !out_cache) return fail(NDGI_ERR_ARG, "NULL ctx, tile_ids or out_cache");
+    if (!out_ok(fmt) || !mode_ok(mode)) return fail(NDGI_ERR_ARG, "bad fmt or mode");
+    if (n == 0) return fail(NDGI_ERR_ARG, "n == 0");
+    if (n > (1u << 24)) return fail(NDGI_ERR_RANGE, "n > 2^24");
+    if (num_slots == 0) return fail(NDGI_ERR_ARG, "num_slots == 0");
+    ndgi_status st = check_t(t);
+    if (st != NDGI_OK) return st;
+    DeviceGuard g(ctx->device);
+    ndgi::KParams p;
+    fill_common(ctx, p);
+    p.nt = 1;
+    p.tc[0] = make_tconst(ctx->L, (double)t);
+    p.full = 0;
+    p.tile_ids = tile_ids;
+    p.slots = slots;
+    p.n_req = n;
+    p.num_slots = num_slots;
+    p.out = out_cache;
+    p.out_fmt = (int)fmt;
+    return launch(ctx, p, mode, static_cast<cudaStream_t>(stream));
+}
+
+ndgi_status ndgi_decode_full(ndgi_ctx* ctx, float t, void* out, ndgi_out_fmt fmt, ndgi_mode mode, void* stream) {
+    if (!ctx || !out) return fail(NDGI_ERR_ARG, "NULL ctx or out");
+    if (!out_ok(fmt) || !mode_ok(mode)) return fail(NDGI_ERR_ARG, "bad fmt or mode");
+    ndgi_status st = check_t(t);
+    if (st != NDGI_OK) return st;
+    DeviceGuard g(ctx->device);
+    return decode_full_async(ctx, &t, 1, out, fmt, mode, static_cast<cudaStream_t>(stream));
+}
+
+ndgi_status ndgi_decode_full_batch(ndgi_ctx* ctx, const float* t, uint32_t n_t, void* out, ndgi_out_fmt fmt,
+                                   ndgi_mode mode, void* stream) {
+    if (!ctx || !out || !t) return fail(NDGI_ERR_ARG, "NULL ctx, t or out");
+    if (!out_ok(fmt) || !mode_ok(mode)) return fail(NDGI_ERR_ARG, "bad fmt or mode");
+    if (n_t == 0) return fail(NDGI_ERR_ARG, "n_t == 0");
+    for (uint32_t i = 0; i < n_t; ++i) {
+        ndgi_status st = check_t(t[i]);
+        if (st != NDGI_OK) return st;
+    }
+    DeviceGuard g(ctx->device);
+    return decode_full_async(ctx, t, n_t, out, fmt, mode, static_cast<cudaStream_t>(stream));
+}
+
+ndgi_status ndgi_decode_full_host(ndgi_ctx* ctx, const float* t, uint32_t n_t, void* out_host, ndgi_out_fmt fmt,
+                                  ndgi_mode mode) {
+    if (!ctx || !out_host || !t) return fail(NDGI_ERR_ARG, "NULL ctx, t or out_host");
+    if (!out_ok(fmt) || !mode_ok(mode)) return fail(NDGI_ERR_ARG, "bad fmt or mode");
+    if (n_t == 0) return fail(NDGI_ERR_ARG, "n_t == 0");
+    for (uint32_t i = 0; i < n_t; ++i) {
+        ndgi_status st = check_t(t[i]);
+        if (st != NDGI_OK) return st;
+    }
+    DeviceGuard g(ctx->device);
+    const size_t bytes = ndgi_full_texels(&ctx->L) * ndgi_texel_bytes(fmt);
+    cudaError_t e;
+    if (ctx->stage_bytes < bytes) {
+        for (int i = 0; i < 2; ++i) {
+            if (ctx->stage[i]) cudaFree(ctx->stage[i]);
+            ctx->stage[i] = nullptr;
+        }
+        ctx->stage_bytes = 0;
+        for (int i = 0; i < 2; ++i) {
+            e = cudaMalloc(&ctx->stage[i], bytes);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+            if (!ctx->hstream[i]) {
+                cudaStreamCreateWithFlags(&ctx->hstream[i], cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&ctx->hevent[i], cudaEventDisableTiming);
+            }
+        }
+        ctx->stage_bytes = bytes;
+    }
+    // time i decodes into stage[i%2] on stream i%2 and is copied out on the same
+    // stream, so decode of i+1 overlaps the copy of i
+    for (uint32_t i = 0; i < n_t; ++i) {
+        const int b = (int)(i & 1u);
+        ndgi_status st = decode_full_async(ctx, t + i, 1, ctx->stage[b], fmt, mode, ctx->hstream[b]);
+        if (st != NDGI_OK) return st;
+        e = cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + (size_t)i * bytes, ctx->stage[b], bytes,
+                            cudaMemcpyDeviceToHost, ctx->hstream[b]);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+    }
+    for (int b = 0; b < 2; ++b) {
+        e = cudaStreamSynchronize(ctx->hstream[b]);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    }
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_device_error(ndgi_ctx* ctx, uint32_t* bad_requests, int reset) {
+    if (!ctx || !bad_requests) return fail(NDGI_ERR_ARG, "NULL ctx or bad_requests");
+    DeviceGuard g(ctx->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+    e = cudaMemcpy(bad_requests, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(error counter)");
+    if (reset) cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_free(ndgi_ctx* ctx) {
+    if (!ctx) return fail(NDGI_ERR_ARG, "NULL ctx");
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(ctx->d_err);
+    for (int i = 0; i < 2; ++i) {
+        if (ctx->stage[i]) cudaFree(ctx->stage[i]);
+        if (ctx->hstream[i]) cudaStreamDestroy(ctx->hstream[i]);
+        if (ctx->hevent[i]) cudaEventDestroy(ctx->hevent[i]);
+    }
+    delete ctx;
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_debug_bc7_decode(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, void* stream) {
+    if (!blocks || !rgba || w % 4 || h % 4 || !w || !h) return fail(NDGI_ERR_ARG, "bad arguments");
+    cudaError_t e = ndgi::launch_bc7_map(blocks, w, h, rgba, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 map decode");
+}
+
+ndgi_status ndgi_debug_bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba) {
+    if (!blocks || !rgba || w % 4 || h % 4 || !w || !h) return fail(NDGI_ERR_ARG, "bad arguments");
+    cudaError_t e = ndgi::bc7_decode_hw(blocks, w, h, rgba);
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 texture decode");
+}
+
+ndgi_status ndgi_debug_gelu_rate(uint32_t iters, float* ms, double* activations) {
+    if (!ms || !activations || !iters) return fail(NDGI_ERR_ARG, "bad arguments");
+    cudaError_t e = ndgi::gelu_rate(iters, ms, activations);
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "gelu rate");
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// ndgi_common.cuh -- kernel-side parameter block and small helpers shared by
+// the CUDA kernels of libndgi.so (never by the oracle).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace ndgi {
+
+enum : int { FMT_BC7 = 0, FMT_U8 = 1, FMT_F16 = 2 };
+enum : int { OUT_RGBA8 = 0, OUT_RGBA16F = 1, OUT_RGBA32F = 2 };
+enum : int { GELU_ERF = 0, GELU_TANH = 1 };
+enum : int { BORDER_MIRROR = 0, BORDER_EVAL_CLAMP = 1 };
+
+constexpr int kMaxT = 32;   // query times per launch
+
+struct TConst {
+    float t;
+    float gamma[4];      // Eq. 4: sin(pi t), cos(pi t), sin(2 pi t), cos(2 pi t)
+    int k0, k1;          // F_uvt slices (R4)
+    float tau;
+    int r0, r1;          // F_ut/F_vt rows (R5)
+    float rho;
+};
+
+// Everything a decode launch needs, passed by value (__grid_constant__).
+struct KParams {
+    // layout (include/ndgi.h)
+    int C, B, P, R_uv, R3, D, U, T, H;
+    int fmt_uv, fmt_uvt, fmt_line, gelu, border_mode;
+    int atlases, tiles_x, tiles_y, num_tiles;
+    // Theta, device, tile-major
+    const uint8_t* uv;
+    const uint8_t* uvt;
+    const uint8_t* ut;
+    const uint8_t* vt;
+    const uint16_t* mlp;
+    size_t uv_tile_bytes, uvt_tile_bytes, uvt_slice_bytes, line_tile_bytes, mlp_tile_elems;
+    // per-call constants (call setup), one set per query time,
+    // computed on the host in fp64
+    int nt;
+    TConst tc[kMaxT];
+    size_t out_t_stride;        // decode_full: texels per atlas set (one t)
+    // requests
+    const uint32_t* tile_ids;   // decode_tiles; nullptr for decode_full
+    const uint32_t* slots;      // nullptr -> slot = request index
+    uint32_t n_req, num_slots;
+    int full;                   // 1: decode_full (atlas addressing, core only)
+    // output
+    void* out;
+    int out_fmt;
+    uint32_t* err;              // device error counter
+    // work decomposition of the fused kernel
+    int strip_rows;             // rows of core per work unit
+    int strips_per_tile;
+    uint32_t units;             // nt * n_req * strips_per_tile
+};
+
+__device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+__device__ __forceinline__ float half_bits_to_float(uint16_t h) {
+    return __half2float(__ushort_as_half(h));
+}
+
+// mirror a core coordinate, reflect without repeating the edge (R3)
+__device__ __forceinline__ int mirror_core(int i, int C) {
+    if (i < 0) i = -i;
+    if (i >= C) i = 2 * (C - 1) - i;
+    return i;
+}
+
+// RN-even(clamp(y,0,1)*255), NaN -> 0 (R12)
+__device__ __forceinline__ uint32_t quant8(float y) {
+    return __float2uint_rn(fminf(fmaxf(y, 0.0f), 1.0f) * 255.0f);
+}
+
+__device__ __forceinline__ void store_texel(void* out, size_t idx, int fmt, float r, float g, float b) {
+    if (fmt == OUT_RGBA8) {
+        const uint32_t v = quant8(r) | (quant8(g) << 8) | (quant8(b) << 16) | 0xff000000u;
+        reinterpret_cast<uint32_t*>(out)[idx] = v;
+    } else if (fmt == OUT_RGBA16F) {
+        __half2 rg = __floats2half2_rn(r, g), ba = __floats2half2_rn(b, 1.0f);
+        uint2 v;
+        v.x = *reinterpret_cast<uint32_t*>(&rg);
+        v.y = *reinterpret_cast<uint32_t*>(&ba);
+        reinterpret_cast<uint2*>(out)[idx] = v;
+    } else {
+        reinterpret_cast<float4*>(out)[idx] = make_float4(r, g, b, 1.0f);
+    }
+}
+
+}  // namespace ndgi
+
+namespace ndgi {
+
+// ---------------------------------------------------------------------------
+// GELU in the fused kernel (FAST mode, reading R7): tanh form on packed f16x2
+// with the constants folded into the neighbouring layers' weights.
+//   With a = sqrt(2/pi) and z~ = a z (the layer's MMA produces z~ directly):
+//   tanh-GELU(z) = 0.5 z (1 + tanh(a (z + 0.044715 z^3)))
+//                = g~ / (2a),   g~ = z~ (1 + tanh(z~ (1 + c z~^2))),  c = 0.044715/a^2
+//   so each hidden activation costs HMUL2, HFMA2, HMUL2, MUFU.TANH, HFMA2
+//   per two values, and 1/(2a) moves into the next layer's weights.
+// ---------------------------------------------------------------------------
+constexpr float kGeluA = 0.7978845608028654f;        // sqrt(2/pi)
+constexpr float kGeluC = 0.044715f / (0.7978845608028654f * 0.7978845608028654f);
+
+__device__ __forceinline__ uint32_t gelu_scaled_f16x2(uint32_t h) {
+    const uint32_t c2 = 0x2C7F2C7Fu;   // f16x2(c), c = 0.0702382 -> f16 0.07025
+    const uint32_t one2 = 0x3C003C00u; // f16x2(1.0)
+    uint32_t s, p, u, t, g;
+    asm("mul.rn.f16x2 %0, %1, %1;" : "=r"(s) : "r"(h));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(p) : "r"(s), "r"(c2), "r"(one2));
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(u) : "r"(h), "r"(p));
+    asm("tanh.approx.f16x2 %0, %1;" : "=r"(t) : "r"(u));
+    asm("fma.rn.f16x2 %0, %1, %2, %1;" : "=r"(g) : "r"(h), "r"(t));
+    return g;
+}
+
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+}  // namespace ndgi

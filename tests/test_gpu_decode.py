@@ -1,0 +1,306 @@
+"""GPU parity of libndgi.so against the CPU oracle (called through the C ABI).
+
+Bars (BASELINE.json north_star):
+* BC7 decode: bit-exact (device decoder vs oracle; vs the B200 texture unit);
+* NDGI_MODE_REF_FP32: max-abs <= 1e-5 on RGBA32F vs the fp64 oracle;
+* NDGI_MODE_FAST (tcgen05, f16 operands): max-abs <= 2e-2, mean-abs <= 2e-3;
+* RGBA8: the kernel's quantisation of its own fp32 y equals RN-even(clamp(y)*255)
+  computed by the oracle in fp32 (same precision), and |dq| <= 1 vs the oracle's y.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import ndgi_synth as S
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2604_12625_b200 as ndgi  # noqa: E402
+
+NTHR = max(1, len(os.sched_getaffinity(0)))
+FAST_MAX, FAST_MEAN, REF_MAX = 2e-2, 2e-3, 1e-5
+
+
+def _load(lay, th):
+    return ndgi.ndgi_load(lay, ndgi.upload_theta(th), 0)
+
+
+def gpu_full(ctx, ts, fmt="rgba32f", mode="fast"):
+    ts = [ts] if np.isscalar(ts) else list(ts)
+    L = ctx.lay
+    C = L["core"]
+    shape = (len(ts), L["atlases"], L["tiles_y"] * C, L["tiles_x"] * C)
+    if fmt == "rgba8":
+        out = torch.zeros(shape + (4,), dtype=torch.uint8, device="cuda")
+    elif fmt == "rgba16f":
+        out = torch.zeros(shape + (4,), dtype=torch.float16, device="cuda")
+    else:
+        out = torch.zeros(shape + (4,), dtype=torch.float32, device="cuda")
+    if len(ts) == 1:
+        ndgi.ndgi_decode_full(ctx, ts[0], out, fmt, mode)
+    else:
+        ndgi.ndgi_decode_full_batch(ctx, ts, out, fmt, mode)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def gpu_tiles(ctx, ids, t, fmt="rgba32f", mode="fast", slots=None, num_slots=None):
+    P = ctx.padded
+    n = len(ids)
+    num_slots = num_slots or n
+    dt = {"rgba8": torch.uint8, "rgba16f": torch.float16, "rgba32f": torch.float32}[fmt]
+    out = torch.zeros((num_slots, P, P, 4), dtype=dt, device="cuda")
+    ids_t = torch.tensor(np.asarray(ids, np.int64), dtype=torch.int32, device="cuda")
+    sl_t = None if slots is None else torch.tensor(np.asarray(slots, np.int64), dtype=torch.int32, device="cuda")
+    ndgi.ndgi_decode_tiles(ctx, ids_t, sl_t, n, num_slots, t, out, fmt, mode)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _err(got, exp):
+    d = np.abs(got[..., :3].astype(np.float64) - exp)
+    return float(d.max()), float(d.mean())
+
+
+# ------------------------------------------------------------------ BC7
+def _mixed_blocks(n, seed, with_mode8=True):
+    words = S.splitmix64(np.arange(3 * n, dtype=np.uint64) + np.uint64(seed)).reshape(n, 3)
+    modes = (words[:, 2] % np.uint64(9 if with_mode8 else 8)).astype(np.int64)
+    return S.bc7_random_blocks(words[:, :2], modes)
+
+
+@pytest.mark.parametrize("payload", ["mixed", "smooth", "mode6"])
+def test_bc7_device_decoder_bit_exact(payload):
+    w = h = 512
+    n = (w // 4) * (h // 4)
+    if payload == "mixed":
+        blocks = _mixed_blocks(n, 17)
+    elif payload == "mode6":
+        blocks = _mixed_blocks(n, 5, False)
+        words = S.splitmix64(np.arange(2 * n, dtype=np.uint64) + np.uint64(99)).reshape(n, 2)
+        blocks = S.bc7_random_blocks(words, np.full(n, 6))
+    else:
+        lay = S.layout(1, 4, 4, "M")
+        blocks = S.make_theta(lay, 3)["uv"].reshape(n, 16)
+    exp = oracle.bc7_decode_image(blocks, w, h)
+    dev_blocks = torch.from_numpy(blocks.copy()).cuda()
+    out = torch.zeros((h, w, 4), dtype=torch.uint8, device="cuda")
+    ndgi.ndgi_debug_bc7_decode(dev_blocks, w, h, out)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), exp)
+
+
+def test_bc7_texture_unit_agrees_with_oracle():
+    """The B200's own BC7 decoder (texture unit) as an independent reference."""
+    w = h = 256
+    n = (w // 4) * (h // 4)
+    blocks = _mixed_blocks(n, 23, with_mode8=False)
+    exp = oracle.bc7_decode_image(blocks, w, h)
+    out = torch.zeros((h, w, 4), dtype=torch.uint8, device="cuda")
+    ndgi.ndgi_debug_bc7_decode_hw(torch.from_numpy(blocks.copy()).cuda(), w, h, out)
+    np.testing.assert_array_equal(out.cpu().numpy(), exp)
+
+
+# ------------------------------------------------------------------ reference mode
+@pytest.mark.parametrize("gelu", ["erf", "tanh"])
+def test_ref_fp32_full_c1(gelu):
+    lay, seed = S.config("c1")
+    lay = dict(lay, gelu=gelu)
+    th = S.make_theta(lay, seed)
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    for t in (0.3, 0.375, 0.0, 1.0):
+        got = gpu_full(ctx, t, "rgba32f", "ref_fp32")[0]
+        exp = M.decode_full(t, NTHR)
+        mx, mean = _err(got, exp)
+        assert mx <= REF_MAX, (t, mx, mean)
+        assert (got[..., 3] == 1.0).all()
+
+
+def test_ref_fp32_tiles_slots_and_small_cores():
+    # ragged geometry the fast path does not take: C=12, R_uv=8 (bilinear F_uv), h=8, eval-clamp border
+    for lay in (S.layout(1, 3, 1, "M", core=12, border=3, uv_res=8, uvt_res=8, uvt_depth=3, line_res=7, line_t=5, hidden=8),
+                S.layout(1, 2, 1, "M", core=8, border=4, uvt_res=4, uvt_depth=2, line_res=4, line_t=2, hidden=4,
+                         border_mode="eval_clamp", fmt_uv="f16", fmt_uvt="u8", fmt_line="f16")):
+        th = S.make_theta(lay, 7, "mixed")
+        M = oracle.Model(lay, th)
+        ctx = _load(lay, th)
+        ids = [1, 0, 2][:lay["num_tiles"]] + [0]
+        slots = list(range(len(ids)))[::-1]
+        got = gpu_tiles(ctx, ids, 0.61, "rgba32f", "ref_fp32", slots=slots, num_slots=len(ids) + 1)
+        exp = M.decode_tiles(ids, 0.61)
+        for r, s in enumerate(slots):
+            mx, _ = _err(got[s], exp[r])
+            assert mx <= REF_MAX, (lay["core"], r, mx)
+
+
+# ------------------------------------------------------------------ fast (tensor-core) mode
+FAST_CASES = {
+    "c1-bc7": (S.config("c1")[0], "smooth"),
+    "c1-bc7-mixed": (S.config("c1")[0], "mixed"),
+    "u8": (S.layout(1, 2, 1, "M", uvt_depth=5, line_t=7, fmt_uv="u8", fmt_uvt="u8"), "smooth"),
+    "f16": (S.layout(1, 2, 1, "M", uvt_depth=5, line_t=7, fmt_uv="f16", fmt_uvt="f16", fmt_line="f16"), "smooth"),
+    "M64": (S.layout(1, 2, 1, "M64", uvt_depth=4, line_t=4), "smooth"),
+    "L-tanh": (S.layout(1, 2, 1, "L", gelu="tanh"), "smooth"),
+    "H": (S.layout(1, 1, 2, "H"), "mixed"),
+    "C256": (S.layout(1, 1, 1, "M", core=256, uv_res=256), "smooth"),
+}
+
+
+@pytest.mark.parametrize("name", list(FAST_CASES))
+def test_fast_full_parity(name):
+    lay, payload = FAST_CASES[name]
+    th = S.make_theta(lay, 41, payload)
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    for t in (0.3, 1.0):
+        got = gpu_full(ctx, t, "rgba32f", "fast")[0]
+        exp = M.decode_full(t, NTHR)
+        mx, mean = _err(got, exp)
+        print(f"{name} t={t}: max {mx:.3e} mean {mean:.3e}")
+        assert mx <= FAST_MAX and mean <= FAST_MEAN, (name, t, mx, mean)
+
+
+def test_fast_tiles_border_and_rgba8():
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed)
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    ids = [3, 1, 0, 2, 1]
+    slots = [4, 0, 6, 2, 5]
+    t = 0.3
+    y32 = gpu_tiles(ctx, ids, t, "rgba32f", "fast", slots=slots, num_slots=8)
+    q8 = gpu_tiles(ctx, ids, t, "rgba8", "fast", slots=slots, num_slots=8)
+    exp = M.decode_tiles(ids, t, NTHR)
+    for r, s in enumerate(slots):
+        mx, mean = _err(y32[s], exp[r])
+        assert mx <= FAST_MAX and mean <= FAST_MEAN, (r, mx, mean)
+        # RGBA8 = the oracle's fp32 quantiser applied to the kernel's own fp32 y
+        np.testing.assert_array_equal(q8[s], oracle.quantize_rgba8(np.ascontiguousarray(y32[s])))
+        dq = np.abs(q8[s][..., :3].astype(int) - oracle.quantize_rgba8(exp[r])[..., :3].astype(int))
+        assert dq.max() <= 1
+    # untouched slots stay zero
+    assert (q8[1] == 0).all() and (q8[3] == 0).all() and (q8[7] == 0).all()
+
+
+def test_fast_full_equals_tiles_core_and_deterministic():
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed, "mixed")
+    ctx = _load(lay, th)
+    full = gpu_full(ctx, 0.7, "rgba8")[0]
+    full2 = gpu_full(ctx, 0.7, "rgba8")[0]
+    np.testing.assert_array_equal(full, full2)
+    tiles = gpu_tiles(ctx, [0, 1, 2, 3], 0.7, "rgba8")
+    C, B = 128, 4
+    for k in range(4):
+        tx, ty = k % 2, k // 2
+        np.testing.assert_array_equal(full[0, ty * C:(ty + 1) * C, tx * C:(tx + 1) * C], tiles[k, B:B + C, B:B + C])
+        # mirrored border is an exact copy (R3)
+        pad = np.pad(tiles[k, B:B + C, B:B + C], ((B, B), (B, B), (0, 0)), mode="reflect")
+        np.testing.assert_array_equal(tiles[k], pad)
+
+
+def test_cross_format_u8_equals_bc7():
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed, "mixed")
+    lay8 = dict(lay, fmt_uv="u8", fmt_uvt="u8")
+    th8 = dict(th)
+    th8["uv"] = np.stack([oracle.bc7_decode_image(th["uv"][k].reshape(-1, 16), 128, 128) for k in range(4)])
+    th8["uvt"] = np.stack([[oracle.bc7_decode_image(th["uvt"][k, d].reshape(-1, 16), 32, 32) for d in range(4)]
+                           for k in range(4)])
+    for mode in ("fast", "ref_fp32"):
+        a = gpu_full(_load(lay, th), 0.45, "rgba32f", mode)
+        b = gpu_full(_load(lay8, th8), 0.45, "rgba32f", mode)
+        np.testing.assert_array_equal(a, b)
+
+
+def test_batch_equals_single_calls():
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed)
+    ctx = _load(lay, th)
+    ts = [i / 24 for i in range(0, 24, 3)]
+    batch = gpu_full(ctx, ts, "rgba8")
+    for i, t in enumerate(ts):
+        np.testing.assert_array_equal(batch[i], gpu_full(ctx, t, "rgba8")[0])
+
+
+def test_small_batches_strips():
+    # n = 1 and n = 3 requests take the strip split (several units per tile)
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed)
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    for ids in ([2], [3, 0, 3]):
+        got = gpu_tiles(ctx, ids, 0.9, "rgba32f")
+        exp = M.decode_tiles(ids, 0.9, NTHR)
+        mx, mean = _err(got, exp)
+        assert mx <= FAST_MAX and mean <= FAST_MEAN
+
+
+def test_bad_ids_and_arguments():
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed)
+    ctx = _load(lay, th)
+    ndgi.ndgi_device_error(ctx, reset=True)
+    out = gpu_tiles(ctx, [0, 7, 1], 0.5, "rgba8", slots=[0, 1, 9], num_slots=3)
+    assert ndgi.ndgi_device_error(ctx, reset=True) == 2     # id 7 and slot 9 rejected
+    assert (out[0] != 0).any() and (out[1] == 0).all()
+    for mode in ("fast", "ref_fp32"):
+        gpu_tiles(ctx, [5], 0.5, "rgba8", mode=mode)
+        assert ndgi.ndgi_device_error(ctx, reset=True) == 1
+    o = torch.zeros((4, 136, 136, 4), dtype=torch.uint8, device="cuda")
+    ids = torch.zeros(4, dtype=torch.int32, device="cuda")
+    for t in (float("nan"), -0.1, 1.5, float("inf")):
+        with pytest.raises(ndgi.NdgiError) as e:
+            ndgi.ndgi_decode_tiles(ctx, ids, None, 4, 4, t, o)
+        assert e.value.status == ndgi.ERR_RANGE
+    lay_bad = dict(lay, hidden=8)
+    th_bad = S.make_theta(lay_bad, 1)
+    ctx_bad = _load(lay_bad, th_bad)
+    with pytest.raises(ndgi.NdgiError) as e:
+        ndgi.ndgi_decode_full(ctx_bad, 0.5, o, "rgba8", "fast")
+    assert e.value.status == ndgi.ERR_UNSUPPORTED
+
+
+def test_c2_fullsize_sampled():
+    """Config 2 (4096^2 atlas, 1024 tiles) in the bench's launch configuration:
+    sampled texels against the oracle evaluated one by one, two whole tiles."""
+    lay, seed = S.config("c2")
+    th = S.make_theta(lay, seed)
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    ts = [5 / 24, 17 / 24]
+    got = gpu_full(ctx, ts, "rgba32f")
+    rng = np.random.default_rng(0)
+    C = 128
+    for ti, t in enumerate(ts):
+        errs = []
+        for _ in range(400):
+            k = int(rng.integers(0, 1024))
+            i, j = (int(v) for v in rng.integers(0, C, 2))
+            tx, ty = k % 32, k // 32
+            exp = M.texel(k, i + 4, j + 4, t)
+            errs.append(np.abs(got[ti, 0, ty * C + j, tx * C + i, :3] - exp))
+        errs = np.array(errs)
+        assert errs.max() <= FAST_MAX and errs.mean() <= FAST_MEAN
+        for k in (0, 1023):
+            tx, ty = k % 32, k // 32
+            exp = M.decode_tiles([k], t, NTHR)[0, 4:4 + C, 4:4 + C]
+            mx, mean = _err(got[ti, 0, ty * C:(ty + 1) * C, tx * C:(tx + 1) * C], exp)
+            assert mx <= FAST_MAX and mean <= FAST_MEAN
+
+
+def test_host_buffer_path():
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed)
+    ctx = _load(lay, th)
+    ts = [0.1, 0.2, 0.3]
+    host = torch.zeros((3, 1, 256, 256, 4), dtype=torch.uint8).pin_memory()
+    ndgi.ndgi_decode_full_host(ctx, ts, host, "rgba8")
+    np.testing.assert_array_equal(host.numpy(), gpu_full(ctx, ts, "rgba8"))
