@@ -1,0 +1,360 @@
+"""bench.py -- NDGI temporal-lightmap decode on B200 (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...   (one rank per GPU)
+
+Workload (BASELINE.json configs[1]): one 4096^2
+lightmap atlas = 32 x 32 NDGI tiles of 128^2, profile M (F_uvt 32^2x12x4,
+h = 16; Table 1/3), BC7 F_uv / F_uvt, u8 line maps, f16 MLP; synthetic seeded
+Theta.  One step = decode_full at the 24 hourly bake times t_i = i/24
+= 24 x 16.78 M written texels, RGBA8, in one launch of the fused kernel.
+Multi-GPU: weak scaling -- every rank owns 1024 tiles of an N x 1024-tile
+scene (tile k on rank k % N) and decodes them with no communication; the
+step time is the max over ranks.
+
+Reported: value = written Gtexel/s (whole job); roofline of the fused kernel
+(ALU-bound: its GELU activations/s against the measured rate of the same
+GELU formulation, plus HBM and tensor fractions); cpu_baseline = the plain C
+oracle on this host's cores over a bounded sample; e2e = the same metric
+through ndgi_decode_full_host (Theta H2D + decode + RGBA8 D2H in the timed
+region); vt_batch_us = per-batch latency of ndgi_decode_tiles for VT batches
+of n random tiles of the 16,384-tile config-3 scene.
+`--impl reference` times the oracle (the reference arm) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ndgi_synth as S  # noqa: E402
+
+METRIC = "decoded lightmap Gtexels/s"
+UNIT = "Gtexel/s"
+N_T = 24
+TS = [i / N_T for i in range(N_T)]
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+def _workload_config(world: int, tiles_per_rank: int) -> dict:
+    return {
+        "workload": "c2: 4096^2 lightmap atlas (32x32 NDGI-M tiles of 128^2, BC7 F_uv/F_uvt, u8 lines, "
+                    "f16 MLP h=16) decoded at 24 times t=i/24 per step (decode_full, RGBA8)",
+        "tiles_per_gpu": tiles_per_rank, "times_per_step": N_T, "core": 128, "profile": "M",
+        "written_texels_per_step": tiles_per_rank * 128 * 128 * N_T * world,
+        "scene_tiles": tiles_per_rank * world, "parallelism": f"tile-sharded x{world} (k % N)",
+        "l2": "flushed between timed steps (256 MiB write); Theta 36.9 MB/GPU",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def cpu_oracle_rate(lay, seed, target_s=8.0):
+    """The oracle as it stands, all host cores, bounded sample of the same workload."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    th = S.make_theta(lay, seed, tiles=list(range(64)))
+    sub = dict(lay, num_tiles=64, atlases=1, tiles_x=64, tiles_y=1)
+    M = oracle.Model(sub, th)
+    t0 = time.perf_counter()
+    M.decode_tiles([0], TS[7], nthreads=cores)           # calibration: one padded tile
+    dt = time.perf_counter() - t0
+    per_tile = dt
+    ntiles = int(max(1, min(64, target_s / max(per_tile, 1e-6))))
+    t0 = time.perf_counter()
+    ids = list(range(ntiles))
+    M.decode_tiles(ids, TS[13], nthreads=cores)
+    dt = time.perf_counter() - t0
+    texels = ntiles * 136 * 136
+    return {"value": texels / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{ntiles} padded 136^2 tiles of c2 at t=13/24 ({texels} texels), fp64 C oracle, "
+                      f"{cores} threads, {dt:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    lay, seed = S.config("c2")
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    th = S.make_theta(lay, seed, tiles=list(range(8)))
+    sub = dict(lay, num_tiles=8, atlases=1, tiles_x=8, tiles_y=1)
+    M = oracle.Model(sub, th)
+    # each step: one core tile (128^2 written texels) at one of the 24 times
+    for w in range(args.warmup):
+        M.decode_tiles([w % 8], TS[w % N_T], nthreads=cores)
+    t0 = time.perf_counter()
+    texels = 0
+    for s in range(args.steps):
+        M.decode_tiles([s % 8], TS[s % N_T], nthreads=cores)
+        texels += 136 * 136
+    dt = time.perf_counter() - t0
+    v = texels / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _workload_config(1, 1024),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": "per step one padded 136^2 tile of c2 at one of the 24 times (fp64 C oracle)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, rank, world, dist):
+    import torch
+
+    import paper_2604_12625_b200 as ndgi
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    lay0, seed = S.config("c2")
+    tiles_per_rank = lay0["num_tiles"]
+    global_ids = [rank + world * i for i in range(tiles_per_rank)]
+    th_np = S.make_theta(lay0, seed, tiles=global_ids)
+    lay = dict(lay0)
+    theta = ndgi.upload_theta(th_np, dev)
+    ctx = ndgi.ndgi_load(lay, theta, dev)
+    per_t = ctx.full_texels()
+    out = torch.empty((N_T, per_t * 4), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ndgi.ndgi_decode_full_batch(ctx, TS, out, "rgba8", "fast", stream)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for i in range(args.steps):
+            flush.zero_()                      # L2 flush between timed steps (outside the events)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    texels_per_step = per_t * N_T * world
+    value = texels_per_step / (ms_per_step * 1e-3) / 1e9
+
+    # ---------------- end-to-end through the host-buffer API (Theta H2D + decode + D2H)
+    e2e = None
+    try:
+        host_theta = {k: v.cpu().pin_memory() for k, v in theta.items()}
+        host_out = torch.empty((N_T, per_t * 4), dtype=torch.uint8).pin_memory()
+        h2d = sum(v.numel() * v.element_size() for v in host_theta.values()) + 4 * N_T
+        d2h = host_out.numel()
+        e2e_steps = max(2, min(args.steps, 5))
+
+        def e2e_step():
+            for k, v in host_theta.items():
+                theta[k].copy_(v, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            ndgi.ndgi_decode_full_host(ctx, TS, host_out, "rgba8", "fast")
+
+        e2e_step()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if dist:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": texels_per_step / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+               "path": "ndgi_decode_full_host (pinned host RGBA8 out) + Theta H2D copy per step"}
+    except Exception as exc:  # pragma: no cover - reported, not hidden
+        e2e = {"value": None, "unit": UNIT, "error": repr(exc)}
+
+    if rank != 0:
+        return
+    # ---------------- roofline of the fused kernel (rank 0)
+    peaks = _peaks()
+    ms_g, acts = ndgi.ndgi_debug_gelu_rate(4096)
+    r_gelu = acts / (ms_g * 1e-3)                              # activations/s, same f16x2 GELU
+    h = lay["hidden"]
+    evaluated = tiles_per_rank * 128 * 128 * N_T               # decode_full: every written texel evaluated
+    kern_s = ms_per_step * 1e-3                                 # one fused-kernel launch per step
+    achieved_act = evaluated * 2 * h / kern_s
+    theta_t_bytes = tiles_per_rank * (16384 + 2 * 1024 + 2 * 2 * 64 * 2 + 595 * 2)   # read at one t
+    alg_bytes = N_T * (theta_t_bytes + tiles_per_rank * 128 * 128 * 4)
+    flops = evaluated * 2 * (16 * h + (h + 16) * h + (h + 16) * 16)               # tensor work as issued
+    roofline = {
+        "bound": "alu", "achieved": achieved_act / 1e9, "peak": r_gelu / 1e9, "unit": "Gact/s",
+        "frac": achieved_act / r_gelu, "traffic": None,
+        "kernel": "ndgi_fused_kernel<16,BC7>", "per_unit": f"2h = {2 * h} GELU activations per evaluated texel",
+        "peak_source": "ndgi_debug_gelu_rate: the kernel's f16x2 tanh-GELU, 148 SMs x 8 CTAs, measured in this run",
+        "hbm_frac": alg_bytes / kern_s / 1e9 / peaks["hbm_gbs"],
+        "tensor_frac": flops / kern_s / 1e12 / peaks.get("bf16_tflops_sustained", 1375.0),
+        "algorithmic_bytes_per_launch": alg_bytes,
+    }
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_oracle_rate(lay0, seed, args.cpu_seconds)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "error": repr(exc)}
+    vt = None
+    if not args.no_vt:
+        try:
+            vt = vt_latency(ndgi, torch, args)
+        except Exception as exc:  # pragma: no cover
+            vt = {"error": repr(exc)}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+        "clocks": clk.summary(), "vt_batch_us": vt,
+        "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def vt_latency(ndgi, torch, args):
+    """Config 3: per-batch latency of ndgi_decode_tiles on a 16,384-tile scene."""
+    lay, seed = S.config("c3")
+    th = ndgi.upload_theta(S.make_theta(lay, seed))
+    ctx = ndgi.ndgi_load(lay, th, torch.cuda.current_device())
+    res = {}
+    stream = torch.cuda.current_stream()
+    for n in (8, 32, 128, 512):
+        batches = S.vt_batches(lay["num_tiles"], n, 16 + 64, seed)
+        cache = torch.empty((n, 136, 136, 4), dtype=torch.uint8, device="cuda")
+        ids = [torch.from_numpy(b[0].astype(np.int32)).cuda() for b in batches]
+        lat = []
+        for f, (b, t) in enumerate(batches):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ndgi.ndgi_decode_tiles(ctx, ids[f], None, n, n, t, cache, "rgba8", "fast", stream)
+            e1.record(stream)
+            e1.synchronize()
+            if f >= 16:
+                lat.append(e0.elapsed_time(e1) * 1e3)
+        lat.sort()
+        p50 = lat[len(lat) // 2]
+        res[str(n)] = {"p50": p50, "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))],
+                       "gtexel_s": n * 136 * 136 / (p50 * 1e-6) / 1e9}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
+    ap.add_argument("--no-vt", action="store_true", help="skip the VT batch-latency leg")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist_mod
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    try:
+        run_gpu(args, rank, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

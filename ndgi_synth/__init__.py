@@ -105,9 +105,20 @@ def _field_params(seed, stream, tiles, nch):
 
 
 def _smooth(a, b, phi, xs, ys):
-    """[tiles][ch] params, xs/ys normalised coords [...] -> [tiles][...][ch]."""
+    """[tiles][ch] params, xs/ys normalised coords [...] -> [tiles][...][ch] (float32)."""
     arg = 2 * np.pi * (a[:, None, :] * xs.reshape(1, -1, 1) + b[:, None, :] * ys.reshape(1, -1, 1)) + phi[:, None, :]
-    return 0.5 + 0.3 * np.sin(arg)
+    return 0.5 + 0.3 * np.sin(arg.astype(np.float32))
+
+
+def _smooth_grid(a, b, phi, n):
+    """Separable evaluation of _smooth on the n x n grid of cell centres:
+    sin(X + Y) = sin X cos Y + cos X sin Y.  -> [tiles][n*n][ch] float32."""
+    c = ((np.arange(n) + 0.5) / n).astype(np.float32)
+    X = 2 * np.pi * a[:, None, :].astype(np.float32) * c[None, :, None]                  # [t][n][ch]
+    Y = 2 * np.pi * b[:, None, :].astype(np.float32) * c[None, :, None] + phi[:, None, :].astype(np.float32)
+    sx, cx, sy, cy = np.sin(X), np.cos(X), np.sin(Y), np.cos(Y)
+    v = sy[:, :, None, :] * cx[:, None, :, :] + cy[:, :, None, :] * sx[:, None, :, :]  # [t][y][x][ch]
+    return (0.5 + 0.3 * v).reshape(a.shape[0], n * n, a.shape[1])
 
 
 class _BitPacker:
@@ -181,20 +192,23 @@ def _bc7_map(seed, stream, tiles, R, nslices, payload):
         blk = bc7_random_blocks(words[..., :2], modes)
         return blk.reshape(len(tiles), nslices, nb, nb, 16)
     a, b, phi = _field_params(seed, stream, tiles, 4)
-    bx = (np.arange(nb) + 0.5) / nb
-    xs = np.tile(bx, nb)
-    ys = np.repeat(bx, nb)
     out = np.empty((len(tiles), nslices, nb, nb, 16), np.uint8)
     keys = _tile_keys(seed, stream + 100, tiles)
     words = _hash(keys, 2 * nblk).reshape(len(tiles), nslices, nb * nb, 2)
     for s in range(nslices):
-        m = _smooth(a, b, phi + 0.7 * s, xs, ys)            # [tiles][nb*nb][4]
-        d = 0.02 + 0.10 * _unif(words[:, s, :, 0])[..., None]
-        lo = np.clip(np.rint((m - d) * 255), 0, 255).astype(np.int64)
-        hi = np.clip(np.rint((m + d) * 255), 0, 255).astype(np.int64)
-        iw = words[:, s, :, 1]
-        idx = np.stack([(iw >> np.uint64(4 * i)) & np.uint64(15) for i in range(16)], -1).astype(np.int64)
-        out[:, s] = bc7_mode6_blocks(lo, hi, idx).reshape(len(tiles), nb, nb, 16)
+        m = _smooth_grid(a, b, phi + 0.7 * s, nb)            # [tiles][nb*nb][4]
+        d = (0.02 + 0.10 * _unif(words[:, s, :, 0])[..., None]).astype(np.float32)
+        lo = np.clip(np.rint((m - d) * 255), 0, 255).astype(np.uint64)
+        hi = np.clip(np.rint((m + d) * 255), 0, 255).astype(np.uint64)
+        # mode 6: bits 0..6 mode, then R0 R1 G0 G1 B0 B1 A0 A1 (7 bits each), P0 = 0 (bit 63);
+        # second word: P1 = 1 (bit 0), indices (bits 1..63) = hashed noise
+        w0 = np.full(lo.shape[:-1], 1 << 6, np.uint64)
+        for c in range(4):
+            w0 |= (lo[..., c] >> np.uint64(1)) << np.uint64(7 + 14 * c)
+            w0 |= (hi[..., c] >> np.uint64(1)) << np.uint64(14 + 14 * c)
+        w1 = words[:, s, :, 1] | np.uint64(1)
+        blk = np.stack([w0, w1], -1).view(np.uint8)
+        out[:, s] = blk.reshape(len(tiles), nb, nb, 16)
     return out
 
 

@@ -49,7 +49,7 @@ cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* r
         cudaTextureDesc td = {};
         td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
         td.filterMode = cudaFilterModePoint;
-        td.readMode = cudaReadModeNormalizedFloat;
+        td.readMode = cudaReadModeElementType;  // BC7 views return UNORM floats
         td.normalizedCoords = 0;
         cudaResourceViewDesc vd = {};
         vd.format = cudaResViewFormatUnsignedBlockCompressed7;
