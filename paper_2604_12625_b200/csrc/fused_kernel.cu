@@ -23,6 +23,9 @@
 // MMA round-trip latency of each other.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "bc7_device.cuh"
 #include "ndgi_common.cuh"
 #include "tc_ptx.cuh"
@@ -98,9 +101,12 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
     return s;
 }
 
-template <int H, int FMT_UV>
+template <int H, int FMT_UV, int CT>
 __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(const __grid_constant__ KParams p) {
     using Cfg = FusedCfg<H>;
+    constexpr int C = CT;                      // core texels per tile side (128 or 256)
+    constexpr int BPR = CT / kThreads;         // 128-texel MMA blocks per row
+    constexpr int chunk_rows = kChunkTexels / CT;
     extern __shared__ __align__(1024) uint8_t smem[];
     const FusedSmem L = fused_smem_layout<H>(p.C, p.R3);
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -133,9 +139,8 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
         ptx::tmem_wait_st();
     }
 
-    const int C = p.C, B = p.B, P = p.P, R3 = p.R3;
-    const int chunk_rows = kChunkTexels / C;
-    const int blocks_per_row = C / kThreads;
+    const int B = p.B, P = p.P, R3 = p.R3;
+    const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
     const uint32_t idesc1 = ptx::idesc_f16_f32(128, H);
     const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
     const uint32_t sb1 = ptx::smem_addr(sB1), sb2 = ptx::smem_addr(sB2), sb3 = ptx::smem_addr(sB3);
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
             for (int e = tid; e < 2 * C; e += kThreads) {
                 const int i = e % C;
                 const uint8_t* m = e < C ? ut : vt;
-                const float sx = ((float)i + 0.5f) / (float)C * (float)p.U - 0.5f;
+                const float sx = fmaf((float)i + 0.5f, (float)p.U * (1.0f / (float)C), -0.5f);
                 const float fl = floorf(sx), fx = sx - fl;
                 const int x0 = clampi((int)fl, 0, p.U - 1), x1 = clampi((int)fl + 1, 0, p.U - 1);
                 float c[2];
@@ -303,12 +308,25 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
         __syncthreads();
 
         // ---- rows of this strip ------------------------------------------------------
+        // per-thread column constants (thread tid owns columns b*128 + tid)
+        int cx0[BPR], cx1[BPR];
+        uint32_t cfx[BPR], cut[BPR];
+#pragma unroll
+        for (int b = 0; b < BPR; ++b) {
+            const int i = b * kThreads + tid;
+            const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
+            const float flx = floorf(sx);
+            cx0[b] = clampi((int)flx, 0, R3 - 1);
+            cx1[b] = clampi((int)flx + 1, 0, R3 - 1);
+            cfx[b] = pack_f16x2(sx - flx, sx - flx);
+            cut[b] = sUt[i];
+        }
         const int j_begin = strip * p.strip_rows, j_end = j_begin + p.strip_rows;
         const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
         for (int jc = j_begin; jc < j_end; jc += chunk_rows) {
             if (FMT_UV == FMT_BC7) {
                 // a3: 128 BC7 blocks of F_uv (rows jc .. jc+chunk_rows) -> smem RGBA8
-                const int bpr = C >> 2;
+                constexpr int bpr = C >> 2;
                 const int brow = tid / bpr, bcol = tid % bpr;
                 const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + brow) * bpr + bcol);
                 uint32_t* dst = sUvc + (brow * 4) * C + bcol * 4;
@@ -322,18 +340,17 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
             for (int jr = 0; jr < chunk_rows; ++jr) {
                 const int j = jc + jr;
                 // per-row constants (uniform): uvt y taps
-                const float sy = ((float)j + 0.5f) / (float)C * (float)R3 - 0.5f;
+                const float sy = fmaf((float)j + 0.5f, sc3, -0.5f);
                 const float fly = floorf(sy);
                 const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
                 const uint32_t fy2 = pack_f16x2(sy - fly, sy - fly);
                 const uint32_t vtv = sVt[j];
-                for (int blk = 0; blk < blocks_per_row; ++blk) {
+#pragma unroll
+                for (int blk = 0; blk < BPR; ++blk) {
                     const int i = blk * kThreads + tid;
                     // ---- a4/a6: gather the Eq. 4 input row of texel (i, j) ----
-                    const float sx = ((float)i + 0.5f) / (float)C * (float)R3 - 0.5f;
-                    const float flx = floorf(sx);
-                    const int x0 = clampi((int)flx, 0, R3 - 1), x1 = clampi((int)flx + 1, 0, R3 - 1);
-                    const uint32_t fx2 = pack_f16x2(sx - flx, sx - flx);
+                    const int x0 = cx0[blk], x1 = cx1[blk];
+                    const uint32_t fx2 = cfx[blk];
                     const uint2 t00 = sUvt[y0 * R3 + x0], t10 = sUvt[y0 * R3 + x1];
                     const uint2 t01 = sUvt[y1 * R3 + x0], t11 = sUvt[y1 * R3 + x1];
                     uint32_t a1[8];
@@ -348,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
                         a1[2] = hv.x;
                         a1[3] = hv.y;
                     }
-                    a1[4] = sUt[i];
+                    a1[4] = cut[blk];
                     a1[5] = vtv;
                     a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
                     a1[7] = 0u;
@@ -415,37 +432,55 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
 }
 
 // ---- host-side launch helpers ---------------------------------------------------
-template <int H, int FMT_UV>
+template <int H, int FMT_UV, int CT>
 static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s, int* ctas_per_sm_out) {
     const FusedSmem L = fused_smem_layout<H>(p.C, p.R3);
-    auto kern = ndgi_fused_kernel<H, FMT_UV>;
+    auto kern = ndgi_fused_kernel<H, FMT_UV, CT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, L.total);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
+    // Resident CTAs per SM from the kernel's own resource use (the runtime's
+    // occupancy query reports 1 for this tcgen05 kernel on driver 580).
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    int dev = 0, smem_sm = 0, regs_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    const int regs_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (kThreads / 32);
+    const int smem_cta = (int)L.total + (int)fa.sharedSizeBytes + 1024;   // + per-CTA reserved smem
+    int occ = regs_sm / regs_cta;
+    if (smem_sm / smem_cta < occ) occ = smem_sm / smem_cta;
+    int occ_api = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_api, kern, kThreads, L.total);
     const int tmem_cap = 512 / (int)FusedCfg<H>::TM_COLS;
     if (occ > tmem_cap) occ = tmem_cap;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     if (ctas_per_sm_out) *ctas_per_sm_out = occ;
     const uint32_t cap = (uint32_t)(num_sms * occ);
     const uint32_t grid = p.units < cap ? p.units : cap;
+    if (getenv("NDGI_VERBOSE"))
+        fprintf(stderr, "[ndgi] fused<H=%d,uv=%d,C=%d> occ=%d (api %d, regs %d, local %zu) grid=%u units=%u strips=%d smem=%u\n",
+                H, FMT_UV, CT, occ, occ_api, fa.numRegs, fa.localSizeBytes, grid, p.units, p.strips_per_tile, L.total);
     kern<<<grid, kThreads, L.total, s>>>(p);
     return cudaGetLastError();
 }
 
 int fused_ctas_per_sm(int H) { return H == 16 ? 8 : 4; }
 
+template <int H, int CT>
+static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t s, int* occ) {
+    if (p.fmt_uv == FMT_BC7) return launch_fused_t<H, FMT_BC7, CT>(p, num_sms, s, occ);
+    if (p.fmt_uv == FMT_U8) return launch_fused_t<H, FMT_U8, CT>(p, num_sms, s, occ);
+    return launch_fused_t<H, FMT_F16, CT>(p, num_sms, s, occ);
+}
+
 cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s) {
     int occ = 0;
-    if (p.H == 16) {
-        if (p.fmt_uv == FMT_BC7) return launch_fused_t<16, FMT_BC7>(p, num_sms, s, &occ);
-        if (p.fmt_uv == FMT_U8) return launch_fused_t<16, FMT_U8>(p, num_sms, s, &occ);
-        return launch_fused_t<16, FMT_F16>(p, num_sms, s, &occ);
-    }
-    if (p.fmt_uv == FMT_BC7) return launch_fused_t<64, FMT_BC7>(p, num_sms, s, &occ);
-    if (p.fmt_uv == FMT_U8) return launch_fused_t<64, FMT_U8>(p, num_sms, s, &occ);
-    return launch_fused_t<64, FMT_F16>(p, num_sms, s, &occ);
+    if (p.H == 16) return p.C == 128 ? launch_fused_fmt<16, 128>(p, num_sms, s, &occ) : launch_fused_fmt<16, 256>(p, num_sms, s, &occ);
+    return p.C == 128 ? launch_fused_fmt<64, 128>(p, num_sms, s, &occ) : launch_fused_fmt<64, 256>(p, num_sms, s, &occ);
 }
 
 }  // namespace ndgi

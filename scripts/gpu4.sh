@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+python -c "import oracle; oracle.build()"
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -5 > gpurun_out/t_all.log
+NDGI_VERBOSE=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-vt > gpurun_out/b_small.log 2>&1
+echo done
