@@ -3,9 +3,10 @@
 // One persistent kernel does the whole hot path of SURVEY.md §8(a):
 //   a1  work units (query time, request, strip of core rows); call constants
 //       gamma(t), k0/k1/tau, r0/r1/rho come precomputed from the host
-//   a2  per unit: the tile's f16 MLP, the two BC7 t-slices of F_uvt, the line
-//       maps at t, and (per 2048-texel chunk) the BC7 F_uv blocks
-//   a3  BC7 decode (bc7_device.cuh) -- one block per thread -> shared memory
+//   a2  per unit: the tile's f16 MLP -> smem B operands, the two BC7 t-slices
+//       of F_uvt, the line maps at t; per 16-row chunk the BC7 F_uv blocks
+//   a3  BC7 decode (bc7_device.cuh), one block per lane, each warp decoding
+//       exactly the blocks its own texels need (no CTA barrier)
 //   a4  V_uvt: tau-blended slice (f16, smem) sampled bilinearly (f16x2 math);
 //       V_uv: the texel itself (R2); V_ut per column / V_vt per row (f16x2)
 //   a5  gamma(t): folded into layer-1's bias column (R6)
@@ -17,10 +18,14 @@
 //       constants folded into the next layer's weights
 //   a8  RGBA8 (or 16F/32F) page-cache writer: core + mirrored border (R3)
 //
-// CTA = 128 threads = 4 warps; thread t owns TMEM lane t = texel t of the
-// current 128-texel block (warp w may only touch lanes 32w..32w+31).  Several
-// CTAs per SM (TMEM: 64 columns per CTA for h = 16, 128 for h = 64) hide the
-// MMA round-trip latency of each other.
+// Warp specialisation (160 threads): warps 0-3 are texel warps -- thread t
+// owns TMEM lane t, i.e. texel t of the current 128-texel block, and does
+// gather, GELU epilogues and output; warp 4 issues the MMAs (one elected
+// lane).  S TMEM slots (4 for h = 16, 2 for h = 64) rotate: while the tensor
+// core runs a layer of slot s, the texel warps run the GELU epilogues of the
+// other slots.
+// Handshakes are mbarriers only: a_ready[s] (128 texel-thread arrivals:
+// "A operand of slot s written") and d_ready[s] (tcgen05.commit: "layer done").
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -32,22 +37,28 @@
 
 namespace ndgi {
 
-constexpr int kThreads = 128;
-constexpr int kChunkTexels = 2048;  // F_uv texels decoded per chunk (128 BC7 blocks)
+constexpr int kTexelThreads = 128;
+constexpr int kThreads = kTexelThreads + 32;   // + MMA warp
+constexpr int kMmaWarp = 4;
+constexpr int kChunkTexels = 2048;             // F_uv texels decoded per chunk (4 warps x 32 blocks x 16)
 
 template <int H>
 struct FusedCfg {
-    static constexpr int K2 = H + 16;                   // layer 2/3 K incl. bias chunk
-    static constexpr uint32_t TM_A1 = 0;                // 8 columns  (K = 16 f16)
-    static constexpr uint32_t TM_A23 = 8;               // K2/2 columns
-    static constexpr uint32_t TM_D = H == 16 ? 32 : 64; // H columns (fp32 accumulators)
-    static constexpr uint32_t TM_COLS = H == 16 ? 64 : 128;
+    static constexpr int K2 = H + 16;                    // layer 2/3 K incl. bias chunk
+    // per slot: A23 = layer-2/3 A operand (K2/2 columns); layer 1's A (K = 16,
+    // 8 columns) aliases its first 8 columns -- dead once layer 1 completes,
+    // and the bias chunk (columns H/2 .. H/2+7) is never overwritten.
+    static constexpr uint32_t TM_A1 = 0;
+    static constexpr uint32_t TM_A23 = 0;
+    static constexpr uint32_t TM_D = H == 16 ? 16 : 64;  // H columns (fp32 accumulators)
+    static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
+    static constexpr int SLOTS = H == 16 ? 4 : 2;         // items in flight per texel warp
+    static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS;
     static constexpr int B1_BYTES = H * 16 * 2;
     static constexpr int B2_BYTES = H * K2 * 2;
     static constexpr int B3_BYTES = 16 * K2 * 2;
-    static constexpr int B_BYTES = B1_BYTES + B2_BYTES + B3_BYTES;
     static_assert(TM_A23 + K2 / 2 <= TM_D, "TMEM layout");
-    static_assert(TM_D + H <= TM_COLS, "TMEM layout");
+    static_assert(TM_D + H <= SLOT_COLS, "TMEM layout");
 };
 
 // element (n, k) of a K-major no-swizzle operand with Kt columns:
@@ -77,8 +88,8 @@ __device__ __forceinline__ void u8x4_to_h2(uint32_t q, uint32_t& rg, uint32_t& b
 }
 
 struct FusedSmem {
-    // offsets in bytes from the dynamic smem base
-    uint32_t b1, b2, b3, uvt, uvc, utcol, vtrow, bar, tmem_slot, total;
+    // byte offsets from the dynamic smem base
+    uint32_t b1, b2, b3, uvt, uvc, utcol, vtrow, bars, tmem_slot, total;
 };
 
 template <int H>
@@ -91,38 +102,58 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
     s.b3 = o; o += Cfg::B3_BYTES;
     o = (o + 127) & ~127u;
     s.uvt = o; o += (uint32_t)(R3 * R3 * 8);         // blended slice, f16x4 per texel
-    s.uvc = o; o += kChunkTexels * 4;                 // decoded F_uv chunk, RGBA8
+    s.uvc = o; o += kChunkTexels * 4;                 // decoded F_uv chunk, RGBA8 (4 per-warp parts)
     s.utcol = o; o += (uint32_t)(C * 4);              // V_ut per column, f16x2
     s.vtrow = o; o += (uint32_t)(C * 4);              // V_vt per row, f16x2
     o = (o + 15) & ~15u;
-    s.bar = o; o += 8;
+    s.bars = o; o += 16 * 8;                          // a_ready[SLOTS], d_ready[SLOTS] (<= 8 each)
     s.tmem_slot = o; o += 8;
     s.total = o;
     return s;
 }
 
+// ---- GELU epilogue of one layer: D (fp32) -> f16x2 GELU~ -> A23 ---------------
+template <int H>
+__device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) {
+#pragma unroll
+    for (int c0 = 0; c0 < H; c0 += 16) {
+        uint32_t d[16], g[8];
+        ptx::tmem_ld_x16(d_addr + c0, d);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
+        ptx::tmem_st_x8(a_addr + c0 / 2, g);
+    }
+}
+
 template <int H, int FMT_UV, int CT>
-__global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kThreads, H == 16 ? 4 : 2) ndgi_fused_kernel(const __grid_constant__ KParams p) {
     using Cfg = FusedCfg<H>;
-    constexpr int C = CT;                      // core texels per tile side (128 or 256)
-    constexpr int BPR = CT / kThreads;         // 128-texel MMA blocks per row
+    constexpr int C = CT;                       // core texels per tile side (128 or 256)
+    constexpr int BPR = CT / kTexelThreads;     // 128-texel MMA blocks per row
     constexpr int chunk_rows = kChunkTexels / CT;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const FusedSmem L = fused_smem_layout<H>(p.C, p.R3);
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const uint32_t bar = ptx::smem_addr(smem + L.bar);
+    const FusedSmem L = fused_smem_layout<H>(C, p.R3);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t bars = ptx::smem_addr(smem + L.bars);
+    constexpr int S = Cfg::SLOTS;
+    auto a_ready = [&](int s) { return bars + 8u * s; };
+    auto d_ready = [&](int s) { return bars + 64u + 8u * s; };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
     __half* sB1 = reinterpret_cast<__half*>(smem + L.b1);
     __half* sB2 = reinterpret_cast<__half*>(smem + L.b2);
     __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
     uint2* sUvt = reinterpret_cast<uint2*>(smem + L.uvt);
-    uint32_t* sUvc = reinterpret_cast<uint32_t*>(smem + L.uvc);
     uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
     uint32_t* sVt = reinterpret_cast<uint32_t*>(smem + L.vtrow);
 
-    // ---- one-time setup: mbarrier, TMEM allocation --------------------------
+    // ---- one-time setup: mbarriers, TMEM allocation ---------------------------
     if (tid == 0) {
-        ptx::mbar_init(bar, 1);
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(a_ready(s), kTexelThreads);
+            ptx::mbar_init(d_ready(s), 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 0) ptx::tmem_alloc<Cfg::TM_COLS>(ptx::smem_addr(tmem_slot));
@@ -130,39 +161,20 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
-
-    // constant part of the layer-2/3 A operand: the bias chunk [1, 0, ..., 0]
-    {
-        uint32_t c[8] = {0x00003C00u, 0, 0, 0, 0, 0, 0, 0};
-        ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A23 + H / 2, c);
-        ptx::tmem_wait_st();
-    }
 
     const int B = p.B, P = p.P, R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
-    const uint32_t idesc1 = ptx::idesc_f16_f32(128, H);
-    const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
-    const uint32_t sb1 = ptx::smem_addr(sB1), sb2 = ptx::smem_addr(sB2), sb3 = ptx::smem_addr(sB3);
-    uint32_t phase = 0;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;  // texel warp's TMEM lane quarter
 
-    // issue one layer (K steps of 16) and wait for it; all threads participate
-    auto run_layer = [&](uint32_t a_col, uint32_t b_saddr, int kt, uint32_t idesc) {
+    if (warp < 4) {
+        // constant part of the layer-2/3 A operand of every slot: bias chunk [1, 0, ..., 0]
+        uint32_t c[8] = {0x00003C00u, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int s = 0; s < S; ++s) ptx::tmem_st_x8(tmem + s * Cfg::SLOT_COLS + lane_base + Cfg::TM_A23 + H / 2, c);
         ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            ptx::tc_fence_after();
-            const uint32_t sbo = (uint32_t)(kt >> 3) * 128u;
-            for (int s = 0; s < kt / 16; ++s)
-                ptx::mma_f16_ts(tmem + Cfg::TM_D, tmem + a_col + 8u * s,
-                                ptx::smem_desc_kmajor(b_saddr + 256u * s, 128u, sbo), idesc, s > 0);
-            ptx::mma_commit(bar);
-        }
-        ptx::mbar_wait(bar, phase);
-        phase ^= 1u;
-        ptx::tc_fence_after();
-    };
+    }
+
+    uint32_t aph = 0u, dph = 0u;   // mbarrier phase bits per slot (MMA warp / texel warps)
 
     for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
         const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
@@ -171,8 +183,8 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
         const uint32_t r = rq % p.n_req;
         const TConst& tc = p.tc[ti];
         int k;
-        size_t out_base;  // texel index of core texel (0,0)
-        size_t row_pitch; // texels between rows
+        size_t out_base;   // texel index of core texel (0,0)
+        size_t row_pitch;  // texels between rows
         if (p.full) {
             k = (int)r;
             const int tx = k % p.tiles_x, ty = (k / p.tiles_x) % p.tiles_y, a = k / (p.tiles_x * p.tiles_y);
@@ -190,9 +202,11 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
             row_pitch = (size_t)P;
             out_base = ((size_t)slot * P + B) * P + B;
         }
+        const int nitems = p.strip_rows * BPR;     // 128-texel blocks of this unit (multiple of S)
+        const int j_begin = strip * p.strip_rows;
 
-        // ---- a2: tile parameters -> shared memory ---------------------------------
-        __syncthreads();  // previous unit's smem readers are done
+        // ---- a2: tile parameters -> shared memory (all 160 threads) ---------------
+        ptx::named_bar_sync(1, kThreads);  // previous unit: all MMAs issued and read back
         {
             const uint16_t* w = p.mlp + p.mlp_tile_elems * k;
             const uint16_t *W1 = w, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
@@ -212,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
                 }
                 sB1[bofs(n, kk, 16)] = __float2half_rn(v);
             }
-            // layer 2: [H][H+16]: 0.5*W2 (absorbs 1/(2a) of GELU and a of the next pre-scale), bias a*b2
+            // layer 2: [H][H+16]: 0.5*W2 (absorbs 1/(2a) of GELU~ and a of the next pre-scale), bias a*b2
             for (int e = tid; e < H * Cfg::K2; e += kThreads) {
                 const int n = e / Cfg::K2, kk = e % Cfg::K2;
                 float v = 0.f;
@@ -276,10 +290,11 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
             const uint8_t* ut = p.ut + p.line_tile_bytes * k;
             const uint8_t* vt = p.vt + p.line_tile_bytes * k;
             const float rho = tc.rho, omr = 1.0f - rho;
+            const float scu = (float)p.U * (1.0f / (float)C);
             for (int e = tid; e < 2 * C; e += kThreads) {
                 const int i = e % C;
                 const uint8_t* m = e < C ? ut : vt;
-                const float sx = fmaf((float)i + 0.5f, (float)p.U * (1.0f / (float)C), -0.5f);
+                const float sx = fmaf((float)i + 0.5f, scu, -0.5f);
                 const float fl = floorf(sx), fx = sx - fl;
                 const int x0 = clampi((int)fl, 0, p.U - 1), x1 = clampi((int)fl + 1, 0, p.U - 1);
                 float c[2];
@@ -305,15 +320,51 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
             }
         }
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
-        __syncthreads();
+        ptx::named_bar_sync(1, kThreads);
 
-        // ---- rows of this strip ------------------------------------------------------
+        if (warp == kMmaWarp) {
+            // ================= MMA issuer: per group of S items, layers 1..3, slots 0..S-1 ====
+            if (lane == 0) {
+                const uint32_t idesc1 = ptx::idesc_f16_f32(128, H);
+                const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
+                const uint32_t sb1 = ptx::smem_addr(sB1), sb2 = ptx::smem_addr(sB2), sb3 = ptx::smem_addr(sB3);
+                const uint64_t bd1 = ptx::smem_desc_kmajor(sb1, 128u, 256u);
+                constexpr uint32_t sbo2 = (uint32_t)(Cfg::K2 / 8) * 128u;
+                for (int g = 0; g < nitems / S; ++g) {
+#pragma unroll 1
+                    for (int l = 0; l < 3; ++l) {
+                        const uint32_t sb = l == 1 ? sb2 : sb3;
+                        const uint32_t id = l == 2 ? idesc3 : idesc1;
+#pragma unroll 1
+                        for (int s = 0; s < S; ++s) {
+                            ptx::mbar_wait(a_ready(s), (aph >> s) & 1u);
+                            aph ^= 1u << s;
+                            ptx::tc_fence_after();
+                            const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
+                            if (l == 0) {
+                                ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A1, bd1, idesc1, 0u);
+                            } else {
+#pragma unroll
+                                for (int st = 0; st < Cfg::K2 / 16; ++st)
+                                    ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A23 + 8u * st,
+                                                    ptx::smem_desc_kmajor(sb + 256u * st, 128u, sbo2), id, st > 0);
+                            }
+                            ptx::mma_commit(d_ready(s));
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            continue;
+        }
+
+        // ===================== texel warps ==========================================
         // per-thread column constants (thread tid owns columns b*128 + tid)
         int cx0[BPR], cx1[BPR];
         uint32_t cfx[BPR], cut[BPR];
 #pragma unroll
         for (int b = 0; b < BPR; ++b) {
-            const int i = b * kThreads + tid;
+            const int i = b * kTexelThreads + tid;
             const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
             const float flx = floorf(sx);
             cx0[b] = clampi((int)flx, 0, R3 - 1);
@@ -321,106 +372,118 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
             cfx[b] = pack_f16x2(sx - flx, sx - flx);
             cut[b] = sUt[i];
         }
-        const int j_begin = strip * p.strip_rows, j_end = j_begin + p.strip_rows;
         const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
-        for (int jc = j_begin; jc < j_end; jc += chunk_rows) {
+        // this warp's decoded F_uv chunk: [row][blk][32 columns] RGBA8
+        uint32_t* sUvw = reinterpret_cast<uint32_t*>(smem + L.uvc) + warp * (chunk_rows * BPR * 32);
+
+        // a3: this warp's 32 BC7 blocks of the chunk starting at core row jc
+        auto decode_chunk = [&](int jc) {
+            if (FMT_UV != FMT_BC7) return;
+            constexpr int bpw = 8 * BPR;                    // blocks per block-row for this warp
+            const int br = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
+            const int gbc = 32 * blk + 8 * warp + bc;       // block column in the tile
+            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + br) * (C >> 2) + gbc);
+            uint32_t* dst = sUvw + ((4 * br) * BPR + blk) * 32 + 4 * bc;
+            uint32_t rowv[4];
+            __syncwarp();   // previous chunk fully gathered by this warp
+            bc7_decode(raw, [&](int i, uint32_t v) {
+                rowv[i & 3] = v;
+                if ((i & 3) == 3)
+                    *reinterpret_cast<uint4*>(dst + (i >> 2) * BPR * 32) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
+            });
+            __syncwarp();
+        };
+
+        // a4/a6: Eq. 4 input row of block `item` -> A1 of slot s, then arrive
+        auto gather = [&](int item, int s) {
+            const int row = j_begin + item / BPR, blk = item % BPR;
+            const int jr = row % chunk_rows;
+            if (jr == 0 && blk == 0) decode_chunk(row);
+            const float sy = fmaf((float)row + 0.5f, sc3, -0.5f);
+            const float fly = floorf(sy);
+            const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
+            const uint32_t fy2 = pack_f16x2(sy - fly, sy - fly);
+            const int i = blk * kTexelThreads + tid;
+            const int x0 = cx0[blk], x1 = cx1[blk];
+            const uint32_t fx2 = cfx[blk];
+            const uint2 t00 = sUvt[y0 * R3 + x0], t10 = sUvt[y0 * R3 + x1];
+            const uint2 t01 = sUvt[y1 * R3 + x0], t11 = sUvt[y1 * R3 + x1];
+            uint32_t a1[8];
+            a1[0] = hlerp2(hlerp2(t00.x, t10.x, fx2), hlerp2(t01.x, t11.x, fx2), fy2);
+            a1[1] = hlerp2(hlerp2(t00.y, t10.y, fx2), hlerp2(t01.y, t11.y, fx2), fy2);
             if (FMT_UV == FMT_BC7) {
-                // a3: 128 BC7 blocks of F_uv (rows jc .. jc+chunk_rows) -> smem RGBA8
-                constexpr int bpr = C >> 2;
-                const int brow = tid / bpr, bcol = tid % bpr;
-                const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + brow) * bpr + bcol);
-                uint32_t* dst = sUvc + (brow * 4) * C + bcol * 4;
-                uint32_t rowv[4];
-                bc7_decode(raw, [&](int i, uint32_t v) {
-                    rowv[i & 3] = v;
-                    if ((i & 3) == 3) *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
-                });
-                __syncthreads();
+                u8x4_to_h2(sUvw[(jr * BPR + blk) * 32 + lane], a1[2], a1[3]);
+            } else if (FMT_UV == FMT_U8) {
+                u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + i), a1[2], a1[3]);
+            } else {
+                const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)row * C + i);
+                a1[2] = hv.x;
+                a1[3] = hv.y;
             }
-            for (int jr = 0; jr < chunk_rows; ++jr) {
-                const int j = jc + jr;
-                // per-row constants (uniform): uvt y taps
-                const float sy = fmaf((float)j + 0.5f, sc3, -0.5f);
-                const float fly = floorf(sy);
-                const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
-                const uint32_t fy2 = pack_f16x2(sy - fly, sy - fly);
-                const uint32_t vtv = sVt[j];
-#pragma unroll
-                for (int blk = 0; blk < BPR; ++blk) {
-                    const int i = blk * kThreads + tid;
-                    // ---- a4/a6: gather the Eq. 4 input row of texel (i, j) ----
-                    const int x0 = cx0[blk], x1 = cx1[blk];
-                    const uint32_t fx2 = cfx[blk];
-                    const uint2 t00 = sUvt[y0 * R3 + x0], t10 = sUvt[y0 * R3 + x1];
-                    const uint2 t01 = sUvt[y1 * R3 + x0], t11 = sUvt[y1 * R3 + x1];
-                    uint32_t a1[8];
-                    a1[0] = hlerp2(hlerp2(t00.x, t10.x, fx2), hlerp2(t01.x, t11.x, fx2), fy2);
-                    a1[1] = hlerp2(hlerp2(t00.y, t10.y, fx2), hlerp2(t01.y, t11.y, fx2), fy2);
-                    if (FMT_UV == FMT_BC7) {
-                        u8x4_to_h2(sUvc[jr * C + i], a1[2], a1[3]);
-                    } else if (FMT_UV == FMT_U8) {
-                        u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)j * C + i), a1[2], a1[3]);
-                    } else {
-                        const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)j * C + i);
-                        a1[2] = hv.x;
-                        a1[3] = hv.y;
-                    }
-                    a1[4] = cut[blk];
-                    a1[5] = vtv;
-                    a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
-                    a1[7] = 0u;
-                    ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A1, a1);
+            a1[4] = cut[blk];
+            a1[5] = sVt[row];
+            a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
+            a1[7] = 0u;
+            ptx::tmem_st_x8(tmem + s * Cfg::SLOT_COLS + lane_base + Cfg::TM_A1, a1);
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(a_ready(s));
+        };
 
-                    // ---- a7: layer 1 ----
-                    run_layer(Cfg::TM_A1, sb1, 16, idesc1);
-                    // epilogue 1: GELU -> A23
-#pragma unroll
-                    for (int c0 = 0; c0 < H; c0 += 16) {
-                        uint32_t d[16], g[8];
-                        ptx::tmem_ld_x16(tmem + lane_base + Cfg::TM_D + c0, d);
-                        ptx::tmem_wait_ld();
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
-                        ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A23 + c0 / 2, g);
-                    }
-                    // ---- layer 2 ----
-                    run_layer(Cfg::TM_A23, sb2, Cfg::K2, idesc1);
-#pragma unroll
-                    for (int c0 = 0; c0 < H; c0 += 16) {
-                        uint32_t d[16], g[8];
-                        ptx::tmem_ld_x16(tmem + lane_base + Cfg::TM_D + c0, d);
-                        ptx::tmem_wait_ld();
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
-                        ptx::tmem_st_x8(tmem + lane_base + Cfg::TM_A23 + c0 / 2, g);
-                    }
-                    // ---- layer 3 ----
-                    run_layer(Cfg::TM_A23, sb3, Cfg::K2, idesc3);
-                    uint32_t yv[4];
-                    ptx::tmem_ld_x4(tmem + lane_base + Cfg::TM_D, yv);
-                    ptx::tmem_wait_ld();
-                    const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
+        auto wait_d = [&](int s) {
+            ptx::mbar_wait(d_ready(s), (dph >> s) & 1u);
+            dph ^= 1u << s;
+            ptx::tc_fence_after();
+        };
 
-                    // ---- a8: page-cache writer (core + mirrored border, R3) ----
-                    const size_t o = out_base + (size_t)j * row_pitch + i;
-                    store_texel(p.out, o, p.out_fmt, y0f, y1f, y2f);
-                    if (!p.full && B > 0) {
-                        const bool bx = (i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2);
-                        const bool by = (j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2);
-                        if (bx || by) {
-                            // mirrored positions: core i -> padded-core offsets -i and 2(C-1)-i
-                            const int xm = i <= B ? -i : 2 * (C - 1) - i;
-                            const int ym = j <= B ? -j : 2 * (C - 1) - j;
-                            const ptrdiff_t base = (ptrdiff_t)out_base;
-                            const ptrdiff_t rp = (ptrdiff_t)row_pitch;
-                            if (bx) store_texel(p.out, (size_t)(base + (ptrdiff_t)j * rp + xm), p.out_fmt, y0f, y1f, y2f);
-                            if (by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + i), p.out_fmt, y0f, y1f, y2f);
-                            if (bx && by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + xm), p.out_fmt, y0f, y1f, y2f);
-                        }
-                    }
+        auto epilogue = [&](int s) {
+            const uint32_t slot = tmem + s * Cfg::SLOT_COLS + lane_base;
+            gelu_epilogue<H>(slot + Cfg::TM_D, slot + Cfg::TM_A23);
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(a_ready(s));
+        };
+
+        // a8: y of block `item` (slot s) -> page cache
+        auto output = [&](int item, int s) {
+            const int j = j_begin + item / BPR, i = (item % BPR) * kTexelThreads + tid;
+            uint32_t yv[4];
+            ptx::tmem_ld_x4(tmem + s * Cfg::SLOT_COLS + lane_base + Cfg::TM_D, yv);
+            ptx::tmem_wait_ld();
+            const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
+            const size_t o = out_base + (size_t)j * row_pitch + i;
+            store_texel(p.out, o, p.out_fmt, y0f, y1f, y2f);
+            if (!p.full && B > 0) {
+                const bool bx = (i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2);
+                const bool by = (j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2);
+                if (bx || by) {
+                    // mirrored positions (R3): core i -> padded-core offsets -i and 2(C-1)-i
+                    const int xm = i <= B ? -i : 2 * (C - 1) - i;
+                    const int ym = j <= B ? -j : 2 * (C - 1) - j;
+                    const ptrdiff_t base = (ptrdiff_t)out_base, rp = (ptrdiff_t)row_pitch;
+                    if (bx) store_texel(p.out, (size_t)(base + (ptrdiff_t)j * rp + xm), p.out_fmt, y0f, y1f, y2f);
+                    if (by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + i), p.out_fmt, y0f, y1f, y2f);
+                    if (bx && by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + xm), p.out_fmt, y0f, y1f, y2f);
                 }
+            }
+        };
+
+#pragma unroll 1
+        for (int s = 0; s < S; ++s) gather(s, s);
+        for (int it = 0; it < nitems; it += S) {
+#pragma unroll 1
+            for (int l = 0; l < 2; ++l) {
+#pragma unroll 1
+                for (int s = 0; s < S; ++s) {   // layer l+1 done for slot s -> GELU -> A of layer l+2
+                    wait_d(s);
+                    epilogue(s);
+                }
+            }
+#pragma unroll 1
+            for (int s = 0; s < S; ++s) {       // layer 3 done -> y -> page cache; refill the slot
+                wait_d(s);
+                output(it + s, s);
+                if (it + S + s < nitems) gather(it + S + s, s);
             }
         }
     }
@@ -433,15 +496,15 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 8 : 4) ndgi_fused_kernel(c
 
 // ---- host-side launch helpers ---------------------------------------------------
 template <int H, int FMT_UV, int CT>
-static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s, int* ctas_per_sm_out) {
-    const FusedSmem L = fused_smem_layout<H>(p.C, p.R3);
+static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
+    const FusedSmem L = fused_smem_layout<H>(CT, p.R3);
     auto kern = ndgi_fused_kernel<H, FMT_UV, CT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     // Resident CTAs per SM from the kernel's own resource use (the runtime's
-    // occupancy query reports 1 for this tcgen05 kernel on driver 580).
+    // occupancy query reports 1 for tcgen05 kernels on driver 580).
     cudaFuncAttributes fa;
     e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
@@ -453,34 +516,30 @@ static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s,
     const int smem_cta = (int)L.total + (int)fa.sharedSizeBytes + 1024;   // + per-CTA reserved smem
     int occ = regs_sm / regs_cta;
     if (smem_sm / smem_cta < occ) occ = smem_sm / smem_cta;
-    int occ_api = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_api, kern, kThreads, L.total);
     const int tmem_cap = 512 / (int)FusedCfg<H>::TM_COLS;
     if (occ > tmem_cap) occ = tmem_cap;
     if (occ < 1) return cudaErrorInvalidConfiguration;
-    if (ctas_per_sm_out) *ctas_per_sm_out = occ;
     const uint32_t cap = (uint32_t)(num_sms * occ);
     const uint32_t grid = p.units < cap ? p.units : cap;
     if (getenv("NDGI_VERBOSE"))
-        fprintf(stderr, "[ndgi] fused<H=%d,uv=%d,C=%d> occ=%d (api %d, regs %d, local %zu) grid=%u units=%u strips=%d smem=%u\n",
-                H, FMT_UV, CT, occ, occ_api, fa.numRegs, fa.localSizeBytes, grid, p.units, p.strips_per_tile, L.total);
+        fprintf(stderr, "[ndgi] fused<H=%d,uv=%d,C=%d> occ=%d (regs %d, local %zu) grid=%u units=%u strips=%d smem=%u\n",
+                H, FMT_UV, CT, occ, fa.numRegs, fa.localSizeBytes, grid, p.units, p.strips_per_tile, L.total);
     kern<<<grid, kThreads, L.total, s>>>(p);
     return cudaGetLastError();
 }
 
-int fused_ctas_per_sm(int H) { return H == 16 ? 8 : 4; }
+int fused_ctas_per_sm(int H) { return 512 / (H == 16 ? (int)FusedCfg<16>::TM_COLS : (int)FusedCfg<64>::TM_COLS); }
 
 template <int H, int CT>
-static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t s, int* occ) {
-    if (p.fmt_uv == FMT_BC7) return launch_fused_t<H, FMT_BC7, CT>(p, num_sms, s, occ);
-    if (p.fmt_uv == FMT_U8) return launch_fused_t<H, FMT_U8, CT>(p, num_sms, s, occ);
-    return launch_fused_t<H, FMT_F16, CT>(p, num_sms, s, occ);
+static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t s) {
+    if (p.fmt_uv == FMT_BC7) return launch_fused_t<H, FMT_BC7, CT>(p, num_sms, s);
+    if (p.fmt_uv == FMT_U8) return launch_fused_t<H, FMT_U8, CT>(p, num_sms, s);
+    return launch_fused_t<H, FMT_F16, CT>(p, num_sms, s);
 }
 
 cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s) {
-    int occ = 0;
-    if (p.H == 16) return p.C == 128 ? launch_fused_fmt<16, 128>(p, num_sms, s, &occ) : launch_fused_fmt<16, 256>(p, num_sms, s, &occ);
-    return p.C == 128 ? launch_fused_fmt<64, 128>(p, num_sms, s, &occ) : launch_fused_fmt<64, 256>(p, num_sms, s, &occ);
+    if (p.H == 16) return p.C == 128 ? launch_fused_fmt<16, 128>(p, num_sms, s) : launch_fused_fmt<16, 256>(p, num_sms, s);
+    return p.C == 128 ? launch_fused_fmt<64, 128>(p, num_sms, s) : launch_fused_fmt<64, 256>(p, num_sms, s);
 }
 
 }  // namespace ndgi
