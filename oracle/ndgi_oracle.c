@@ -541,11 +541,14 @@ void oracle_quantize_rgba8_f64(const double *y3, size_t n, uint8_t *out)
 
 void oracle_quantize_rgba8_f32(const float *y, size_t stride, size_t n, uint8_t *out)
 {
+    /* the clamp is taken in fp32 (the kernel's precision); the product
+     * clamp(y)*255 is exact in double, so nearbyint rounds the exact value
+     * (RN-even) as R12 defines -- no intermediate fp32 rounding of the product */
     for (size_t i = 0; i < n; ++i) {
         for (int c = 0; c < 3; ++c) {
             float v = y[stride * i + c];
             v = fminf(fmaxf(v, 0.0f), 1.0f);
-            out[4 * i + c] = (uint8_t)nearbyintf(v * 255.0f);
+            out[4 * i + c] = (uint8_t)nearbyint((double)v * 255.0);
         }
         out[4 * i + 3] = 255;
     }

@@ -18,18 +18,16 @@
 //       constants folded into the next layer's weights
 //   a8  RGBA8 (or 16F/32F) page-cache writer: core + mirrored border (R3)
 //
-// Warp specialisation (160 threads): warps 0-3 are texel warps -- thread t
-// owns TMEM lane t, i.e. texel t of the current 128-texel block, and does
-// gather, GELU epilogues and output; warp 4 issues the MMAs (one elected
-// lane).  S TMEM slots (4 for h = 16, 2 for h = 64) rotate: while the tensor
-// core runs a layer of slot s, the texel warps run the GELU epilogues of the
-// other slots.
-// Handshakes are mbarriers only: a_ready[s] (128 texel-thread arrivals:
-// "A operand of slot s written") and d_ready[s] (tcgen05.commit: "layer done").
+// CTA = 4 warps; thread t owns TMEM lane t, i.e. texel t of each 128-texel
+// item.  A step carries S items (S TMEM slots: 2 for h = 16, 1 for h = 64)
+// through the three layers together: per layer one CTA barrier, S (x K/16)
+// tcgen05.mma issued by one elected lane, one tcgen05.commit -> mbarrier.
+// Several CTAs per SM (6 for h = 16) hide each other's MMA latency.
 #include <cuda_runtime.h>
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "bc7_device.cuh"
 #include "ndgi_common.cuh"
@@ -37,9 +35,7 @@
 
 namespace ndgi {
 
-constexpr int kTexelThreads = 128;
-constexpr int kThreads = kTexelThreads + 32;   // + MMA warp
-constexpr int kMmaWarp = 4;
+constexpr int kThreads = 128;
 constexpr int kChunkTexels = 2048;             // F_uv texels decoded per chunk (4 warps x 32 blocks x 16)
 
 template <int H>
@@ -52,8 +48,9 @@ struct FusedCfg {
     static constexpr uint32_t TM_A23 = 0;
     static constexpr uint32_t TM_D = H == 16 ? 16 : 64;  // H columns (fp32 accumulators)
     static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
-    static constexpr int SLOTS = H == 16 ? 4 : 2;         // items in flight per texel warp
-    static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS;
+    static constexpr int SLOTS = H == 16 ? 2 : 1;        // 128-texel items per MMA step (one TMEM slot each)
+    static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS < 32 ? 32 : SLOTS * SLOT_COLS;
+    static constexpr int MIN_CTAS = H == 16 ? 6 : 4;     // register budget: 85 / 128 per thread
     static constexpr int B1_BYTES = H * 16 * 2;
     static constexpr int B2_BYTES = H * K2 * 2;
     static constexpr int B3_BYTES = 16 * K2 * 2;
@@ -89,7 +86,7 @@ __device__ __forceinline__ void u8x4_to_h2(uint32_t q, uint32_t& rg, uint32_t& b
 
 struct FusedSmem {
     // byte offsets from the dynamic smem base
-    uint32_t b1, b2, b3, uvt, uvc, utcol, vtrow, bars, tmem_slot, total;
+    uint32_t b1, b2, b3, uvt, uvc, utcol, rowtab, cnt, bars, tmem_slot, total;
 };
 
 template <int H>
@@ -104,9 +101,10 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
     s.uvt = o; o += (uint32_t)(R3 * R3 * 8);         // blended slice, f16x4 per texel
     s.uvc = o; o += kChunkTexels * 4;                 // decoded F_uv chunk, RGBA8 (4 per-warp parts)
     s.utcol = o; o += (uint32_t)(C * 4);              // V_ut per column, f16x2
-    s.vtrow = o; o += (uint32_t)(C * 4);              // V_vt per row, f16x2
     o = (o + 15) & ~15u;
-    s.bars = o; o += 16 * 8;                          // a_ready[SLOTS], d_ready[SLOTS] (<= 8 each)
+    s.rowtab = o; o += (uint32_t)(C * 16);            // per core row: y0*R3, y1*R3, fy (f16x2), V_vt (f16x2)
+    s.cnt = o; o += 8 * 4;                            // (unused)
+    s.bars = o; o += 8 * 8;                           // d_ready
     s.tmem_slot = o; o += 8;
     s.total = o;
     return s;
@@ -128,32 +126,28 @@ __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) 
 }
 
 template <int H, int FMT_UV, int CT>
-__global__ void __launch_bounds__(kThreads, H == 16 ? 4 : 2) ndgi_fused_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_kernel(const __grid_constant__ KParams p) {
     using Cfg = FusedCfg<H>;
+    constexpr int S = Cfg::SLOTS;
     constexpr int C = CT;                       // core texels per tile side (128 or 256)
-    constexpr int BPR = CT / kTexelThreads;     // 128-texel MMA blocks per row
+    constexpr int BPR = CT / kThreads;          // 128-texel MMA blocks per row
     constexpr int chunk_rows = kChunkTexels / CT;
     extern __shared__ __align__(1024) uint8_t smem[];
     const FusedSmem L = fused_smem_layout<H>(C, p.R3);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t bars = ptx::smem_addr(smem + L.bars);
-    constexpr int S = Cfg::SLOTS;
-    auto a_ready = [&](int s) { return bars + 8u * s; };
-    auto d_ready = [&](int s) { return bars + 64u + 8u * s; };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
     __half* sB1 = reinterpret_cast<__half*>(smem + L.b1);
     __half* sB2 = reinterpret_cast<__half*>(smem + L.b2);
     __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
     uint2* sUvt = reinterpret_cast<uint2*>(smem + L.uvt);
     uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
-    uint32_t* sVt = reinterpret_cast<uint32_t*>(smem + L.vtrow);
+    uint4* sRow = reinterpret_cast<uint4*>(smem + L.rowtab);
 
-    // ---- one-time setup: mbarriers, TMEM allocation ---------------------------
+    // ---- one-time setup: counters, mbarriers, TMEM allocation -------------------
+    if (tid < 8) reinterpret_cast<uint32_t*>(smem + L.cnt)[tid] = 0u;
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(a_ready(s), kTexelThreads);
-            ptx::mbar_init(d_ready(s), 1);
-        }
+        ptx::mbar_init(bars, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 0) ptx::tmem_alloc<Cfg::TM_COLS>(ptx::smem_addr(tmem_slot));
@@ -164,17 +158,17 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 4 : 2) ndgi_fused_kernel(c
 
     const int B = p.B, P = p.P, R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;  // texel warp's TMEM lane quarter
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
+    const uint32_t tm_lane = tmem + lane_base;
 
-    if (warp < 4) {
-        // constant part of the layer-2/3 A operand of every slot: bias chunk [1, 0, ..., 0]
+    {   // constant part of the layer-2/3 A operand of every slot: bias chunk [1, 0, ..., 0]
         uint32_t c[8] = {0x00003C00u, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-        for (int s = 0; s < S; ++s) ptx::tmem_st_x8(tmem + s * Cfg::SLOT_COLS + lane_base + Cfg::TM_A23 + H / 2, c);
+        for (int s = 0; s < S; ++s) ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23 + H / 2, c);
         ptx::tmem_wait_st();
     }
 
-    uint32_t aph = 0u, dph = 0u;   // mbarrier phase bits per slot (MMA warp / texel warps)
+    uint32_t dph = 0u;   // d_ready phase
 
     for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
         const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
@@ -205,8 +199,8 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 4 : 2) ndgi_fused_kernel(c
         const int nitems = p.strip_rows * BPR;     // 128-texel blocks of this unit (multiple of S)
         const int j_begin = strip * p.strip_rows;
 
-        // ---- a2: tile parameters -> shared memory (all 160 threads) ---------------
-        ptx::named_bar_sync(1, kThreads);  // previous unit: all MMAs issued and read back
+        // ---- a2: tile parameters -> shared memory -----------------------------------
+        __syncthreads();  // previous unit's MMAs complete and all smem readers done
         {
             const uint16_t* w = p.mlp + p.mlp_tile_elems * k;
             const uint16_t *W1 = w, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
@@ -316,69 +310,50 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 4 : 2) ndgi_fused_kernel(c
                     float v = (1.f - fx) * omr * v00 + fx * omr * v10 + (1.f - fx) * rho * v01 + fx * rho * v11;
                     c[q] = p.fmt_line == FMT_U8 ? v * (1.0f / 255.0f) : v;
                 }
-                (e < C ? sUt : sVt)[i] = pack_f16x2(c[0], c[1]);
+                if (e < C) {
+                    sUt[i] = pack_f16x2(c[0], c[1]);
+                } else {
+                    // per-row gather table: F_uvt y taps and weight, V_vt
+                    const float sy = fmaf((float)i + 0.5f, sc3, -0.5f);
+                    const float fly = floorf(sy);
+                    const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
+                    sRow[i] = make_uint4((uint32_t)(y0 * R3) * 8u, (uint32_t)(y1 * R3) * 8u, pack_f16x2(sy - fly, sy - fly),
+                                         pack_f16x2(c[0], c[1]));
+                }
             }
         }
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
-        ptx::named_bar_sync(1, kThreads);
+        __syncthreads();
 
-        if (warp == kMmaWarp) {
-            // ================= MMA issuer: per group of S items, layers 1..3, slots 0..S-1 ====
-            if (lane == 0) {
-                const uint32_t idesc1 = ptx::idesc_f16_f32(128, H);
-                const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
-                const uint32_t sb1 = ptx::smem_addr(sB1), sb2 = ptx::smem_addr(sB2), sb3 = ptx::smem_addr(sB3);
-                const uint64_t bd1 = ptx::smem_desc_kmajor(sb1, 128u, 256u);
-                constexpr uint32_t sbo2 = (uint32_t)(Cfg::K2 / 8) * 128u;
-                for (int g = 0; g < nitems / S; ++g) {
-#pragma unroll 1
-                    for (int l = 0; l < 3; ++l) {
-                        const uint32_t sb = l == 1 ? sb2 : sb3;
-                        const uint32_t id = l == 2 ? idesc3 : idesc1;
-#pragma unroll 1
-                        for (int s = 0; s < S; ++s) {
-                            ptx::mbar_wait(a_ready(s), (aph >> s) & 1u);
-                            aph ^= 1u << s;
-                            ptx::tc_fence_after();
-                            const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
-                            if (l == 0) {
-                                ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A1, bd1, idesc1, 0u);
-                            } else {
-#pragma unroll
-                                for (int st = 0; st < Cfg::K2 / 16; ++st)
-                                    ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A23 + 8u * st,
-                                                    ptx::smem_desc_kmajor(sb + 256u * st, 128u, sbo2), id, st > 0);
-                            }
-                            ptx::mma_commit(d_ready(s));
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            continue;
-        }
-
-        // ===================== texel warps ==========================================
-        // per-thread column constants (thread tid owns columns b*128 + tid)
-        int cx0[BPR], cx1[BPR];
-        uint32_t cfx[BPR], cut[BPR];
+        // per-thread column constants (thread tid owns columns b*128 + tid):
+        // byte offsets of the two F_uvt x taps in the blended slice, x weight, V_ut
+        uint32_t cxb0[BPR], cxb1[BPR], cfx[BPR], cut[BPR];
 #pragma unroll
         for (int b = 0; b < BPR; ++b) {
-            const int i = b * kTexelThreads + tid;
+            const int i = b * kThreads + tid;
             const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
             const float flx = floorf(sx);
-            cx0[b] = clampi((int)flx, 0, R3 - 1);
-            cx1[b] = clampi((int)flx + 1, 0, R3 - 1);
+            cxb0[b] = (uint32_t)clampi((int)flx, 0, R3 - 1) * 8u;
+            cxb1[b] = (uint32_t)clampi((int)flx + 1, 0, R3 - 1) * 8u;
             cfx[b] = pack_f16x2(sx - flx, sx - flx);
             cut[b] = sUt[i];
         }
         const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
+        const uint8_t* sUvtB = reinterpret_cast<const uint8_t*>(sUvt);
         // this warp's decoded F_uv chunk: [row][blk][32 columns] RGBA8
         uint32_t* sUvw = reinterpret_cast<uint32_t*>(smem + L.uvc) + warp * (chunk_rows * BPR * 32);
+        // MMA descriptors of this unit's weights
+        const uint32_t idesc1 = ptx::idesc_f16_f32(128, H);
+        const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
+        constexpr uint32_t sbo2 = (uint32_t)(Cfg::K2 / 8) * 128u;
+        const uint64_t bd1 = ptx::smem_desc_kmajor(ptx::smem_addr(sB1), 128u, 256u);
+        const uint64_t bd2 = ptx::smem_desc_kmajor(ptx::smem_addr(sB2), 128u, sbo2);
+        const uint64_t bd3 = ptx::smem_desc_kmajor(ptx::smem_addr(sB3), 128u, sbo2);
+        const int out_fmt = p.out_fmt;
+        const bool tiles_border = !p.full && B > 0;
 
         // a3: this warp's 32 BC7 blocks of the chunk starting at core row jc
         auto decode_chunk = [&](int jc) {
-            if (FMT_UV != FMT_BC7) return;
             constexpr int bpw = 8 * BPR;                    // blocks per block-row for this warp
             const int br = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
             const int gbc = 32 * blk + 8 * warp + bc;       // block column in the tile
@@ -394,97 +369,127 @@ __global__ void __launch_bounds__(kThreads, H == 16 ? 4 : 2) ndgi_fused_kernel(c
             __syncwarp();
         };
 
-        // a4/a6: Eq. 4 input row of block `item` -> A1 of slot s, then arrive
-        auto gather = [&](int item, int s) {
-            const int row = j_begin + item / BPR, blk = item % BPR;
+        // one layer for all S items of the step: A written by all 128 threads ->
+        // CTA barrier -> one elected lane of warp 0 issues S x (K/16) MMAs and
+        // commits them to d_ready -> everyone waits for the accumulators
+        auto run_layer = [&](auto layer) {
+            constexpr int l = decltype(layer)::value;
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncthreads();
+            if (warp == 0) {
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
+                        if (l == 0) {
+                            ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A1, bd1, idesc1, 0u);
+                        } else {
+#pragma unroll
+                            for (int st = 0; st < Cfg::K2 / 16; ++st)   // +256 B (= +16 in the desc) per K step
+                                ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A23 + 8u * st,
+                                                (l == 1 ? bd2 : bd3) + 16u * st, l == 1 ? idesc1 : idesc3, st > 0);
+                        }
+                    }
+                    ptx::mma_commit(bars);
+                }
+                __syncwarp();
+            }
+            ptx::mbar_wait_fast(bars, dph);
+            dph ^= 1u;
+            ptx::tc_fence_after();
+        };
+        using L0 = std::integral_constant<int, 0>;
+        using L1 = std::integral_constant<int, 1>;
+        using L2 = std::integral_constant<int, 2>;
+
+        // a4/a6: Eq. 4 input row of block (row, blk) -> A1 of slot s
+        auto gather = [&](int row, int blk, int s) {
             const int jr = row % chunk_rows;
-            if (jr == 0 && blk == 0) decode_chunk(row);
-            const float sy = fmaf((float)row + 0.5f, sc3, -0.5f);
-            const float fly = floorf(sy);
-            const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
-            const uint32_t fy2 = pack_f16x2(sy - fly, sy - fly);
-            const int i = blk * kTexelThreads + tid;
-            const int x0 = cx0[blk], x1 = cx1[blk];
+            if (FMT_UV == FMT_BC7 && jr == 0 && blk == 0) decode_chunk(row);
+            const uint4 rt = sRow[row];                  // y0 row byte offset, y1 row byte offset, fy, V_vt
+            const uint2 t00 = *reinterpret_cast<const uint2*>(sUvtB + rt.x + cxb0[blk]);
+            const uint2 t10 = *reinterpret_cast<const uint2*>(sUvtB + rt.x + cxb1[blk]);
+            const uint2 t01 = *reinterpret_cast<const uint2*>(sUvtB + rt.y + cxb0[blk]);
+            const uint2 t11 = *reinterpret_cast<const uint2*>(sUvtB + rt.y + cxb1[blk]);
             const uint32_t fx2 = cfx[blk];
-            const uint2 t00 = sUvt[y0 * R3 + x0], t10 = sUvt[y0 * R3 + x1];
-            const uint2 t01 = sUvt[y1 * R3 + x0], t11 = sUvt[y1 * R3 + x1];
             uint32_t a1[8];
-            a1[0] = hlerp2(hlerp2(t00.x, t10.x, fx2), hlerp2(t01.x, t11.x, fx2), fy2);
-            a1[1] = hlerp2(hlerp2(t00.y, t10.y, fx2), hlerp2(t01.y, t11.y, fx2), fy2);
+            a1[0] = hlerp2(hlerp2(t00.x, t10.x, fx2), hlerp2(t01.x, t11.x, fx2), rt.z);
+            a1[1] = hlerp2(hlerp2(t00.y, t10.y, fx2), hlerp2(t01.y, t11.y, fx2), rt.z);
             if (FMT_UV == FMT_BC7) {
                 u8x4_to_h2(sUvw[(jr * BPR + blk) * 32 + lane], a1[2], a1[3]);
             } else if (FMT_UV == FMT_U8) {
-                u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + i), a1[2], a1[3]);
+                u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + blk * kThreads + tid), a1[2], a1[3]);
             } else {
-                const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)row * C + i);
+                const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)row * C + blk * kThreads + tid);
                 a1[2] = hv.x;
                 a1[3] = hv.y;
             }
             a1[4] = cut[blk];
-            a1[5] = sVt[row];
+            a1[5] = rt.w;
             a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
             a1[7] = 0u;
-            ptx::tmem_st_x8(tmem + s * Cfg::SLOT_COLS + lane_base + Cfg::TM_A1, a1);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(a_ready(s));
+            ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1, a1);
         };
 
-        auto wait_d = [&](int s) {
-            ptx::mbar_wait(d_ready(s), (dph >> s) & 1u);
-            dph ^= 1u << s;
-            ptx::tc_fence_after();
-        };
-
-        auto epilogue = [&](int s) {
-            const uint32_t slot = tmem + s * Cfg::SLOT_COLS + lane_base;
-            gelu_epilogue<H>(slot + Cfg::TM_D, slot + Cfg::TM_A23);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(a_ready(s));
-        };
-
-        // a8: y of block `item` (slot s) -> page cache
-        auto output = [&](int item, int s) {
-            const int j = j_begin + item / BPR, i = (item % BPR) * kTexelThreads + tid;
+        // a8: y of block (row j, blk) in slot s -> page cache
+        auto output = [&](int j, int blk, int s) {
+            const int i = blk * kThreads + tid;
             uint32_t yv[4];
-            ptx::tmem_ld_x4(tmem + s * Cfg::SLOT_COLS + lane_base + Cfg::TM_D, yv);
+            ptx::tmem_ld_x4(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, yv);
             ptx::tmem_wait_ld();
             const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
             const size_t o = out_base + (size_t)j * row_pitch + i;
-            store_texel(p.out, o, p.out_fmt, y0f, y1f, y2f);
-            if (!p.full && B > 0) {
+            if (out_fmt == OUT_RGBA8) {
+                const uint32_t v = rgba8_fma(y0f, y1f, y2f);
+                uint32_t* out = reinterpret_cast<uint32_t*>(p.out);
+                out[o] = v;
+                if (tiles_border) {
+                    const bool bx = (i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2);
+                    const bool by = (j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2);
+                    if (bx || by) {
+                        // mirrored positions (R3): core i -> padded-core offsets -i and 2(C-1)-i
+                        const ptrdiff_t xm = i <= B ? -i : 2 * (C - 1) - i;
+                        const ptrdiff_t ym = j <= B ? -j : 2 * (C - 1) - j;
+                        const ptrdiff_t base = (ptrdiff_t)out_base, rp = (ptrdiff_t)row_pitch;
+                        if (bx) out[base + j * rp + xm] = v;
+                        if (by) out[base + ym * rp + i] = v;
+                        if (bx && by) out[base + ym * rp + xm] = v;
+                    }
+                }
+                return;
+            }
+            store_texel(p.out, o, out_fmt, y0f, y1f, y2f);
+            if (tiles_border) {
                 const bool bx = (i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2);
                 const bool by = (j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2);
                 if (bx || by) {
-                    // mirrored positions (R3): core i -> padded-core offsets -i and 2(C-1)-i
                     const int xm = i <= B ? -i : 2 * (C - 1) - i;
                     const int ym = j <= B ? -j : 2 * (C - 1) - j;
                     const ptrdiff_t base = (ptrdiff_t)out_base, rp = (ptrdiff_t)row_pitch;
-                    if (bx) store_texel(p.out, (size_t)(base + (ptrdiff_t)j * rp + xm), p.out_fmt, y0f, y1f, y2f);
-                    if (by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + i), p.out_fmt, y0f, y1f, y2f);
-                    if (bx && by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + xm), p.out_fmt, y0f, y1f, y2f);
+                    if (bx) store_texel(p.out, (size_t)(base + (ptrdiff_t)j * rp + xm), out_fmt, y0f, y1f, y2f);
+                    if (by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + i), out_fmt, y0f, y1f, y2f);
+                    if (bx && by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + xm), out_fmt, y0f, y1f, y2f);
                 }
             }
         };
 
-#pragma unroll 1
-        for (int s = 0; s < S; ++s) gather(s, s);
+        // S items per step; item n = (row j_begin + n / BPR, block n % BPR)
         for (int it = 0; it < nitems; it += S) {
-#pragma unroll 1
-            for (int l = 0; l < 2; ++l) {
-#pragma unroll 1
-                for (int s = 0; s < S; ++s) {   // layer l+1 done for slot s -> GELU -> A of layer l+2
-                    wait_d(s);
-                    epilogue(s);
-                }
-            }
-#pragma unroll 1
-            for (int s = 0; s < S; ++s) {       // layer 3 done -> y -> page cache; refill the slot
-                wait_d(s);
-                output(it + s, s);
-                if (it + S + s < nitems) gather(it + S + s, s);
-            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s) % BPR, s);
+            run_layer(L0{});
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);
+            run_layer(L1{});
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);
+            run_layer(L2{});
+#pragma unroll
+            for (int s = 0; s < S; ++s) output(j_begin + (it + s) / BPR, (it + s) % BPR, s);
         }
     }
 
@@ -512,7 +517,7 @@ static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-    const int regs_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (kThreads / 32);
+    const int regs_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (kThreads / 32);   // per-warp allocation unit 256
     const int smem_cta = (int)L.total + (int)fa.sharedSizeBytes + 1024;   // + per-CTA reserved smem
     int occ = regs_sm / regs_cta;
     if (smem_sm / smem_cta < occ) occ = smem_sm / smem_cta;
@@ -528,7 +533,7 @@ static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s)
     return cudaGetLastError();
 }
 
-int fused_ctas_per_sm(int H) { return 512 / (H == 16 ? (int)FusedCfg<16>::TM_COLS : (int)FusedCfg<64>::TM_COLS); }
+int fused_ctas_per_sm(int H) { return H == 16 ? FusedCfg<16>::MIN_CTAS : FusedCfg<64>::MIN_CTAS; }
 
 template <int H, int CT>
 static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t s) {

@@ -69,15 +69,19 @@ __device__ __forceinline__ int mirror_core(int i, int C) {
     return i;
 }
 
-// RN-even(clamp(y,0,1)*255), NaN -> 0 (R12)
-__device__ __forceinline__ uint32_t quant8(float y) {
-    return __float2uint_rn(fminf(fmaxf(y, 0.0f), 1.0f) * 255.0f);
+// RGBA8 texel on the FMA pipe (no F2I on the XU/MUFU pipe): clamp to [0,1],
+// then t*255 + 1.5*2^23 rounds the exact product to the nearest integer, ties
+// to even, into the low mantissa bits (R12); A = 255.
+__device__ __forceinline__ uint32_t rgba8_fma(float r, float g, float b) {
+    const uint32_t qr = __float_as_uint(fmaf(__saturatef(r), 255.0f, 12582912.0f));
+    const uint32_t qg = __float_as_uint(fmaf(__saturatef(g), 255.0f, 12582912.0f));
+    const uint32_t qb = __float_as_uint(fmaf(__saturatef(b), 255.0f, 12582912.0f));
+    return __byte_perm(__byte_perm(qr, qg, 0x0040u), __byte_perm(qb, 0xffu, 0x0040u), 0x5410u);
 }
 
 __device__ __forceinline__ void store_texel(void* out, size_t idx, int fmt, float r, float g, float b) {
     if (fmt == OUT_RGBA8) {
-        const uint32_t v = quant8(r) | (quant8(g) << 8) | (quant8(b) << 16) | 0xff000000u;
-        reinterpret_cast<uint32_t*>(out)[idx] = v;
+        reinterpret_cast<uint32_t*>(out)[idx] = rgba8_fma(r, g, b);
     } else if (fmt == OUT_RGBA16F) {
         __half2 rg = __floats2half2_rn(r, g), ba = __floats2half2_rn(b, 1.0f);
         uint2 v;

@@ -48,8 +48,34 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// hot-loop wait: plain spin on try_wait (which itself suspends in hardware);
+// traps after ~2^28 polls so a lost commit cannot hang the device
+__device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity))
+        if (++n == (1u << 28)) __trap();
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// shared-memory atomic add with acquire-release semantics at CTA scope
+__device__ __forceinline__ uint32_t atom_add_acqrel_cta(uint32_t addr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
+
+// one lane of the (converged) warp returns true
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
 }
 
 // named barrier over `n` threads (multiple of 32)

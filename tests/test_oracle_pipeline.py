@@ -135,5 +135,6 @@ def test_quantize_rgba8_rn_even():
     rng = np.random.default_rng(1)
     y32 = rng.uniform(-0.1, 1.1, (1000, 4)).astype(np.float32)
     q = oracle.quantize_rgba8(y32)
-    exp = np.rint(np.clip(y32[:, :3], 0, 1).astype(np.float32) * np.float32(255)).astype(np.uint8)
+    # RN-even of the exact product clamp(y)*255 (R12; the product is exact in fp64)
+    exp = np.rint(np.clip(y32[:, :3], 0, 1).astype(np.float64) * 255.0).astype(np.uint8)
     np.testing.assert_array_equal(q[:, :3], exp)
