@@ -16,7 +16,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libndgi.so")
+LIB_PATH = os.environ.get("NDGI_LIB") or os.path.join(_HERE, "libndgi.so")   # NDGI_LIB: experiment builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

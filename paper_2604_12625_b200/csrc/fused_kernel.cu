@@ -50,7 +50,10 @@ struct FusedCfg {
     static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
     static constexpr int SLOTS = H == 16 ? 2 : 1;        // 128-texel items per MMA step (one TMEM slot each)
     static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS < 32 ? 32 : SLOTS * SLOT_COLS;
-    static constexpr int MIN_CTAS = H == 16 ? 6 : 4;     // register budget: 85 / 128 per thread
+#ifndef NDGI_MIN_CTAS16
+#define NDGI_MIN_CTAS16 8
+#endif
+    static constexpr int MIN_CTAS = H == 16 ? NDGI_MIN_CTAS16 : 4;   // register budget: 64 / 128 per thread
     static constexpr int B1_BYTES = H * 16 * 2;
     static constexpr int B2_BYTES = H * K2 * 2;
     static constexpr int B3_BYTES = 16 * K2 * 2;
