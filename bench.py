@@ -179,8 +179,9 @@ def run_gpu(args, rank, world, dist):
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
     lay0, seed = S.config("c2")
+    from paper_2604_12625_b200 import parallel as par
     tiles_per_rank = lay0["num_tiles"]
-    global_ids = [rank + world * i for i in range(tiles_per_rank)]
+    global_ids = par.shard_tiles(tiles_per_rank * world, world, rank)   # tile k on rank k % N
     th_np = S.make_theta(lay0, seed, tiles=global_ids)
     lay = dict(lay0)
     theta = ndgi.upload_theta(th_np, dev)
@@ -214,9 +215,7 @@ def run_gpu(args, rank, world, dist):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = sum(step_ms)
     if dist:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+        tot_ms = par.max_over_ranks(tot_ms, dist, "cuda")
     ms_per_step = tot_ms / args.steps
     texels_per_step = per_t * N_T * world
     value = texels_per_step / (ms_per_step * 1e-3) / 1e9
@@ -244,9 +243,7 @@ def run_gpu(args, rank, world, dist):
             e2e_step()
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         if dist:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+            e2e_s = par.max_over_ranks(e2e_s, dist, "cuda")
         e2e = {"value": texels_per_step / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                "path": "ndgi_decode_full_host (pinned host RGBA8 out) + Theta H2D copy per step"}
