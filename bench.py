@@ -52,6 +52,14 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
 
 
+def _traffic():
+    """DRAM bytes per launch of the fused kernel from the committed ncu capture."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def _workload_config(world: int, tiles_per_rank: int) -> dict:
     return {
         "workload": "c2: 4096^2 lightmap atlas (32x32 NDGI-M tiles of 128^2, BC7 F_uv/F_uvt, u8 lines, "
@@ -265,7 +273,7 @@ def run_gpu(args, rank, world, dist):
     flops = evaluated * 2 * (16 * h + (h + 16) * h + (h + 16) * 16)               # tensor work as issued
     roofline = {
         "bound": "alu", "achieved": achieved_act / 1e9, "peak": r_gelu / 1e9, "unit": "Gact/s",
-        "frac": achieved_act / r_gelu, "traffic": None,
+        "frac": achieved_act / r_gelu, "traffic": _traffic(),
         "kernel": "ndgi_fused_kernel<16,BC7>", "per_unit": f"2h = {2 * h} GELU activations per evaluated texel",
         "peak_source": "ndgi_debug_gelu_rate: the kernel's f16x2 tanh-GELU, 148 SMs x 8 CTAs, measured in this run",
         "hbm_frac": alg_bytes / kern_s / 1e9 / peaks["hbm_gbs"],
