@@ -50,6 +50,9 @@ struct FusedCfg {
     static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
     static constexpr int SLOTS = H == 16 ? 2 : 1;        // 128-texel items per MMA step (one TMEM slot each)
     static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS < 32 ? 32 : SLOTS * SLOT_COLS;
+#ifndef NDGI_JOINT_EPI
+#define NDGI_JOINT_EPI 1
+#endif
 #ifndef NDGI_MIN_CTAS16
 #define NDGI_MIN_CTAS16 8
 #endif
@@ -126,6 +129,22 @@ __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) 
             g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
         ptx::tmem_st_x8(a_addr + c0 / 2, g);
     }
+}
+
+// h = 16, two items: both accumulators loaded before one wait, 16 independent
+// GELU pairs in flight (more ILP for the MUFU pipe)
+__device__ __forceinline__ void gelu_epilogue2_h16(uint32_t d0, uint32_t a0, uint32_t d1, uint32_t a1) {
+    uint32_t x[16], y[16], g[8], h[8];
+    ptx::tmem_ld_x16(d0, x);
+    ptx::tmem_ld_x16(d1, y);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(x[2 * q]), __uint_as_float(x[2 * q + 1])));
+        h[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(y[2 * q]), __uint_as_float(y[2 * q + 1])));
+    }
+    ptx::tmem_st_x8(a0, g);
+    ptx::tmem_st_x8(a1, h);
 }
 
 template <int H, int FMT_UV, int CT>
@@ -478,18 +497,27 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             }
         };
 
+        auto epilogues = [&]() {
+#if NDGI_JOINT_EPI
+            if constexpr (H == 16 && S == 2) {
+                gelu_epilogue2_h16(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, tm_lane + Cfg::SLOT_COLS + Cfg::TM_D,
+                                   tm_lane + Cfg::SLOT_COLS + Cfg::TM_A23);
+                return;
+            }
+#endif
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);
+        };
+
         // S items per step; item n = (row j_begin + n / BPR, block n % BPR)
         for (int it = 0; it < nitems; it += S) {
 #pragma unroll
             for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s) % BPR, s);
             run_layer(L0{});
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-                gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);
+            epilogues();
             run_layer(L1{});
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-                gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);
+            epilogues();
             run_layer(L2{});
 #pragma unroll
             for (int s = 0; s < S; ++s) output(j_begin + (it + s) / BPR, (it + s) % BPR, s);
