@@ -29,123 +29,15 @@
 #include <cstdlib>
 #include <type_traits>
 
-#include "bc7_device.cuh"
-#include "ndgi_common.cuh"
-#include "tc_ptx.cuh"
+#include "fused_common.cuh"
 
 namespace ndgi {
 
 constexpr int kThreads = 128;
-constexpr int kChunkTexels = 2048;             // F_uv texels decoded per chunk (4 warps x 32 blocks x 16)
 
-template <int H>
-struct FusedCfg {
-    static constexpr int K2 = H + 16;                    // layer 2/3 K incl. bias chunk
-    // per slot: A23 = layer-2/3 A operand (K2/2 columns); layer 1's A (K = 16,
-    // 8 columns) aliases its first 8 columns -- dead once layer 1 completes,
-    // and the bias chunk (columns H/2 .. H/2+7) is never overwritten.
-    static constexpr uint32_t TM_A1 = 0;
-    static constexpr uint32_t TM_A23 = 0;
-    static constexpr uint32_t TM_D = H == 16 ? 16 : 64;  // H columns (fp32 accumulators)
-    static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
-    static constexpr int SLOTS = H == 16 ? 2 : 1;        // 128-texel items per MMA step (one TMEM slot each)
-    static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS < 32 ? 32 : SLOTS * SLOT_COLS;
 #ifndef NDGI_JOINT_EPI
 #define NDGI_JOINT_EPI 1
 #endif
-#ifndef NDGI_MIN_CTAS16
-#define NDGI_MIN_CTAS16 8
-#endif
-    static constexpr int MIN_CTAS = H == 16 ? NDGI_MIN_CTAS16 : 4;   // register budget: 64 / 128 per thread
-    static constexpr int B1_BYTES = H * 16 * 2;
-    static constexpr int B2_BYTES = H * K2 * 2;
-    static constexpr int B3_BYTES = 16 * K2 * 2;
-    static_assert(TM_A23 + K2 / 2 <= TM_D, "TMEM layout");
-    static_assert(TM_D + H <= SLOT_COLS, "TMEM layout");
-};
-
-// element (n, k) of a K-major no-swizzle operand with Kt columns:
-// [n/8][k/8][n%8][k%8] halves -> LBO = 128 B, SBO = Kt/8 * 128 B
-__device__ __forceinline__ int bofs(int n, int k, int Kt) {
-    return (((n >> 3) * (Kt >> 3) + (k >> 3)) << 6) + ((n & 7) << 3) + (k & 7);
-}
-
-__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
-    uint32_t r;
-    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-    return r;
-}
-__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t r;
-    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-}
-// a + f (b - a), packed
-__device__ __forceinline__ uint32_t hlerp2(uint32_t a, uint32_t b, uint32_t f2) { return hfma2(f2, hsub2(b, a), a); }
-
-// 4 u8 channels -> two f16x2 holding the integers 0..255 exactly
-__device__ __forceinline__ void u8x4_to_h2(uint32_t q, uint32_t& rg, uint32_t& ba) {
-    const uint32_t k1024 = 0x64006400u;  // f16x2(1024, 1024); 0x64XX = 1024 + XX
-    rg = hsub2(__byte_perm(q, 0x64646464u, 0x5140u), k1024);
-    ba = hsub2(__byte_perm(q, 0x64646464u, 0x7362u), k1024);
-}
-
-struct FusedSmem {
-    // byte offsets from the dynamic smem base
-    uint32_t b1, b2, b3, uvt, uvc, utcol, rowtab, cnt, bars, tmem_slot, total;
-};
-
-template <int H>
-__host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
-    using Cfg = FusedCfg<H>;
-    FusedSmem s{};
-    uint32_t o = 0;
-    s.b1 = o; o += Cfg::B1_BYTES;
-    s.b2 = o; o += Cfg::B2_BYTES;
-    s.b3 = o; o += Cfg::B3_BYTES;
-    o = (o + 127) & ~127u;
-    s.uvt = o; o += (uint32_t)(R3 * R3 * 8);         // blended slice, f16x4 per texel
-    s.uvc = o; o += kChunkTexels * 4;                 // decoded F_uv chunk, RGBA8 (4 per-warp parts)
-    s.utcol = o; o += (uint32_t)(C * 4);              // V_ut per column, f16x2
-    o = (o + 15) & ~15u;
-    s.rowtab = o; o += (uint32_t)(C * 16);            // per core row: y0*R3, y1*R3, fy (f16x2), V_vt (f16x2)
-    s.cnt = o; o += 8 * 4;                            // (unused)
-    s.bars = o; o += 8 * 8;                           // d_ready
-    s.tmem_slot = o; o += 8;
-    s.total = o;
-    return s;
-}
-
-// ---- GELU epilogue of one layer: D (fp32) -> f16x2 GELU~ -> A23 ---------------
-template <int H>
-__device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) {
-#pragma unroll
-    for (int c0 = 0; c0 < H; c0 += 16) {
-        uint32_t d[16], g[8];
-        ptx::tmem_ld_x16(d_addr + c0, d);
-        ptx::tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
-        ptx::tmem_st_x8(a_addr + c0 / 2, g);
-    }
-}
-
-// h = 16, two items: both accumulators loaded before one wait, 16 independent
-// GELU pairs in flight (more ILP for the MUFU pipe)
-__device__ __forceinline__ void gelu_epilogue2_h16(uint32_t d0, uint32_t a0, uint32_t d1, uint32_t a1) {
-    uint32_t x[16], y[16], g[8], h[8];
-    ptx::tmem_ld_x16(d0, x);
-    ptx::tmem_ld_x16(d1, y);
-    ptx::tmem_wait_ld();
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(x[2 * q]), __uint_as_float(x[2 * q + 1])));
-        h[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(y[2 * q]), __uint_as_float(y[2 * q + 1])));
-    }
-    ptx::tmem_st_x8(a0, g);
-    ptx::tmem_st_x8(a1, h);
-}
 
 template <int H, int FMT_UV, int CT>
 __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_kernel(const __grid_constant__ KParams p) {
@@ -223,127 +115,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 
         // ---- a2: tile parameters -> shared memory -----------------------------------
         __syncthreads();  // previous unit's MMAs complete and all smem readers done
-        {
-            const uint16_t* w = p.mlp + p.mlp_tile_elems * k;
-            const uint16_t *W1 = w, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
-            const float a = kGeluA;
-            const float s_uv = FMT_UV == FMT_F16 ? a : a / 255.0f;   // F_uv enters in q units (R8)
-            // layer 1: [H][16]: k 0..11 = Eq. 4 features, 12 = bias (gamma(t) folded), 13..15 = 0
-            for (int e = tid; e < H * 16; e += kThreads) {
-                const int n = e >> 4, kk = e & 15;
-                float v = 0.f;
-                if (kk < 12) {
-                    const float wv = half_bits_to_float(__ldg(W1 + n * 16 + kk));
-                    v = wv * ((kk >= 4 && kk < 8) ? s_uv : a);
-                } else if (kk == 12) {
-                    float acc = half_bits_to_float(__ldg(b1 + n));
-                    for (int g = 0; g < 4; ++g) acc = fmaf(half_bits_to_float(__ldg(W1 + n * 16 + 12 + g)), tc.gamma[g], acc);
-                    v = a * acc;
-                }
-                sB1[bofs(n, kk, 16)] = __float2half_rn(v);
-            }
-            // layer 2: [H][H+16]: 0.5*W2 (absorbs 1/(2a) of GELU~ and a of the next pre-scale), bias a*b2
-            for (int e = tid; e < H * Cfg::K2; e += kThreads) {
-                const int n = e / Cfg::K2, kk = e % Cfg::K2;
-                float v = 0.f;
-                if (kk < H) v = 0.5f * half_bits_to_float(__ldg(W2 + n * H + kk));
-                else if (kk == H) v = a * half_bits_to_float(__ldg(b2 + n));
-                sB2[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
-            }
-            // layer 3: [16][H+16]: rows 0..2 = W3/(2a), bias b3 (exact); rows 3..15 = 0
-            for (int e = tid; e < 16 * Cfg::K2; e += kThreads) {
-                const int n = e / Cfg::K2, kk = e % Cfg::K2;
-                float v = 0.f;
-                if (n < 3) {
-                    if (kk < H) v = half_bits_to_float(__ldg(W3 + n * H + kk)) * (0.5f / a);
-                    else if (kk == H) v = half_bits_to_float(__ldg(b3 + n));
-                }
-                sB3[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
-            }
-            // F_uvt slices k0, k1 blended with tau (R4, R17) -> f16x4 [R3][R3], values in [0,1]
-            const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
-            const float tau = tc.tau, omt = 1.0f - tau;
-            if (p.fmt_uvt == FMT_BC7) {
-                const int nbx = R3 >> 2, nb = nbx * nbx;
-                const uint4* s0 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k0);
-                const uint4* s1 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k1);
-                for (int bi = tid; bi < nb; bi += kThreads) {
-                    uint32_t t0[16], t1[16];
-                    bc7_decode(__ldg(s0 + bi), [&](int i, uint32_t v) { t0[i] = v; });
-                    bc7_decode(__ldg(s1 + bi), [&](int i, uint32_t v) { t1[i] = v; });
-                    const int bx = bi % nbx, by = bi / nbx;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float c[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            c[q] = (omt * (float)((t0[i] >> (8 * q)) & 0xffu) + tau * (float)((t1[i] >> (8 * q)) & 0xffu)) *
-                                   (1.0f / 255.0f);
-                        sUvt[(by * 4 + (i >> 2)) * R3 + bx * 4 + (i & 3)] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
-                    }
-                }
-            } else {
-                const int ntex = R3 * R3;
-                for (int e = tid; e < ntex; e += kThreads) {
-                    float c[4];
-                    if (p.fmt_uvt == FMT_U8) {
-                        const uint32_t q0 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k0) + e);
-                        const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + e);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            c[q] = (omt * (float)((q0 >> (8 * q)) & 0xffu) + tau * (float)((q1 >> (8 * q)) & 0xffu)) * (1.0f / 255.0f);
-                    } else {
-                        const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * e;
-                        const uint16_t* h1 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k1) + 4 * e;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            c[q] = omt * half_bits_to_float(__ldg(h0 + q)) + tau * half_bits_to_float(__ldg(h1 + q));
-                    }
-                    sUvt[e] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
-                }
-            }
-            // line maps (R5): V_ut(u_i) per core column i, V_vt(v_j) per core row j
-            const uint8_t* ut = p.ut + p.line_tile_bytes * k;
-            const uint8_t* vt = p.vt + p.line_tile_bytes * k;
-            const float rho = tc.rho, omr = 1.0f - rho;
-            const float scu = (float)p.U * (1.0f / (float)C);
-            for (int e = tid; e < 2 * C; e += kThreads) {
-                const int i = e % C;
-                const uint8_t* m = e < C ? ut : vt;
-                const float sx = fmaf((float)i + 0.5f, scu, -0.5f);
-                const float fl = floorf(sx), fx = sx - fl;
-                const int x0 = clampi((int)fl, 0, p.U - 1), x1 = clampi((int)fl + 1, 0, p.U - 1);
-                float c[2];
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    float v00, v10, v01, v11;
-                    if (p.fmt_line == FMT_U8) {
-                        v00 = (float)__ldg(m + (tc.r0 * p.U + x0) * 2 + q);
-                        v10 = (float)__ldg(m + (tc.r0 * p.U + x1) * 2 + q);
-                        v01 = (float)__ldg(m + (tc.r1 * p.U + x0) * 2 + q);
-                        v11 = (float)__ldg(m + (tc.r1 * p.U + x1) * 2 + q);
-                    } else {
-                        const uint16_t* mh = reinterpret_cast<const uint16_t*>(m);
-                        v00 = half_bits_to_float(__ldg(mh + (tc.r0 * p.U + x0) * 2 + q));
-                        v10 = half_bits_to_float(__ldg(mh + (tc.r0 * p.U + x1) * 2 + q));
-                        v01 = half_bits_to_float(__ldg(mh + (tc.r1 * p.U + x0) * 2 + q));
-                        v11 = half_bits_to_float(__ldg(mh + (tc.r1 * p.U + x1) * 2 + q));
-                    }
-                    float v = (1.f - fx) * omr * v00 + fx * omr * v10 + (1.f - fx) * rho * v01 + fx * rho * v11;
-                    c[q] = p.fmt_line == FMT_U8 ? v * (1.0f / 255.0f) : v;
-                }
-                if (e < C) {
-                    sUt[i] = pack_f16x2(c[0], c[1]);
-                } else {
-                    // per-row gather table: F_uvt y taps and weight, V_vt
-                    const float sy = fmaf((float)i + 0.5f, sc3, -0.5f);
-                    const float fly = floorf(sy);
-                    const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
-                    sRow[i] = make_uint4((uint32_t)(y0 * R3) * 8u, (uint32_t)(y1 * R3) * 8u, pack_f16x2(sy - fly, sy - fly),
-                                         pack_f16x2(c[0], c[1]));
-                }
-            }
-        }
+        unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads);
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
         __syncthreads();
 
@@ -499,9 +271,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 
         auto epilogues = [&]() {
 #if NDGI_JOINT_EPI
-            if constexpr (H == 16 && S == 2) {
-                gelu_epilogue2_h16(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, tm_lane + Cfg::SLOT_COLS + Cfg::TM_D,
-                                   tm_lane + Cfg::SLOT_COLS + Cfg::TM_A23);
+            if constexpr (H == 16) {
+                gelu_epilogue_h16<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
                 return;
             }
 #endif

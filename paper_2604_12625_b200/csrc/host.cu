@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -15,6 +16,7 @@
 namespace ndgi {
 cudaError_t launch_ref(const KParams& p, cudaStream_t stream);
 cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_fused_ws(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
 cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, cudaStream_t s);
 cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
@@ -176,7 +178,12 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
     if (mode == NDGI_MODE_FAST) {
         if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
         choose_strips(p, ctx->num_sms);
-        e = ndgi::launch_fused(p, ctx->num_sms, s);
+        static const int variant = [] {
+            const char* v = getenv("NDGI_KERNEL");   // "ws" = warp-specialised h=16 kernel
+            return v && strcmp(v, "ws") == 0 ? 1 : 0;
+        }();
+        if (variant == 1 && p.H == 16) e = ndgi::launch_fused_ws(p, ctx->num_sms, s);
+        else e = ndgi::launch_fused(p, ctx->num_sms, s);
     } else {
         e = ndgi::launch_ref(p, s);
     }
