@@ -225,6 +225,10 @@ NDGI_API ndgi_status ndgi_debug_bc7_decode_hw(const void* blocks, uint32_t w, ui
  * Synchronous. */
 NDGI_API ndgi_status ndgi_debug_gelu_rate(uint32_t iters, float* ms, double* activations);
 
+/* tcgen05 round-trip microbenchmark (st A, barrier, MMA M128N16K16, commit,
+ * mbarrier wait, ld D) on one CTA: SM cycles per iteration.  Synchronous. */
+NDGI_API ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_iter);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,7 @@ _SIGS = {
     "ndgi_debug_bc7_decode": (_I, [_P, _U32, _U32, _P, _P]),
     "ndgi_debug_bc7_decode_hw": (_I, [_P, _U32, _U32, _P]),
     "ndgi_debug_gelu_rate": (_I, [_U32, C.POINTER(_F), C.POINTER(C.c_double)]),
+    "ndgi_debug_mma_latency": (_I, [_U32, C.POINTER(C.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -207,6 +208,13 @@ def ndgi_debug_gelu_rate(iters: int = 4096) -> tuple[float, float]:
     ms, acts = C.c_float(0), C.c_double(0)
     _check(_lib.ndgi_debug_gelu_rate(iters, C.byref(ms), C.byref(acts)), "ndgi_debug_gelu_rate")
     return float(ms.value), float(acts.value)
+
+
+def ndgi_debug_mma_latency(iters: int = 1000) -> float:
+    """SM cycles per tcgen05 round trip (st A, barrier, MMA, commit, wait, ld D)."""
+    c = C.c_double(0)
+    _check(_lib.ndgi_debug_mma_latency(iters, C.byref(c)), "ndgi_debug_mma_latency")
+    return float(c.value)
 
 
 def raw_call(name: str, *args) -> int:

@@ -109,3 +109,69 @@ cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts) {
 }
 
 }  // namespace ndgi
+
+// ---------------------------------------------------------------------------
+// tcgen05 round-trip microbenchmark: one CTA of 128 threads repeats
+//   tcgen05.st A -> wait::st -> fence -> bar.sync -> (thread 0) mma M128 N16 K16
+//   -> commit -> all threads mbarrier wait -> tcgen05.ld D -> wait::ld
+// and reports cycles per iteration (the latency each layer of the fused kernel
+// pays when nothing else hides it).
+// ---------------------------------------------------------------------------
+#include "tc_ptx.cuh"
+namespace ndgi {
+__global__ void __launch_bounds__(128, 1) mma_latency_kernel(uint32_t iters, long long* out) {
+    __shared__ __align__(1024) uint8_t sB[16 * 16 * 2];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 16 * 16 * 2; i += 128) sB[i] = 0;
+    const uint32_t b = ptx::smem_addr(&bar);
+    if (tid == 0) { ptx::mbar_init(b, 1); ptx::fence_mbar_init(); }
+    if (warp == 0) ptx::tmem_alloc<32>(ptx::smem_addr(&tslot));
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tslot, lane_base = (uint32_t)(warp * 32) << 16;
+    const uint64_t bd = ptx::smem_desc_kmajor(ptx::smem_addr(sB), 128u, 256u);
+    const uint32_t idesc = ptx::idesc_f16_f32(128, 16);
+    uint32_t a[8] = {0, 0, 0, 0, 0, 0, 0, 0}, d[16], phase = 0, acc = 0;
+    long long t0 = 0;
+    for (uint32_t it = 0; it < iters + 8; ++it) {
+        if (it == 8) t0 = clock64();
+        a[0] = acc;
+        ptx::tmem_st_x8(tmem + lane_base, a);
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            ptx::tc_fence_after();
+            ptx::mma_f16_ts(tmem + 16, tmem, bd, idesc, 0u);
+            ptx::mma_commit(b);
+        }
+        ptx::mbar_wait_fast(b, phase);
+        phase ^= 1u;
+        ptx::tc_fence_after();
+        ptx::tmem_ld_x16(tmem + lane_base + 16, d);
+        ptx::tmem_wait_ld();
+        acc += d[0];
+    }
+    if (tid == 0) { out[0] = clock64() - t0; out[1] = acc; }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<32>(tmem);
+}
+
+cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter) {
+    long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 16);
+    if (e != cudaSuccess) return e;
+    mma_latency_kernel<<<1, 128>>>(iters, d);
+    e = cudaDeviceSynchronize();
+    long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    *cycles_per_iter = (double)h[0] / iters;
+    return e;
+}
+}  // namespace ndgi

@@ -20,6 +20,9 @@ constexpr int kChunkTexels = 2048;             // F_uv texels decoded per chunk 
 #ifndef NDGI_SLOTS16
 #define NDGI_SLOTS16 2
 #endif
+#ifndef NDGI_GROUPS16
+#define NDGI_GROUPS16 1
+#endif
 
 template <int H>
 struct FusedCfg {
@@ -32,7 +35,8 @@ struct FusedCfg {
     static constexpr uint32_t TM_D = H == 16 ? 16 : 64;  // H columns (fp32 accumulators)
     static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
     static constexpr int SLOTS = H == 16 ? NDGI_SLOTS16 : 1;   // 128-texel items per MMA step (one TMEM slot each)
-    static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS < 32 ? 32 : SLOTS * SLOT_COLS;
+    static constexpr int GROUPS = H == 16 ? NDGI_GROUPS16 : 1;   // independent step groups (ping-pong)
+    static constexpr uint32_t TM_COLS = GROUPS * SLOTS * SLOT_COLS < 32 ? 32 : GROUPS * SLOTS * SLOT_COLS;
     static constexpr int MIN_CTAS = H == 16 ? NDGI_MIN_CTAS16 : 4;   // register budget: 64 / 128 per thread
     static constexpr int B1_BYTES = H * 16 * 2;
     static constexpr int B2_BYTES = H * K2 * 2;
@@ -146,7 +150,7 @@ __device__ __forceinline__ void gelu_epilogue2_h16(uint32_t d0, uint32_t a0, uin
 // B operands (with the folds of DESIGN.md §6.1), the tau-blended F_uvt slice,
 // V_ut per column and the per-row gather table (F_uvt y taps, V_vt).
 // Executed by threads tid = 0 .. nthr-1 of the CTA.
-template <int H, int FMT_UV, int C>
+template <int H, int FMT_UV, int C, bool TC_WEIGHTS = true>
 __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc, int k, uint8_t* smem,
                                               const FusedSmem& L, int tid, int nthr) {
     using Cfg = FusedCfg<H>;
@@ -163,6 +167,7 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
             const uint16_t *W1 = w, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
             const float a = kGeluA;
             const float s_uv = FMT_UV == FMT_F16 ? a : a / 255.0f;   // F_uv enters in q units (R8)
+            if constexpr (TC_WEIGHTS) {
             // layer 1: [H][16]: k 0..11 = Eq. 4 features, 12 = bias (gamma(t) folded), 13..15 = 0
             for (int e = tid; e < H * 16; e += nthr) {
                 const int n = e >> 4, kk = e & 15;
@@ -194,6 +199,7 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                     else if (kk == H) v = half_bits_to_float(__ldg(b3 + n));
                 }
                 sB3[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
+            }
             }
             // F_uvt slices k0, k1 blended with tau (R4, R17) -> f16x4 [R3][R3], values in [0,1]
             const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;

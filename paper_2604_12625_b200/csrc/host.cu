@@ -17,10 +17,12 @@ namespace ndgi {
 cudaError_t launch_ref(const KParams& p, cudaStream_t stream);
 cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_ws(const KParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_fused_hmma(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
 cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, cudaStream_t s);
 cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
 cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts);
+cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter);
 }  // namespace ndgi
 
 struct ndgi_ctx {
@@ -179,10 +181,13 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
         if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
         choose_strips(p, ctx->num_sms);
         static const int variant = [] {
-            const char* v = getenv("NDGI_KERNEL");   // "ws" = warp-specialised h=16 kernel
-            return v && strcmp(v, "ws") == 0 ? 1 : 0;
+            const char* v = getenv("NDGI_KERNEL");   // "ws" / "hmma": h = 16 kernel variants
+            if (v && strcmp(v, "ws") == 0) return 1;
+            if (v && strcmp(v, "hmma") == 0) return 2;
+            return 0;
         }();
         if (variant == 1 && p.H == 16) e = ndgi::launch_fused_ws(p, ctx->num_sms, s);
+        else if (variant == 2 && p.H == 16) e = ndgi::launch_fused_hmma(p, ctx->num_sms, s);
         else e = ndgi::launch_fused(p, ctx->num_sms, s);
     } else {
         e = ndgi::launch_ref(p, s);
@@ -417,6 +422,12 @@ ndgi_status ndgi_debug_gelu_rate(uint32_t iters, float* ms, double* activations)
     if (!ms || !activations || !iters) return fail(NDGI_ERR_ARG, "bad arguments");
     cudaError_t e = ndgi::gelu_rate(iters, ms, activations);
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "gelu rate");
+}
+
+ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_iter) {
+    if (!cycles_per_iter || !iters) return fail(NDGI_ERR_ARG, "bad arguments");
+    cudaError_t e = ndgi::mma_latency(iters, cycles_per_iter);
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "mma latency");
 }
 
 }  // extern "C"

@@ -48,11 +48,29 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
-// hot-loop wait: plain spin on try_wait (which itself suspends in hardware);
-// traps after ~2^28 polls so a lost commit cannot hang the device
+#ifndef NDGI_WAIT_HINT_NS
+#define NDGI_WAIT_HINT_NS 0
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity) {
+#if NDGI_WAIT_HINT_NS > 0
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "n"(NDGI_WAIT_HINT_NS)
+        : "memory");
+    return ok != 0;
+#else
+    return mbar_try_wait(bar, parity);
+#endif
+}
+// hot-loop wait: try_wait suspends the warp in hardware (optionally with a
+// suspend-time hint); traps after ~2^28 polls so a lost commit cannot hang
 __device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
-    while (!mbar_try_wait(bar, parity))
+    while (!mbar_try_wait_hint(bar, parity))
         if (++n == (1u << 28)) __trap();
 }
 
