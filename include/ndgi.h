@@ -229,6 +229,11 @@ NDGI_API ndgi_status ndgi_debug_gelu_rate(uint32_t iters, float* ms, double* act
  * mbarrier wait, ld D) on one CTA: SM cycles per iteration.  Synchronous. */
 NDGI_API ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_iter);
 
+/* TMEM layout probe of an f16-accumulator MMA (M128 N16 K16, B = identity):
+ * host_out[128][24] receives columns 0..15 of every lane, then the same columns
+ * read with .pack::16b (8 words).  Synchronous. */
+NDGI_API ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out);
+
 #ifdef __cplusplus
 }
 #endif

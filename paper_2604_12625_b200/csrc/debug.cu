@@ -175,3 +175,69 @@ cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter) {
     return e;
 }
 }  // namespace ndgi
+
+// ---------------------------------------------------------------------------
+// Layout probe: one M128 N16 K16 MMA with an f16 accumulator (c_format F16);
+// A[m][k] = m + k/16 (as f16), B = identity (N = K = 16) -> D[m][n] = A[m][n].
+// out[128][24]: columns 0..15 of every lane as raw 32-bit words, then the same
+// 16 columns read with tcgen05.ld ... .pack::16b (8 words).
+// ---------------------------------------------------------------------------
+namespace ndgi {
+__global__ void __launch_bounds__(128, 1) tmem_f16_probe_kernel(uint32_t* out) {
+    __shared__ __align__(1024) __half sB[16 * 16];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    // B in the K-major no-swizzle layout [n/8][k/8][n%8][k%8], identity
+    for (int e = tid; e < 256; e += 128) {
+        const int n = e >> 4, k = e & 15;
+        const int off = (((n >> 3) * 2 + (k >> 3)) << 6) + ((n & 7) << 3) + (k & 7);
+        sB[off] = __float2half(n == k ? 1.0f : 0.0f);
+    }
+    const uint32_t b = ptx::smem_addr(&bar);
+    if (tid == 0) { ptx::mbar_init(b, 1); ptx::fence_mbar_init(); }
+    if (warp == 0) ptx::tmem_alloc<64>(ptx::smem_addr(&tslot));
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tslot, lane_base = (uint32_t)(warp * 32) << 16;
+    uint32_t a[8];
+    for (int c = 0; c < 8; ++c) a[c] = pack_f16x2((float)tid + (2 * c) / 16.0f, (float)tid + (2 * c + 1) / 16.0f);
+    ptx::tmem_st_x8(tmem + lane_base, a);
+    uint32_t z[16] = {0};
+    ptx::tmem_st_x8(tmem + lane_base + 16, *reinterpret_cast<uint32_t(*)[8]>(z));
+    ptx::tmem_st_x8(tmem + lane_base + 24, *reinterpret_cast<uint32_t(*)[8]>(z + 8));
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+        ptx::tc_fence_after();
+        const uint32_t idesc = (0u << 4) | ((16u >> 3) << 17) | ((128u >> 4) << 24);   // D format F16
+        ptx::mma_f16_ts(tmem + 16, tmem, ptx::smem_desc_kmajor(ptx::smem_addr(sB), 128u, 256u), idesc, 0u);
+        ptx::mma_commit(b);
+    }
+    ptx::mbar_wait_fast(b, 0);
+    ptx::tc_fence_after();
+    uint32_t d[16], pk[8];
+    ptx::tmem_ld_x16(tmem + lane_base + 16, d);
+    ptx::tmem_ld_x8_pack16(tmem + lane_base + 16, pk);
+    ptx::tmem_wait_ld();
+    for (int c = 0; c < 16; ++c) out[tid * 24 + c] = d[c];
+    for (int c = 0; c < 8; ++c) out[tid * 24 + 16 + c] = pk[c];
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<64>(tmem);
+}
+
+cudaError_t tmem_f16_probe(uint32_t* host_out) {
+    uint32_t* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 128 * 24 * 4);
+    if (e != cudaSuccess) return e;
+    tmem_f16_probe_kernel<<<1, 128>>>(d);
+    e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(host_out, d, 128 * 24 * 4, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
+}  // namespace ndgi

@@ -114,6 +114,27 @@ __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) 
 
 // h = 16, S items: all accumulators loaded before one wait, 8*S independent
 // GELU pairs in flight
+#ifndef NDGI_F16ACC
+#define NDGI_F16ACC 1
+#endif
+
+// h = 16, S items with f16 accumulators (layers 1, 2): tcgen05.ld .pack::16b
+// delivers the 16 pre-activations as 8 f16x2 words -- no fp32 -> f16 packing
+template <int S>
+__device__ __forceinline__ void gelu_epilogue_h16_f16acc(uint32_t d0, uint32_t a0, uint32_t stride) {
+    uint32_t x[S][8];
+#pragma unroll
+    for (int s = 0; s < S; ++s) ptx::tmem_ld_x8_pack16(d0 + s * stride, x[s]);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        uint32_t g[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) g[q] = gelu_scaled_f16x2(x[s][q]);
+        ptx::tmem_st_x8(a0 + s * stride, g);
+    }
+}
+
 template <int S>
 __device__ __forceinline__ void gelu_epilogue_h16(uint32_t d0, uint32_t a0, uint32_t stride) {
     uint32_t x[S][16];

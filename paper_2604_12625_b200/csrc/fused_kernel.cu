@@ -137,7 +137,9 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         // this warp's decoded F_uv chunk: [row][blk][32 columns] RGBA8
         uint32_t* sUvw = reinterpret_cast<uint32_t*>(smem + L.uvc) + warp * (chunk_rows * BPR * 32);
         // MMA descriptors of this unit's weights
-        const uint32_t idesc1 = ptx::idesc_f16_f32(128, H);
+        // layers 1, 2: f16 accumulators for h = 16 (the GELU input is f16 anyway);
+        // layer 3 (the output y): fp32
+        const uint32_t idesc1 = (H == 16 && NDGI_F16ACC) ? ptx::idesc_f16_f16(128, H) : ptx::idesc_f16_f32(128, H);
         const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
         constexpr uint32_t sbo2 = (uint32_t)(Cfg::K2 / 8) * 128u;
         const uint64_t bd1 = ptx::smem_desc_kmajor(ptx::smem_addr(sB1), 128u, 256u);
@@ -272,7 +274,11 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         auto epilogues = [&]() {
 #if NDGI_JOINT_EPI
             if constexpr (H == 16) {
+#if NDGI_F16ACC
+                gelu_epilogue_h16_f16acc<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
+#else
                 gelu_epilogue_h16<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
+#endif
                 return;
             }
 #endif

@@ -23,6 +23,7 @@ cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* 
 cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
 cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts);
 cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter);
+cudaError_t tmem_f16_probe(uint32_t* host_out);
 }  // namespace ndgi
 
 struct ndgi_ctx {
@@ -428,6 +429,12 @@ ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_iter) {
     if (!cycles_per_iter || !iters) return fail(NDGI_ERR_ARG, "bad arguments");
     cudaError_t e = ndgi::mma_latency(iters, cycles_per_iter);
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "mma latency");
+}
+
+ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out) {
+    if (!host_out) return fail(NDGI_ERR_ARG, "bad arguments");
+    cudaError_t e = ndgi::tmem_f16_probe(host_out);
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "tmem f16 probe");
 }
 
 }  // extern "C"

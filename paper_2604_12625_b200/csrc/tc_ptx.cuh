@@ -138,6 +138,12 @@ __device__ __forceinline__ void tmem_ld_x4(uint32_t taddr, uint32_t (&r)[4]) {
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(taddr));
 }
+// 16 columns holding one 16-bit value each (f16 accumulators) -> 8 packed f16x2
+__device__ __forceinline__ void tmem_ld_x8_pack16(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_st_x8(uint32_t taddr, const uint32_t (&r)[8]) {
@@ -184,6 +190,12 @@ __device__ __forceinline__ uint64_t smem_desc_kmajor(uint32_t saddr, uint32_t lb
     d |= (uint64_t)((sbo >> 4) & 0x3fffu) << 32;
     d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
     return d;                // base offset 0, layout type 0 = SWIZZLE_NONE
+}
+
+// Instruction descriptor, kind::f16: A = B = f16, D = f16 (one value per TMEM
+// column, read back packed with tcgen05.ld .pack::16b), both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16_f16(uint32_t M, uint32_t N) {
+    return (0u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 // Instruction descriptor, kind::f16: A = B = f16, D = f32, both K-major.
