@@ -35,6 +35,9 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
+#ifndef NDGI_ONEWAIT
+#define NDGI_ONEWAIT 0
+#endif
 #ifndef NDGI_JOINT_EPI
 #define NDGI_JOINT_EPI 1
 #endif
@@ -192,7 +195,13 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 }
                 __syncwarp();
             }
+#if NDGI_ONEWAIT
+            // only warp 0 polls the mbarrier; the others sleep in the CTA barrier
+            if (warp == 0) ptx::mbar_wait_fast(bars, dph);
+            __syncthreads();
+#else
             ptx::mbar_wait_fast(bars, dph);
+#endif
             dph ^= 1u;
             ptx::tc_fence_after();
         };
