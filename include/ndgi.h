@@ -234,6 +234,14 @@ NDGI_API ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_i
  * read with .pack::16b (8 words).  Synchronous. */
 NDGI_API ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out);
 
+/* Cycle accounting of the fused kernel (only in builds with -DNDGI_PROFILE=1;
+ * NDGI_ERR_UNSUPPORTED otherwise): sums over warps of SM cycles spent in
+ * [barrier (incl. tcgen05.wait::st), MMA issue + mbarrier wait, GELU epilogues,
+ * gather, output, unit prologue, total, steps, step loops, warp-0 MMA issue,
+ * max resident CTAs per SM, sum of resident CTAs at CTA start] (12 words).
+ * reset != 0 zeroes the counters. */
+NDGI_API ndgi_status ndgi_debug_fused_profile(uint64_t* out12, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,7 @@ _SIGS = {
     "ndgi_debug_gelu_rate": (_I, [_U32, C.POINTER(_F), C.POINTER(C.c_double)]),
     "ndgi_debug_mma_latency": (_I, [_U32, C.POINTER(C.c_double)]),
     "ndgi_debug_tmem_f16_probe": (_I, [_P]),
+    "ndgi_debug_fused_profile": (_I, [_P, _I]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)

@@ -81,11 +81,12 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
     using Cfg = FusedCfg<H>;
     FusedSmem s{};
     uint32_t o = 0;
+    // every offset but the total is a compile-time constant (H, C template
+    // parameters): the R3-sized slice goes last
     s.b1 = o; o += Cfg::B1_BYTES;
     s.b2 = o; o += Cfg::B2_BYTES;
     s.b3 = o; o += Cfg::B3_BYTES;
     o = (o + 127) & ~127u;
-    s.uvt = o; o += (uint32_t)(R3 * R3 * 8);         // blended slice, f16x4 per texel
     s.uvc = o; o += kChunkTexels * 4;                 // decoded F_uv chunk, RGBA8 (4 per-warp parts)
     s.utcol = o; o += (uint32_t)(C * 4);              // V_ut per column, f16x2
     o = (o + 15) & ~15u;
@@ -93,6 +94,8 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
     s.cnt = o; o += 8 * 4;                            // (unused)
     s.bars = o; o += 8 * 8;                           // d_ready
     s.tmem_slot = o; o += 8;
+    o = (o + 127) & ~127u;
+    s.uvt = o; o += (uint32_t)(R3 * R3 * 8);         // blended slice, f16x4 per texel
     s.total = o;
     return s;
 }

@@ -35,6 +35,20 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
+#ifndef NDGI_PROFILE
+#define NDGI_PROFILE 0
+#endif
+#if NDGI_PROFILE
+// cycle accounting per warp (lane 0): [0] barrier, [1] mbarrier wait, [2] epilogue,
+// [3] gather, [4] output, [5] unit prologue, [6] total, [7] steps
+__device__ unsigned long long g_ndgi_prof[12];
+__device__ int g_ndgi_res[256];   // resident CTAs per SM (profiling builds only)
+#define PROF_T0() (_pt = clock64())
+#define PROF_ADD(k) do { long long _n = clock64(); if (lane == 0) prof[k] += _n - _pt; _pt = _n; } while (0)
+#else
+#define PROF_T0() do {} while (0)
+#define PROF_ADD(k) do {} while (0)
+#endif
 #ifndef NDGI_ONEWAIT
 #define NDGI_ONEWAIT 0
 #endif
@@ -42,7 +56,9 @@ constexpr int kThreads = 128;
 #define NDGI_JOINT_EPI 1
 #endif
 
-template <int H, int FMT_UV, int CT>
+// FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
+// no format switch, row pointers instead of 64-bit index arithmetic
+template <int H, int FMT_UV, int CT, bool FULL8>
 __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_kernel(const __grid_constant__ KParams p) {
     using Cfg = FusedCfg<H>;
     constexpr int S = Cfg::SLOTS;
@@ -86,6 +102,18 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     }
 
     uint32_t dph = 0u;   // d_ready phase
+#if NDGI_PROFILE
+    unsigned long long prof[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (tid == 0) {
+        const int now = atomicAdd(&g_ndgi_res[smid & 255], 1) + 1;
+        atomicMax(reinterpret_cast<unsigned long long*>(&g_ndgi_prof[10]), (unsigned long long)now);
+        atomicAdd(&g_ndgi_prof[11], (unsigned long long)now);
+    }
+    const long long prof_start = clock64();
+    long long _pt = prof_start;
+#endif
 
     for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
         const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
@@ -118,7 +146,11 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 
         // ---- a2: tile parameters -> shared memory -----------------------------------
         __syncthreads();  // previous unit's MMAs complete and all smem readers done
-        unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads);
+        {
+            PROF_T0();
+            unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads);
+            PROF_ADD(5);
+        }
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
         __syncthreads();
 
@@ -173,9 +205,11 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         // commits them to d_ready -> everyone waits for the accumulators
         auto run_layer = [&](auto layer) {
             constexpr int l = decltype(layer)::value;
+            PROF_T0();
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncthreads();
+            PROF_ADD(0);
             if (warp == 0) {
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
@@ -194,6 +228,9 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                     ptx::mma_commit(bars);
                 }
                 __syncwarp();
+#if NDGI_PROFILE
+                if (lane == 0) prof[9] += clock64() - _pt;
+#endif
             }
 #if NDGI_ONEWAIT
             // only warp 0 polls the mbarrier; the others sleep in the CTA barrier
@@ -202,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 #else
             ptx::mbar_wait_fast(bars, dph);
 #endif
+            PROF_ADD(1);
             dph ^= 1u;
             ptx::tc_fence_after();
         };
@@ -238,6 +276,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1, a1);
         };
 
+        // FULL8: this thread's texel of core row j_begin in the RGBA8 atlas
+        uint32_t* const orow = reinterpret_cast<uint32_t*>(p.out) + out_base + (size_t)j_begin * row_pitch + tid;
+        const uint32_t rp32 = (uint32_t)row_pitch;
+
         // a8: y of block (row j, blk) in slot s -> page cache
         auto output = [&](int j, int blk, int s) {
             const int i = blk * kThreads + tid;
@@ -245,6 +287,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             ptx::tmem_ld_x4(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, yv);
             ptx::tmem_wait_ld();
             const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
+            if constexpr (FULL8) {
+                orow[(size_t)((uint32_t)(j - j_begin) * rp32) + blk * kThreads] = rgba8_fma(y0f, y1f, y2f);
+                return;
+            }
             const size_t o = out_base + (size_t)j * row_pitch + i;
             if (out_fmt == OUT_RGBA8) {
                 const uint32_t v = rgba8_fma(y0f, y1f, y2f);
@@ -297,20 +343,43 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         };
 
         // S items per step; item n = (row j_begin + n / BPR, block n % BPR)
+#if NDGI_PROFILE
+        const long long loop_t0 = clock64();
+#endif
         for (int it = 0; it < nitems; it += S) {
+            PROF_T0();
 #pragma unroll
             for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s) % BPR, s);
+            PROF_ADD(3);
             run_layer(L0{});
+            PROF_T0();
             epilogues();
+            PROF_ADD(2);
             run_layer(L1{});
+            PROF_T0();
             epilogues();
+            PROF_ADD(2);
             run_layer(L2{});
+            PROF_T0();
 #pragma unroll
             for (int s = 0; s < S; ++s) output(j_begin + (it + s) / BPR, (it + s) % BPR, s);
+            PROF_ADD(4);
+#if NDGI_PROFILE
+            if (lane == 0) prof[7] += 1;
+#endif
         }
+#if NDGI_PROFILE
+        if (lane == 0) prof[8] += clock64() - loop_t0;
+#endif
     }
 
     // ---- teardown --------------------------------------------------------------------
+#if NDGI_PROFILE
+    prof[6] = clock64() - prof_start;
+    if (tid == 0) atomicSub(&g_ndgi_res[smid & 255], 1);
+    if (lane == 0)
+        for (int q = 0; q < 10; ++q) atomicAdd(&g_ndgi_prof[q], prof[q]);
+#endif
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc<Cfg::TM_COLS>(tmem);
@@ -320,7 +389,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 template <int H, int FMT_UV, int CT>
 static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
     const FusedSmem L = fused_smem_layout<H>(CT, p.R3);
-    auto kern = ndgi_fused_kernel<H, FMT_UV, CT>;
+    auto kern = (p.full && p.out_fmt == OUT_RGBA8) ? ndgi_fused_kernel<H, FMT_UV, CT, true>
+                                                   : ndgi_fused_kernel<H, FMT_UV, CT, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -349,6 +419,19 @@ static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s)
     kern<<<grid, kThreads, L.total, s>>>(p);
     return cudaGetLastError();
 }
+
+#if NDGI_PROFILE
+int fused_prof_read(unsigned long long* out8, int reset) {
+    cudaMemcpyFromSymbol(out8, g_ndgi_prof, 12 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_ndgi_prof, z, sizeof(z));
+    }
+    return 1;
+}
+#else
+int fused_prof_read(unsigned long long*, int) { return 0; }
+#endif
 
 int fused_ctas_per_sm(int H) { return H == 16 ? FusedCfg<16>::MIN_CTAS : FusedCfg<64>::MIN_CTAS; }
 

@@ -18,12 +18,14 @@ cudaError_t launch_ref(const KParams& p, cudaStream_t stream);
 cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_ws(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_hmma(const KParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_fused_pipe(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
 cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, cudaStream_t s);
 cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
 cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts);
 cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter);
 cudaError_t tmem_f16_probe(uint32_t* host_out);
+int fused_prof_read(unsigned long long* out8, int reset);
 }  // namespace ndgi
 
 struct ndgi_ctx {
@@ -181,15 +183,19 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
     if (mode == NDGI_MODE_FAST) {
         if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
         choose_strips(p, ctx->num_sms);
+        // NDGI_KERNEL selects the measured h = 16 alternatives (DESIGN.md
+        // §6.1 schedule experiments): ws, hmma, pipe
         static const int variant = [] {
-            const char* v = getenv("NDGI_KERNEL");   // "ws" / "hmma": h = 16 kernel variants
+            const char* v = getenv("NDGI_KERNEL");
             if (v && strcmp(v, "ws") == 0) return 1;
             if (v && strcmp(v, "hmma") == 0) return 2;
+            if (v && strcmp(v, "pipe") == 0) return 3;
             return 0;
         }();
-        if (variant == 1 && p.H == 16) e = ndgi::launch_fused_ws(p, ctx->num_sms, s);
-        else if (variant == 2 && p.H == 16) e = ndgi::launch_fused_hmma(p, ctx->num_sms, s);
-        else e = ndgi::launch_fused(p, ctx->num_sms, s);
+        if (p.H != 16 || variant == 0) e = ndgi::launch_fused(p, ctx->num_sms, s);
+        else if (variant == 1) e = ndgi::launch_fused_ws(p, ctx->num_sms, s);
+        else if (variant == 2) e = ndgi::launch_fused_hmma(p, ctx->num_sms, s);
+        else e = ndgi::launch_fused_pipe(p, ctx->num_sms, s);
     } else {
         e = ndgi::launch_ref(p, s);
     }
@@ -435,6 +441,13 @@ ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out) {
     if (!host_out) return fail(NDGI_ERR_ARG, "bad arguments");
     cudaError_t e = ndgi::tmem_f16_probe(host_out);
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "tmem f16 probe");
+}
+
+ndgi_status ndgi_debug_fused_profile(uint64_t* out8, int reset) {
+    if (!out8) return fail(NDGI_ERR_ARG, "bad arguments");
+    if (!ndgi::fused_prof_read(reinterpret_cast<unsigned long long*>(out8), reset))
+        return fail(NDGI_ERR_UNSUPPORTED, "built without NDGI_PROFILE");
+    return NDGI_OK;
 }
 
 }  // extern "C"

@@ -66,12 +66,38 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity
     return mbar_try_wait(bar, parity);
 #endif
 }
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+#ifndef NDGI_WAITMODE
+#define NDGI_WAITMODE 0
+#endif
 // hot-loop wait: try_wait suspends the warp in hardware (optionally with a
-// suspend-time hint); traps after ~2^28 polls so a lost commit cannot hang
+// suspend-time hint); traps after ~2^28 polls so a lost commit cannot hang.
+// NDGI_WAITMODE 1: non-suspending test_wait poll; 2: poll + short nanosleep
 __device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
+#if NDGI_WAITMODE == 1
+    while (!mbar_test_wait(bar, parity))
+        if (++n == (1u << 30)) __trap();
+#elif NDGI_WAITMODE == 2
+    while (!mbar_test_wait(bar, parity)) {
+        __nanosleep(32);
+        if (++n == (1u << 28)) __trap();
+    }
+#else
     while (!mbar_try_wait_hint(bar, parity))
         if (++n == (1u << 28)) __trap();
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -149,6 +175,12 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void tmem_st_x8(uint32_t taddr, const uint32_t (&r)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                  "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+// 8 packed f16x2 -> 16 columns holding one 16-bit value each (f16 accumulator layout)
+__device__ __forceinline__ void tmem_st_x8_unpack16(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.unpack::16b.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                  : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
