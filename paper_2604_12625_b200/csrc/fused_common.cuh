@@ -73,7 +73,7 @@ __device__ __forceinline__ void u8x4_to_h2(uint32_t q, uint32_t& rg, uint32_t& b
 
 struct FusedSmem {
     // byte offsets from the dynamic smem base
-    uint32_t b1, b2, b3, uvt, uvc, utcol, rowtab, cnt, bars, tmem_slot, total;
+    uint32_t b1, b2, b3, uvt, uvc, utcol, rowtab, colc, cnt, bars, tmem_slot, total;
 };
 
 template <int H>
@@ -91,6 +91,7 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
     s.utcol = o; o += (uint32_t)(C * 4);              // V_ut per column, f16x2
     o = (o + 15) & ~15u;
     s.rowtab = o; o += (uint32_t)(C * 16);            // per core row: y0*R3, y1*R3, fy (f16x2), V_vt (f16x2)
+    s.colc = o; o += (uint32_t)(C * 16);              // per core column: x0 / x1 slice byte offsets, fx (f16x2), V_ut
     s.cnt = o; o += 8 * 4;                            // (unused)
     s.bars = o; o += 8 * 8;                           // d_ready
     s.tmem_slot = o; o += 8;

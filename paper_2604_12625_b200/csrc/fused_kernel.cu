@@ -52,6 +52,9 @@ __device__ int g_ndgi_res[256];   // resident CTAs per SM (profiling builds only
 #ifndef NDGI_ONEWAIT
 #define NDGI_ONEWAIT 0
 #endif
+#ifndef NDGI_WAIT_GUARD
+#define NDGI_WAIT_GUARD 0   // 1: bounded mbarrier polls (trap after 2^28), for debugging
+#endif
 #ifndef NDGI_JOINT_EPI
 #define NDGI_JOINT_EPI 1
 #endif
@@ -73,7 +76,6 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     __half* sB1 = reinterpret_cast<__half*>(smem + L.b1);
     __half* sB2 = reinterpret_cast<__half*>(smem + L.b2);
     __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
-    uint2* sUvt = reinterpret_cast<uint2*>(smem + L.uvt);
     uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
     uint4* sRow = reinterpret_cast<uint4*>(smem + L.rowtab);
 
@@ -154,23 +156,23 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
         __syncthreads();
 
-        // per-thread column constants (thread tid owns columns b*128 + tid):
-        // byte offsets of the two F_uvt x taps in the blended slice, x weight, V_ut
-        uint32_t cxb0[BPR], cxb1[BPR], cfx[BPR], cut[BPR];
+        // per-column gather constants (column i = b*128 + tid, written and read by
+        // the same thread): byte offsets of the two F_uvt x taps from the smem
+        // base, the x weight, V_ut
+        uint4* sCol = reinterpret_cast<uint4*>(smem + L.colc);
 #pragma unroll
         for (int b = 0; b < BPR; ++b) {
             const int i = b * kThreads + tid;
             const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
             const float flx = floorf(sx);
-            cxb0[b] = (uint32_t)clampi((int)flx, 0, R3 - 1) * 8u;
-            cxb1[b] = (uint32_t)clampi((int)flx + 1, 0, R3 - 1) * 8u;
-            cfx[b] = pack_f16x2(sx - flx, sx - flx);
-            cut[b] = sUt[i];
+            sCol[i] = make_uint4(L.uvt + (uint32_t)clampi((int)flx, 0, R3 - 1) * 8u,
+                                 L.uvt + (uint32_t)clampi((int)flx + 1, 0, R3 - 1) * 8u, pack_f16x2(sx - flx, sx - flx),
+                                 sUt[i]);
         }
         const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
-        const uint8_t* sUvtB = reinterpret_cast<const uint8_t*>(sUvt);
-        // this warp's decoded F_uv chunk: [row][blk][32 columns] RGBA8
-        uint32_t* sUvw = reinterpret_cast<uint32_t*>(smem + L.uvc) + warp * (chunk_rows * BPR * 32);
+        // decoded F_uv chunk, row-major [chunk_rows][C] RGBA8 (each warp decodes
+        // the blocks of its own 32 columns)
+        uint32_t* sUv = reinterpret_cast<uint32_t*>(smem + L.uvc);
         // MMA descriptors of this unit's weights
         // layers 1, 2: f16 accumulators for h = 16 (the GELU input is f16 anyway);
         // layer 3 (the output y): fp32
@@ -189,13 +191,13 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const int br = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
             const int gbc = 32 * blk + 8 * warp + bc;       // block column in the tile
             const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + br) * (C >> 2) + gbc);
-            uint32_t* dst = sUvw + ((4 * br) * BPR + blk) * 32 + 4 * bc;
+            uint32_t* dst = sUv + (4 * br) * C + 4 * gbc;
             uint32_t rowv[4];
             __syncwarp();   // previous chunk fully gathered by this warp
             bc7_decode(raw, [&](int i, uint32_t v) {
                 rowv[i & 3] = v;
                 if ((i & 3) == 3)
-                    *reinterpret_cast<uint4*>(dst + (i >> 2) * BPR * 32) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
+                    *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
             });
             __syncwarp();
         };
@@ -236,8 +238,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             // only warp 0 polls the mbarrier; the others sleep in the CTA barrier
             if (warp == 0) ptx::mbar_wait_fast(bars, dph);
             __syncthreads();
-#else
+#elif NDGI_WAIT_GUARD
             ptx::mbar_wait_fast(bars, dph);
+#else
+            ptx::mbar_wait_spin(bars, dph);
 #endif
             PROF_ADD(1);
             dph ^= 1u;
@@ -247,21 +251,20 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         using L1 = std::integral_constant<int, 1>;
         using L2 = std::integral_constant<int, 2>;
 
-        // a4/a6: Eq. 4 input row of block (row, blk) -> A1 of slot s
-        auto gather = [&](int row, int blk, int s) {
-            const int jr = row % chunk_rows;
-            if (FMT_UV == FMT_BC7 && jr == 0 && blk == 0) decode_chunk(row);
+        // a4/a6: Eq. 4 input row of block (row, blk) -> A1 of slot s; jr = row
+        // within the decoded F_uv chunk
+        auto gather = [&](int row, int jr, int blk, int s) {
             const uint4 rt = sRow[row];                  // y0 row byte offset, y1 row byte offset, fy, V_vt
-            const uint2 t00 = *reinterpret_cast<const uint2*>(sUvtB + rt.x + cxb0[blk]);
-            const uint2 t10 = *reinterpret_cast<const uint2*>(sUvtB + rt.x + cxb1[blk]);
-            const uint2 t01 = *reinterpret_cast<const uint2*>(sUvtB + rt.y + cxb0[blk]);
-            const uint2 t11 = *reinterpret_cast<const uint2*>(sUvtB + rt.y + cxb1[blk]);
-            const uint32_t fx2 = cfx[blk];
+            const uint4 cc = sCol[blk * kThreads + tid]; // x0, x1 byte offsets (from smem base), fx, V_ut
+            const uint2 t00 = *reinterpret_cast<const uint2*>(smem + rt.x + cc.x);
+            const uint2 t10 = *reinterpret_cast<const uint2*>(smem + rt.x + cc.y);
+            const uint2 t01 = *reinterpret_cast<const uint2*>(smem + rt.y + cc.x);
+            const uint2 t11 = *reinterpret_cast<const uint2*>(smem + rt.y + cc.y);
             uint32_t a1[8];
-            a1[0] = hlerp2(hlerp2(t00.x, t10.x, fx2), hlerp2(t01.x, t11.x, fx2), rt.z);
-            a1[1] = hlerp2(hlerp2(t00.y, t10.y, fx2), hlerp2(t01.y, t11.y, fx2), rt.z);
+            a1[0] = hlerp2(hlerp2(t00.x, t10.x, cc.z), hlerp2(t01.x, t11.x, cc.z), rt.z);
+            a1[1] = hlerp2(hlerp2(t00.y, t10.y, cc.z), hlerp2(t01.y, t11.y, cc.z), rt.z);
             if (FMT_UV == FMT_BC7) {
-                u8x4_to_h2(sUvw[(jr * BPR + blk) * 32 + lane], a1[2], a1[3]);
+                u8x4_to_h2(sUv[jr * C + blk * kThreads + tid], a1[2], a1[3]);
             } else if (FMT_UV == FMT_U8) {
                 u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + blk * kThreads + tid), a1[2], a1[3]);
             } else {
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 a1[2] = hv.x;
                 a1[3] = hv.y;
             }
-            a1[4] = cut[blk];
+            a1[4] = cc.w;
             a1[5] = rt.w;
             a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
             a1[7] = 0u;
@@ -346,10 +349,13 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 #if NDGI_PROFILE
         const long long loop_t0 = clock64();
 #endif
-        for (int it = 0; it < nitems; it += S) {
+        constexpr int chunk_items = chunk_rows * BPR;   // strips are whole F_uv chunks
+        for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
+        if (FMT_UV == FMT_BC7) decode_chunk(j_begin + c0 / BPR);
+        for (int it = c0; it < c0 + chunk_items; it += S) {
             PROF_T0();
 #pragma unroll
-            for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s) % BPR, s);
+            for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s - c0) / BPR, (it + s) % BPR, s);
             PROF_ADD(3);
             run_layer(L0{});
             PROF_T0();
@@ -367,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 #if NDGI_PROFILE
             if (lane == 0) prof[7] += 1;
 #endif
+        }
         }
 #if NDGI_PROFILE
         if (lane == 0) prof[8] += clock64() - loop_t0;

@@ -100,6 +100,18 @@ __device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
 #endif
 }
 
+// hot-loop wait without the poll counter: the whole loop is TRYWAIT + branch
+// (the CUTLASS-style wait); used where the issuing code is unconditional
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "NDGI_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra NDGI_WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
