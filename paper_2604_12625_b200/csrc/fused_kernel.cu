@@ -279,6 +279,48 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1, a1);
         };
 
+        // C = 128, two consecutive rows per step: both rows usually sit between
+        // the same two F_uvt rows (R3 <= C/2), so the x-lerped taps of the first
+        // row serve the second (warp-uniform test, exact: same operands)
+        auto gather_rows2 = [&](int row, int jr) {
+            const uint4 rt0 = sRow[row], rt1 = sRow[row + 1];
+            const uint4 cc = sCol[tid];
+            auto xlerp = [&](uint32_t yoff, uint32_t& lo, uint32_t& hi) {
+                const uint2 a = *reinterpret_cast<const uint2*>(smem + yoff + cc.x);
+                const uint2 b = *reinterpret_cast<const uint2*>(smem + yoff + cc.y);
+                lo = hlerp2(a.x, b.x, cc.z);
+                hi = hlerp2(a.y, b.y, cc.z);
+            };
+            uint32_t y0lo, y0hi, y1lo, y1hi;
+            xlerp(rt0.x, y0lo, y0hi);
+            xlerp(rt0.y, y1lo, y1hi);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const uint4 rt = s ? rt1 : rt0;
+                if (s == 1 && (rt1.x != rt0.x || rt1.y != rt0.y)) {
+                    xlerp(rt1.x, y0lo, y0hi);
+                    xlerp(rt1.y, y1lo, y1hi);
+                }
+                uint32_t a1[8];
+                a1[0] = hlerp2(y0lo, y1lo, rt.z);
+                a1[1] = hlerp2(y0hi, y1hi, rt.z);
+                if (FMT_UV == FMT_BC7) {
+                    u8x4_to_h2(sUv[(jr + s) * C + tid], a1[2], a1[3]);
+                } else if (FMT_UV == FMT_U8) {
+                    u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)(row + s) * C + tid), a1[2], a1[3]);
+                } else {
+                    const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)(row + s) * C + tid);
+                    a1[2] = hv.x;
+                    a1[3] = hv.y;
+                }
+                a1[4] = cc.w;
+                a1[5] = rt.w;
+                a1[6] = 0x00003C00u;
+                a1[7] = 0u;
+                ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1, a1);
+            }
+        };
+
         // FULL8: this thread's texel of core row j_begin in the RGBA8 atlas
         uint32_t* const orow = reinterpret_cast<uint32_t*>(p.out) + out_base + (size_t)j_begin * row_pitch + tid;
         const uint32_t rp32 = (uint32_t)row_pitch;
@@ -354,8 +396,12 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         if (FMT_UV == FMT_BC7) decode_chunk(j_begin + c0 / BPR);
         for (int it = c0; it < c0 + chunk_items; it += S) {
             PROF_T0();
+            if constexpr (BPR == 1 && S == 2) {
+                gather_rows2(j_begin + it, it - c0);
+            } else {
 #pragma unroll
-            for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s - c0) / BPR, (it + s) % BPR, s);
+                for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s - c0) / BPR, (it + s) % BPR, s);
+            }
             PROF_ADD(3);
             run_layer(L0{});
             PROF_T0();
