@@ -125,18 +125,19 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def cpu_oracle_rate(lay, seed, target_s=8.0):
-    """The oracle as it stands, all host cores, bounded sample of the same workload."""
+def cpu_oracle_rate(lay, seed, target_s=12.0, max_tiles=512):
+    """The oracle as it stands, all host cores, bounded sample of the same workload
+    (about target_s seconds of CPU work, at most max_tiles tiles)."""
     import oracle
     cores = len(os.sched_getaffinity(0))
-    th = S.make_theta(lay, seed, tiles=list(range(64)))
-    sub = dict(lay, num_tiles=64, atlases=1, tiles_x=64, tiles_y=1)
+    th = S.make_theta(lay, seed, tiles=list(range(max_tiles)))
+    sub = dict(lay, num_tiles=max_tiles, atlases=1, tiles_x=max_tiles, tiles_y=1)
     M = oracle.Model(sub, th)
     t0 = time.perf_counter()
     M.decode_tiles([0], TS[7], nthreads=cores)           # calibration: one padded tile
     dt = time.perf_counter() - t0
     per_tile = dt
-    ntiles = int(max(1, min(64, target_s / max(per_tile, 1e-6))))
+    ntiles = int(max(1, min(max_tiles, target_s / max(per_tile, 1e-6))))
     t0 = time.perf_counter()
     ids = list(range(ntiles))
     M.decode_tiles(ids, TS[13], nthreads=cores)
@@ -338,7 +339,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     ap.add_argument("--no-vt", action="store_true", help="skip the VT batch-latency leg")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

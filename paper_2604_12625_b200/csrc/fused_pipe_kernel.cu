@@ -83,7 +83,7 @@ __device__ __forceinline__ void pipe_store(const KParams& p, size_t out_base, si
     }
 }
 
-template <int FMT_UV, int CT>
+template <int FMT_UV, int CT, bool FULL8>
 __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
     ndgi_fused_pipe_kernel(const __grid_constant__ KParams p) {
     using namespace pipe;
@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
     constexpr int C = CT;
     constexpr int BPR = CT / kPipeThreads;
     constexpr int chunk_rows = kChunkTexels / CT;
+    constexpr int chunk_steps = chunk_rows * BPR / S;
     extern __shared__ __align__(1024) uint8_t smem[];
     const FusedSmem L = fused_smem_layout<H>(C, p.R3);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -102,9 +103,10 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
     __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
     uint32_t* sBias2 = reinterpret_cast<uint32_t*>(smem + L.b2 + 512);   // a*b2 as 8 f16x2
     float* sBias3 = reinterpret_cast<float*>(smem + L.b3 + 512);         // b3 (fp32, exact)
-    const uint2* sUvt = reinterpret_cast<const uint2*>(smem + L.uvt);
     const uint32_t* sUt = reinterpret_cast<const uint32_t*>(smem + L.utcol);
     const uint4* sRow = reinterpret_cast<const uint4*>(smem + L.rowtab);
+    uint4* sCol = reinterpret_cast<uint4*>(smem + L.colc);
+    uint32_t* sUv = reinterpret_cast<uint32_t*>(smem + L.uvc);   // decoded F_uv chunk [chunk_rows][C]
 
     if (tid == 0) {
         ptx::mbar_init(bars, 1);
@@ -124,7 +126,6 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
     const uint64_t bd1 = ptx::smem_desc_kmajor(ptx::smem_addr(sB1), 128u, 256u);
     const uint64_t bd2 = ptx::smem_desc_kmajor(ptx::smem_addr(sB2), 128u, 256u);
     const uint64_t bd3 = ptx::smem_desc_kmajor(ptx::smem_addr(sB3), 128u, 256u);
-    const int out_fmt = p.out_fmt;
     uint32_t dph = 0u;
 
     for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
@@ -154,7 +155,6 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
         }
         const int nsteps = p.strip_rows * BPR / S;
         const int j_begin = strip * p.strip_rows;
-        const bool tiles_border = !p.full && B > 0;
 
         // ---- a2: tile parameters -> shared memory --------------------------------
         __syncthreads();   // previous unit: all MMAs complete, all smem readers done
@@ -190,21 +190,17 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
         ptx::fence_proxy_async_smem();   // B operands: generic-proxy writes -> tensor core
         __syncthreads();
 
-        // per-thread column constants (thread owns columns b*128 + tid)
-        uint32_t cxb0[BPR], cxb1[BPR], cfx[BPR], cut[BPR];
+        // per-column gather constants (written and read by the same thread)
 #pragma unroll
         for (int b = 0; b < BPR; ++b) {
             const int i = b * kPipeThreads + tid;
             const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
             const float flx = floorf(sx);
-            cxb0[b] = (uint32_t)clampi((int)flx, 0, R3 - 1) * 8u;
-            cxb1[b] = (uint32_t)clampi((int)flx + 1, 0, R3 - 1) * 8u;
-            cfx[b] = pack_f16x2(sx - flx, sx - flx);
-            cut[b] = sUt[i];
+            sCol[i] = make_uint4(L.uvt + (uint32_t)clampi((int)flx, 0, R3 - 1) * 8u,
+                                 L.uvt + (uint32_t)clampi((int)flx + 1, 0, R3 - 1) * 8u, pack_f16x2(sx - flx, sx - flx),
+                                 sUt[i]);
         }
         const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
-        const uint8_t* sUvtB = reinterpret_cast<const uint8_t*>(sUvt);
-        uint32_t* sUvw = reinterpret_cast<uint32_t*>(smem + L.uvc) + warp * (chunk_rows * BPR * 32);
 
         // a3: this warp's 32 BC7 blocks of the chunk starting at core row jc
         auto decode_chunk = [&](int jc) {
@@ -212,33 +208,31 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
             const int br = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
             const int gbc = 32 * blk + 8 * warp + bc;
             const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + br) * (C >> 2) + gbc);
-            uint32_t* dst = sUvw + ((4 * br) * BPR + blk) * 32 + 4 * bc;
+            uint32_t* dst = sUv + (4 * br) * C + 4 * gbc;
             uint32_t rowv[4];
             __syncwarp();
             bc7_decode(raw, [&](int i, uint32_t v) {
                 rowv[i & 3] = v;
                 if ((i & 3) == 3)
-                    *reinterpret_cast<uint4*>(dst + (i >> 2) * BPR * 32) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
+                    *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
             });
             __syncwarp();
         };
 
-        // a4/a6: Eq. 4 input row of item n (row j_begin + n / BPR, block n % BPR) -> A0 of slot s
-        auto gather = [&](int n, int s) {
-            const int row = j_begin + n / BPR, blk = n % BPR;
-            const int jr = row % chunk_rows;
-            if (FMT_UV == FMT_BC7 && jr == 0 && blk == 0) decode_chunk(row);
-            const uint4 rt = sRow[row];
-            const uint2 t00 = *reinterpret_cast<const uint2*>(sUvtB + rt.x + cxb0[blk]);
-            const uint2 t10 = *reinterpret_cast<const uint2*>(sUvtB + rt.x + cxb1[blk]);
-            const uint2 t01 = *reinterpret_cast<const uint2*>(sUvtB + rt.y + cxb0[blk]);
-            const uint2 t11 = *reinterpret_cast<const uint2*>(sUvtB + rt.y + cxb1[blk]);
-            const uint32_t fx2 = cfx[blk];
+        // a4/a6: Eq. 4 input rows of step n -> A0 of both slots
+        auto xlerp = [&](uint32_t yoff, const uint4& cc, uint32_t& lo, uint32_t& hi) {
+            const uint2 a = *reinterpret_cast<const uint2*>(smem + yoff + cc.x);
+            const uint2 b = *reinterpret_cast<const uint2*>(smem + yoff + cc.y);
+            lo = hlerp2(a.x, b.x, cc.z);
+            hi = hlerp2(a.y, b.y, cc.z);
+        };
+        auto finish_row = [&](int row, int jr, int blk, const uint4& rt, const uint4& cc, uint32_t y0lo, uint32_t y0hi,
+                              uint32_t y1lo, uint32_t y1hi, int s) {
             uint32_t a1[8];
-            a1[0] = hlerp2(hlerp2(t00.x, t10.x, fx2), hlerp2(t01.x, t11.x, fx2), rt.z);
-            a1[1] = hlerp2(hlerp2(t00.y, t10.y, fx2), hlerp2(t01.y, t11.y, fx2), rt.z);
+            a1[0] = hlerp2(y0lo, y1lo, rt.z);
+            a1[1] = hlerp2(y0hi, y1hi, rt.z);
             if (FMT_UV == FMT_BC7) {
-                u8x4_to_h2(sUvw[(jr * BPR + blk) * 32 + lane], a1[2], a1[3]);
+                u8x4_to_h2(sUv[jr * C + blk * kPipeThreads + tid], a1[2], a1[3]);
             } else if (FMT_UV == FMT_U8) {
                 u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + blk * kPipeThreads + tid),
                            a1[2], a1[3]);
@@ -247,11 +241,58 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
                 a1[2] = hv.x;
                 a1[3] = hv.y;
             }
-            a1[4] = cut[blk];
+            a1[4] = cc.w;
             a1[5] = rt.w;
             a1[6] = 0x00003C00u;   // k = 12: 1.0 (layer-1 bias column), k = 13: 0
             a1[7] = 0u;
             ptx::tmem_st_x8(tm_lane + s * SLOT + TA0, a1);
+        };
+        auto gather_step = [&](int n) {
+            const int it = n * S;   // first item of the step
+            const int c0 = (n / chunk_steps) * chunk_steps * S;
+            if (FMT_UV == FMT_BC7 && it == c0) decode_chunk(j_begin + c0 / BPR);
+            if constexpr (BPR == 1) {
+                // two consecutive rows, usually between the same two F_uvt rows
+                const int row = j_begin + it, jr = it - c0;
+                const uint4 rt0 = sRow[row], rt1 = sRow[row + 1];
+                const uint4 cc = sCol[tid];
+                uint32_t y0lo, y0hi, y1lo, y1hi;
+                xlerp(rt0.x, cc, y0lo, y0hi);
+                xlerp(rt0.y, cc, y1lo, y1hi);
+                finish_row(row, jr, 0, rt0, cc, y0lo, y0hi, y1lo, y1hi, 0);
+                if (rt1.x != rt0.x || rt1.y != rt0.y) {
+                    xlerp(rt1.x, cc, y0lo, y0hi);
+                    xlerp(rt1.y, cc, y1lo, y1hi);
+                }
+                finish_row(row + 1, jr + 1, 0, rt1, cc, y0lo, y0hi, y1lo, y1hi, 1);
+            } else {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int row = j_begin + (it + s) / BPR, jr = (it + s - c0) / BPR, blk = (it + s) % BPR;
+                    const uint4 rt = sRow[row];
+                    const uint4 cc = sCol[blk * kPipeThreads + tid];
+                    uint32_t y0lo, y0hi, y1lo, y1hi;
+                    xlerp(rt.x, cc, y0lo, y0hi);
+                    xlerp(rt.y, cc, y1lo, y1hi);
+                    finish_row(row, jr, blk, rt, cc, y0lo, y0hi, y1lo, y1hi, s);
+                }
+            }
+        };
+
+        // a8: page-cache writes of step n from registers
+        uint32_t* const orow = reinterpret_cast<uint32_t*>(p.out) + out_base + (size_t)j_begin * row_pitch + tid;
+        const uint32_t rp32 = (uint32_t)row_pitch;
+        auto output_step = [&](int n, const float (&y)[S][3]) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int it = n * S + s, jo = it / BPR, i = (it % BPR) * kPipeThreads + tid;
+                if constexpr (FULL8) {
+                    orow[(size_t)((uint32_t)jo * rp32) + (it % BPR) * kPipeThreads] = rgba8_fma(y[s][0], y[s][1], y[s][2]);
+                } else {
+                    pipe_store(p, out_base, row_pitch, j_begin + jo, i, C, B, !p.full && B > 0, p.out_fmt, y[s][0], y[s][1],
+                               y[s][2]);
+                }
+            }
         };
 
         // all A/D TMEM traffic of this thread done -> CTA barrier -> one lane
@@ -276,18 +317,26 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
             }
         };
         auto wait_d = [&]() {
-            ptx::mbar_wait_fast(bars, dph);
+            ptx::mbar_wait_spin(bars, dph);
             dph ^= 1u;
             ptx::tc_fence_after();
         };
+        auto gelu_to_a = [&](uint32_t (&x)[S][8]) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                uint32_t g[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) g[q] = gelu_scaled_f16x2(x[s][q]);
+                ptx::tmem_st_x8(tm_lane + s * SLOT + TA, g);
+            }
+        };
 
         // ---- a7/a8: the pipelined step loop ----------------------------------------
-#pragma unroll
-        for (int s = 0; s < S; ++s) gather(s, s);
+        gather_step(0);
         sync_issue(0);
+        float y[S][3];
         for (int step = 0; step < nsteps; ++step) {
-            const bool more = step + 1 < nsteps;
-            // layer 1 done: GELU -> A; D <- a*b2 for layer 2
+            // layer 1 done: D <- a*b2, GELU -> A; previous step's page-cache writes
             wait_d();
             {
                 uint32_t x[S][8];
@@ -303,21 +352,11 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
                     for (int s = 0; s < S; ++s) ptx::tmem_st_x8_unpack16(tm_lane + s * SLOT + TD, bb);
                 }
 #endif
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    uint32_t g[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) g[q] = gelu_scaled_f16x2(x[s][q]);
-                    ptx::tmem_st_x8(tm_lane + s * SLOT + TA, g);
-                }
+                if (step > 0) output_step(step - 1, y);
+                gelu_to_a(x);
             }
             sync_issue(1);
-            // next step's inputs while layer 2 runs
-            if (more) {
-#pragma unroll
-                for (int s = 0; s < S; ++s) gather((step + 1) * S + s, s);
-            }
-            // layer 2 done: (+ a*b2) GELU -> A
+            // layer 2 done: (+ a*b2) GELU -> A; next step's inputs -> A0
             wait_d();
             {
                 uint32_t x[S][8];
@@ -335,18 +374,12 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
                         for (int q = 0; q < 8; ++q) asm("add.rn.f16x2 %0, %0, %1;" : "+r"(x[s][q]) : "r"(bb[q]));
                 }
 #endif
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    uint32_t g[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) g[q] = gelu_scaled_f16x2(x[s][q]);
-                    ptx::tmem_st_x8(tm_lane + s * SLOT + TA, g);
-                }
+                if (step + 1 < nsteps) gather_step(step + 1);
+                gelu_to_a(x);
             }
             sync_issue(2);
             // output layer done: y -> registers, release D, start the next step
             wait_d();
-            float y[S][3];
             {
                 uint32_t yv[S][4];
 #pragma unroll
@@ -360,15 +393,9 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
                     y[s][2] = __uint_as_float(yv[s][2]) + b3.z;
                 }
             }
-            if (more) sync_issue(0);
-            // a8: page-cache writes of this step, overlapping the next layer-1 MMA
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int n = step * S + s;
-                pipe_store(p, out_base, row_pitch, j_begin + n / BPR, (n % BPR) * kPipeThreads + tid, C, B, tiles_border,
-                           out_fmt, y[s][0], y[s][1], y[s][2]);
-            }
+            if (step + 1 < nsteps) sync_issue(0);
         }
+        output_step(nsteps - 1, y);
     }
 
     ptx::tc_fence_before();
@@ -379,7 +406,8 @@ __global__ void __launch_bounds__(kPipeThreads, NDGI_PIPE_MIN_CTAS)
 template <int FMT_UV, int CT>
 static cudaError_t launch_pipe_t(const KParams& p, int num_sms, cudaStream_t s) {
     const FusedSmem L = fused_smem_layout<16>(CT, p.R3);
-    auto kern = ndgi_fused_pipe_kernel<FMT_UV, CT>;
+    auto kern = (p.full && p.out_fmt == OUT_RGBA8) ? ndgi_fused_pipe_kernel<FMT_UV, CT, true>
+                                                   : ndgi_fused_pipe_kernel<FMT_UV, CT, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
