@@ -315,19 +315,23 @@ def vt_latency(ndgi, torch, args):
         batches = S.vt_batches(lay["num_tiles"], n, 16 + 64, seed)
         cache = torch.empty((n, 136, 136, 4), dtype=torch.uint8, device="cuda")
         ids = [torch.from_numpy(b[0].astype(np.int32)).cuda() for b in batches]
-        lat = []
+        lat, host = [], []
         for f, (b, t) in enumerate(batches):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
+            h0 = time.perf_counter()
             ndgi.ndgi_decode_tiles(ctx, ids[f], None, n, n, t, cache, "rgba8", "fast", stream)
+            h1 = time.perf_counter()
             e1.record(stream)
             e1.synchronize()
             if f >= 16:
                 lat.append(e0.elapsed_time(e1) * 1e3)
+                host.append((h1 - h0) * 1e6)
         lat.sort()
+        host.sort()
         p50 = lat[len(lat) // 2]
         res[str(n)] = {"p50": p50, "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))],
-                       "gtexel_s": n * 136 * 136 / (p50 * 1e-6) / 1e9}
+                       "gtexel_s": n * 136 * 136 / (p50 * 1e-6) / 1e9, "host_call_us_p50": host[len(host) // 2]}
     return res
 
 

@@ -139,9 +139,13 @@ typedef struct ndgi_params {
 /*
  * Creates a context on CUDA device `device` for the given layout and Theta.
  * Validates the layout (synchronously), queries the device (must be an
- * sm_100 part for decode), repacks nothing from Theta (zero-copy), uploads
- * the small per-context state and synchronises once.  *out is set only on
- * NDGI_OK.  Errors: ARG (null/invalid layout), DEVICE, CUDA, NOMEM.
+ * sm_100 part for decode), keeps the feature maps zero-copy (borrowed), and
+ * for layouts NDGI_MODE_FAST takes derives the per-tile tensor-core weight
+ * operands from `mlp` once (context-owned device memory: 2,880 B per tile
+ * for h = 16, 16,128 B for h = 64; the MLP weights must therefore not change
+ * after this call -- create a new context instead), then synchronises once.
+ * *out is set only on NDGI_OK.  Errors: ARG (null/invalid layout), DEVICE,
+ * CUDA, NOMEM.
  */
 NDGI_API ndgi_status ndgi_load(const ndgi_layout* layout, const ndgi_params* params, int device, ndgi_ctx** out);
 

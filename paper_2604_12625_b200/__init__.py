@@ -129,10 +129,18 @@ class Context:
     def full_texels(self) -> int:
         return int(_lib.ndgi_full_texels(C.byref(self.layout)))
 
+    def close(self) -> None:
+        """Frees the context (idempotent); also called when the object is collected."""
+        lib = _lib
+        if getattr(self, "handle", None) and lib is not None:
+            lib.ndgi_free(self.handle)
+        self.handle = None
+
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib.ndgi_free(self.handle)
-            self.handle = None
+        try:
+            self.close()
+        except Exception:   # interpreter shutdown: module globals may be gone
+            pass
 
 
 def ndgi_load(lay: dict, theta: dict, device: int = 0) -> Context:

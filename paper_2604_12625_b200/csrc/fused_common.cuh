@@ -171,6 +171,87 @@ __device__ __forceinline__ void gelu_epilogue2_h16(uint32_t d0, uint32_t a0, uin
     ptx::tmem_st_x8(a1, h);
 }
 
+// ---- load-time weight prepack ------------------------------------------------
+// Per tile, the t-independent part of the three tcgen05 B operands with the
+// GELU folds of DESIGN.md §6.1, already in the smem layout (bofs), followed by
+// [b1[n], W1[n][12..15]] as fp32 for the per-call gamma(t) fold into layer-1's
+// bias column (k = 12, left 0 here).  Built once by ndgi_load; a work unit
+// then moves it to smem with one coalesced 16-B copy per thread.
+template <int H>
+struct WPack {
+    using Cfg = FusedCfg<H>;
+    static constexpr uint32_t B_BYTES = Cfg::B1_BYTES + Cfg::B2_BYTES + Cfg::B3_BYTES;
+    static constexpr uint32_t G_BYTES = ((uint32_t)H * 5 * 4 + 15u) & ~15u;
+    static constexpr uint32_t BYTES = B_BYTES + G_BYTES;
+};
+
+template <int H>
+__global__ void prep_weights_kernel(const uint16_t* __restrict__ mlp, size_t tile_elems, float s_uv,
+                                    uint8_t* __restrict__ out, int num_tiles) {
+    using Cfg = FusedCfg<H>;
+    const float a = kGeluA;
+    for (int k = blockIdx.x; k < num_tiles; k += gridDim.x) {
+        const uint16_t* w = mlp + tile_elems * k;
+        const uint16_t *W1 = w, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
+        uint8_t* o = out + (size_t)WPack<H>::BYTES * k;
+        __half* B1 = reinterpret_cast<__half*>(o);
+        __half* B2 = reinterpret_cast<__half*>(o + Cfg::B1_BYTES);
+        __half* B3 = reinterpret_cast<__half*>(o + Cfg::B1_BYTES + Cfg::B2_BYTES);
+        float* G = reinterpret_cast<float*>(o + WPack<H>::B_BYTES);
+        for (int e = threadIdx.x; e < H * 16; e += blockDim.x) {
+            const int n = e >> 4, kk = e & 15;
+            float v = 0.f;
+            if (kk < 12) v = half_bits_to_float(W1[n * 16 + kk]) * ((kk >= 4 && kk < 8) ? s_uv : a);
+            B1[bofs(n, kk, 16)] = __float2half_rn(v);
+        }
+        for (int e = threadIdx.x; e < H * Cfg::K2; e += blockDim.x) {
+            const int n = e / Cfg::K2, kk = e % Cfg::K2;
+            float v = 0.f;
+            if (kk < H) v = 0.5f * half_bits_to_float(W2[n * H + kk]);
+            else if (kk == H) v = a * half_bits_to_float(b2[n]);
+            B2[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
+        }
+        for (int e = threadIdx.x; e < 16 * Cfg::K2; e += blockDim.x) {
+            const int n = e / Cfg::K2, kk = e % Cfg::K2;
+            float v = 0.f;
+            if (n < 3) {
+                if (kk < H) v = half_bits_to_float(W3[n * H + kk]) * (0.5f / a);
+                else if (kk == H) v = half_bits_to_float(b3[n]);
+            }
+            B3[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
+        }
+        for (int e = threadIdx.x; e < H * 5; e += blockDim.x) {
+            const int n = e / 5, g = e % 5;
+            G[e] = half_bits_to_float(g == 0 ? b1[n] : W1[n * 16 + 11 + g]);
+        }
+    }
+}
+
+// the prepacked B operands of tile k -> smem (L.b1, L.b2, L.b3 are contiguous),
+// patching layer-1's bias column with a (b1 + W1_gamma gamma(t)) (R6) on the way
+template <int H>
+__device__ __forceinline__ void copy_prepacked_weights(const KParams& p, const TConst& tc, int k, uint8_t* smem,
+                                                       const FusedSmem& L, int tid, int nthr) {
+    using Cfg = FusedCfg<H>;
+    const uint8_t* base = p.wpack + (size_t)WPack<H>::BYTES * k;
+    const uint4* src = reinterpret_cast<const uint4*>(base);
+    const float* G = reinterpret_cast<const float*>(base + WPack<H>::B_BYTES);
+    uint4* dst = reinterpret_cast<uint4*>(smem + L.b1);
+    for (int c = tid; c < (int)(WPack<H>::B_BYTES / 16); c += nthr) {
+        uint4 v = __ldg(src + c);
+        if (c < Cfg::B1_BYTES / 16 && ((c >> 3) & 1)) {
+            // this chunk is k = 8..15 of B1 row n: element k = 12 is v.z's low half
+            const int n = (c >> 4) * 8 + (c & 7);
+            float acc = __ldg(G + n * 5);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) acc = fmaf(__ldg(G + n * 5 + 1 + g), tc.gamma[g], acc);
+            const uint32_t hb = (uint32_t)__half_as_ushort(__float2half_rn(kGeluA * acc));
+            v.z = (v.z & 0xffff0000u) | hb;
+        }
+        dst[c] = v;
+    }
+}
+
 // a2 (+a5): one unit's parameters -> shared memory: the tile's MLP as tcgen05
 // B operands (with the folds of DESIGN.md §6.1), the tau-blended F_uvt slice,
 // V_ut per column and the per-row gather table (F_uvt y taps, V_vt).

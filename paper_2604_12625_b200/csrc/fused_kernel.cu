@@ -27,6 +27,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "fused_common.cuh"
@@ -150,7 +151,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         __syncthreads();  // previous unit's MMAs complete and all smem readers done
         {
             PROF_T0();
-            unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads);
+            copy_prepacked_weights<H>(p, tc, k, smem, L, tid, kThreads);
+            unit_prologue<H, FMT_UV, C, false>(p, tc, k, smem, L, tid, kThreads);
             PROF_ADD(5);
         }
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
@@ -185,18 +187,24 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         const int out_fmt = p.out_fmt;
         const bool tiles_border = !p.full && B > 0;
 
-        // a3: this warp's 32 BC7 blocks of the chunk starting at core row jc
-        auto decode_chunk = [&](int jc) {
+        // a3: this warp's BC7 blocks of the chunk of `crows` core rows (4..16)
+        // starting at row jc: one block per lane; for short chunks (small VT
+        // batches) the spare lanes decode a duplicate and do not store, so the
+        // warp-uniform decoder paths stay converged
+        auto decode_chunk = [&](int jc, int crows) {
             constexpr int bpw = 8 * BPR;                    // blocks per block-row for this warp
-            const int br = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
+            const int br_all = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
+            const int nbr = crows >> 2;
+            const int br = br_all < nbr ? br_all : br_all % nbr;
             const int gbc = 32 * blk + 8 * warp + bc;       // block column in the tile
             const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + br) * (C >> 2) + gbc);
             uint32_t* dst = sUv + (4 * br) * C + 4 * gbc;
+            const bool store = br_all < nbr;
             uint32_t rowv[4];
             __syncwarp();   // previous chunk fully gathered by this warp
             bc7_decode(raw, [&](int i, uint32_t v) {
                 rowv[i & 3] = v;
-                if ((i & 3) == 3)
+                if ((i & 3) == 3 && store)
                     *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
             });
             __syncwarp();
@@ -391,9 +399,11 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 #if NDGI_PROFILE
         const long long loop_t0 = clock64();
 #endif
-        constexpr int chunk_items = chunk_rows * BPR;   // strips are whole F_uv chunks
+        // strips are whole F_uv chunks, or (small batches) 4..8-row strips
+        const int crows = p.strip_rows < chunk_rows ? p.strip_rows : chunk_rows;
+        const int chunk_items = crows * BPR;
         for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
-        if (FMT_UV == FMT_BC7) decode_chunk(j_begin + c0 / BPR);
+        if (FMT_UV == FMT_BC7) decode_chunk(j_begin + c0 / BPR, crows);
         for (int it = c0; it < c0 + chunk_items; it += S) {
             PROF_T0();
             if constexpr (BPR == 1 && S == 2) {
@@ -439,12 +449,30 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 }
 
 // ---- host-side launch helpers ---------------------------------------------------
-template <int H, int FMT_UV, int CT>
-static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
-    const FusedSmem L = fused_smem_layout<H>(CT, p.R3);
-    auto kern = (p.full && p.out_fmt == OUT_RGBA8) ? ndgi_fused_kernel<H, FMT_UV, CT, true>
-                                                   : ndgi_fused_kernel<H, FMT_UV, CT, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+// Launch configuration of one kernel instantiation on one device for one smem
+// size: computed once (attribute calls cost microseconds, which a small VT
+// batch would otherwise pay on every call).
+struct LaunchCfg {
+    int dev = -1;
+    uint32_t smem = 0;
+    int occ = 0;
+};
+
+template <typename K>
+static cudaError_t fused_launch_cfg(K kern, uint32_t smem, int tmem_cols, int& occ_out) {
+    constexpr int kMaxDev = 16;
+    static std::mutex mu;
+    static LaunchCfg cache[kMaxDev];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    LaunchCfg& c = cache[dev % kMaxDev];
+    if (c.dev == dev && c.smem == smem) {
+        occ_out = c.occ;
+        return cudaSuccess;
+    }
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
@@ -453,22 +481,37 @@ static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s)
     cudaFuncAttributes fa;
     e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
-    int dev = 0, smem_sm = 0, regs_sm = 0;
-    cudaGetDevice(&dev);
+    int smem_sm = 0, regs_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
     const int regs_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (kThreads / 32);   // per-warp allocation unit 256
-    const int smem_cta = (int)L.total + (int)fa.sharedSizeBytes + 1024;   // + per-CTA reserved smem
+    const int smem_cta = (int)smem + (int)fa.sharedSizeBytes + 1024;   // + per-CTA reserved smem
     int occ = regs_sm / regs_cta;
     if (smem_sm / smem_cta < occ) occ = smem_sm / smem_cta;
-    const int tmem_cap = 512 / (int)FusedCfg<H>::TM_COLS;
+    const int tmem_cap = 512 / tmem_cols;
     if (occ > tmem_cap) occ = tmem_cap;
     if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (getenv("NDGI_VERBOSE"))
+        fprintf(stderr, "[ndgi] fused launch cfg: occ=%d (regs %d, local %zu) smem=%u\n", occ, fa.numRegs,
+                fa.localSizeBytes, smem);
+    c.dev = dev;
+    c.smem = smem;
+    c.occ = occ;
+    occ_out = occ;
+    return cudaSuccess;
+}
+
+template <int H, int FMT_UV, int CT>
+static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
+    const FusedSmem L = fused_smem_layout<H>(CT, p.R3);
+    const bool full8 = p.full && p.out_fmt == OUT_RGBA8;
+    auto kern = full8 ? ndgi_fused_kernel<H, FMT_UV, CT, true> : ndgi_fused_kernel<H, FMT_UV, CT, false>;
+    int occ = 0;
+    cudaError_t e = full8 ? fused_launch_cfg(ndgi_fused_kernel<H, FMT_UV, CT, true>, L.total, FusedCfg<H>::TM_COLS, occ)
+                          : fused_launch_cfg(ndgi_fused_kernel<H, FMT_UV, CT, false>, L.total, FusedCfg<H>::TM_COLS, occ);
+    if (e != cudaSuccess) return e;
     const uint32_t cap = (uint32_t)(num_sms * occ);
     const uint32_t grid = p.units < cap ? p.units : cap;
-    if (getenv("NDGI_VERBOSE"))
-        fprintf(stderr, "[ndgi] fused<H=%d,uv=%d,C=%d> occ=%d (regs %d, local %zu) grid=%u units=%u strips=%d smem=%u\n",
-                H, FMT_UV, CT, occ, fa.numRegs, fa.localSizeBytes, grid, p.units, p.strips_per_tile, L.total);
     kern<<<grid, kThreads, L.total, s>>>(p);
     return cudaGetLastError();
 }
@@ -485,6 +528,17 @@ int fused_prof_read(unsigned long long* out8, int reset) {
 #else
 int fused_prof_read(unsigned long long*, int) { return 0; }
 #endif
+
+size_t wpack_tile_bytes(int H) { return H == 16 ? WPack<16>::BYTES : WPack<64>::BYTES; }
+
+cudaError_t prep_weights(const uint16_t* mlp, size_t tile_elems, int H, int fmt_uv, uint8_t* out, int num_tiles,
+                         cudaStream_t s) {
+    const float s_uv = fmt_uv == FMT_F16 ? kGeluA : kGeluA / 255.0f;   // F_uv enters in q units (R8)
+    const int grid = num_tiles < 4096 ? num_tiles : 4096;
+    if (H == 16) prep_weights_kernel<16><<<grid, 256, 0, s>>>(mlp, tile_elems, s_uv, out, num_tiles);
+    else prep_weights_kernel<64><<<grid, 256, 0, s>>>(mlp, tile_elems, s_uv, out, num_tiles);
+    return cudaGetLastError();
+}
 
 int fused_ctas_per_sm(int H) { return H == 16 ? FusedCfg<16>::MIN_CTAS : FusedCfg<64>::MIN_CTAS; }
 

@@ -20,6 +20,9 @@ cudaError_t launch_fused_ws(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_hmma(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_pipe(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
+size_t wpack_tile_bytes(int H);
+cudaError_t prep_weights(const uint16_t* mlp, size_t tile_elems, int H, int fmt_uv, uint8_t* out, int num_tiles,
+                         cudaStream_t s);
 cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, cudaStream_t s);
 cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
 cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts);
@@ -34,6 +37,7 @@ struct ndgi_ctx {
     int device;
     int num_sms;
     uint32_t* d_err;
+    uint8_t* wpack;   // prepacked tcgen05 B operands per tile (FAST layouts), owned
     // host-buffer path
     cudaStream_t hstream[2];
     cudaEvent_t hevent[2];
@@ -148,6 +152,7 @@ void fill_common(const ndgi_ctx* ctx, ndgi::KParams& p) {
     p.ut = static_cast<const uint8_t*>(ctx->P.ut);
     p.vt = static_cast<const uint8_t*>(ctx->P.vt);
     p.mlp = ctx->P.mlp;
+    p.wpack = ctx->wpack;
     p.uv_tile_bytes = map2d_bytes(L.fmt_uv, L.uv_res, L.uv_res, 4);
     p.uvt_slice_bytes = map2d_bytes(L.fmt_uvt, L.uvt_res, L.uvt_res, 4);
     p.uvt_tile_bytes = p.uvt_slice_bytes * L.uvt_depth;
@@ -161,16 +166,29 @@ ndgi_status check_t(float t) {
     return NDGI_OK;
 }
 
-// work decomposition of the fused kernel: smallest number of strips per tile
-// that still gives >= 2 waves of work units (VT batches), rows multiple of
-// the 2048-texel F_uv chunk
-void choose_strips(ndgi::KParams& p, int num_sms) {
+// work decomposition of the fused kernel (strips of core rows per tile).
+// Strips are whole 2048-texel F_uv chunks, or -- default kernel -- down to
+// min_rows = 4 rows (one BC7 block row).  More strips mean more parallel
+// units but one tile prologue per unit; the measured VT optimum (config 3,
+// scripts/strip_sweep.py: n = 8/32/128/512 -> 32/16/8/4 strips) follows
+// s^2 * requests >= 8192.  Kernels without short strips: >= 2 waves.
+void choose_strips(ndgi::KParams& p, int num_sms, int min_rows) {
     const int C = p.C;
     const int chunk_rows = 2048 / C;
-    const int max_strips = C / chunk_rows;
-    const uint64_t target = 2ull * num_sms * ndgi::fused_ctas_per_sm(p.H);
+    const int max_strips = C / (min_rows < chunk_rows ? min_rows : chunk_rows);
+    const uint64_t req = (uint64_t)p.nt * p.n_req;
     int s = 1;
-    while (s < max_strips && (uint64_t)p.nt * p.n_req * s < target) s *= 2;
+    if (min_rows < chunk_rows) {
+        while (s < max_strips && (uint64_t)s * s * req < 8192u) s *= 2;
+    } else {
+        const uint64_t target = 2ull * num_sms * ndgi::fused_ctas_per_sm(p.H);
+        while (s < max_strips && req * s < target) s *= 2;
+    }
+    static const int forced = [] {   // experiments: NDGI_STRIPS=<power of 2>
+        const char* v = getenv("NDGI_STRIPS");
+        return v ? atoi(v) : 0;
+    }();
+    if (forced > 0) s = forced < max_strips ? forced : max_strips;
     p.strips_per_tile = s;
     p.strip_rows = C / s;
     p.units = (uint32_t)((uint64_t)p.nt * p.n_req * s);
@@ -182,7 +200,6 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
     cudaError_t e;
     if (mode == NDGI_MODE_FAST) {
         if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
-        choose_strips(p, ctx->num_sms);
         // NDGI_KERNEL selects the measured h = 16 alternatives (DESIGN.md
         // §6.1 schedule experiments): ws, hmma, pipe
         static const int variant = [] {
@@ -192,6 +209,8 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
             if (v && strcmp(v, "pipe") == 0) return 3;
             return 0;
         }();
+        const bool deflt = p.H != 16 || variant == 0;
+        choose_strips(p, ctx->num_sms, deflt ? 4 : 16);
         if (p.H != 16 || variant == 0) e = ndgi::launch_fused(p, ctx->num_sms, s);
         else if (variant == 1) e = ndgi::launch_fused_ws(p, ctx->num_sms, s);
         else if (variant == 2) e = ndgi::launch_fused_hmma(p, ctx->num_sms, s);
@@ -286,11 +305,26 @@ ndgi_status ndgi_load(const ndgi_layout* layout, const ndgi_params* params, int 
         return cuda_fail(e, "cudaMalloc(error counter)");
     }
     cudaMemset(c->d_err, 0, sizeof(uint32_t));
-    e = cudaDeviceSynchronize();
+    int fast = 0;
+    validate(layout, &fast);
+    if (fast) {
+        // G_Phi's folded B operands, once per context
+        const size_t tb = ndgi::wpack_tile_bytes((int)layout->hidden);
+        e = cudaMalloc(&c->wpack, tb * layout->num_tiles);
+        if (e != cudaSuccess) {
+            cudaFree(c->d_err);
+            delete c;
+            return cuda_fail(e, "cudaMalloc(prepacked weights)");
+        }
+        e = ndgi::prep_weights(params->mlp, mlp_elems(layout->hidden), (int)layout->hidden, (int)layout->fmt_uv,
+                               c->wpack, (int)layout->num_tiles, 0);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(c->d_err);
+        if (c->wpack) cudaFree(c->wpack);
         delete c;
-        return cuda_fail(e, "ndgi_load sync");
+        return cuda_fail(e, "ndgi_load prepack / sync");
     }
     *out = c;
     return NDGI_OK;
@@ -404,6 +438,7 @@ ndgi_status ndgi_free(ndgi_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaDeviceSynchronize();
     cudaFree(ctx->d_err);
+    if (ctx->wpack) cudaFree(ctx->wpack);
     for (int i = 0; i < 2; ++i) {
         if (ctx->stage[i]) cudaFree(ctx->stage[i]);
         if (ctx->hstream[i]) cudaStreamDestroy(ctx->hstream[i]);

@@ -35,6 +35,7 @@ struct KParams {
     const uint8_t* ut;
     const uint8_t* vt;
     const uint16_t* mlp;
+    const uint8_t* wpack;       // per-tile prepacked tcgen05 B operands (ndgi_load), or nullptr
     size_t uv_tile_bytes, uvt_tile_bytes, uvt_slice_bytes, line_tile_bytes, mlp_tile_elems;
     // per-call constants (call setup), one set per query time,
     // computed on the host in fp64

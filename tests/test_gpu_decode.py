@@ -243,6 +243,20 @@ def test_small_batches_strips():
         assert mx <= FAST_MAX and mean <= FAST_MEAN
 
 
+def test_strip_split_is_bit_exact():
+    # a tile decoded alone (4-row strips, 32 units) == the same tile inside a
+    # batch big enough for whole-tile units (RGBA8 and RGBA32F, bit-equal)
+    lay, seed = S.config("c1")
+    th = S.make_theta(lay, seed)
+    ctx = _load(lay, th)
+    big = [k % 4 for k in range(2400)]
+    for fmt in ("rgba8", "rgba32f"):
+        many = gpu_tiles(ctx, big, 0.45, fmt)
+        for k in range(4):
+            one = gpu_tiles(ctx, [k], 0.45, fmt)
+            np.testing.assert_array_equal(one[0], many[k])
+
+
 def test_bad_ids_and_arguments():
     lay, seed = S.config("c1")
     th = S.make_theta(lay, seed)
