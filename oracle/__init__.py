@@ -74,6 +74,9 @@ def lib():
             "oracle_quantize_rgba8_f64": (None, [P, C.c_size_t, P]),
             "oracle_quantize_rgba8_f32": (None, [P, C.c_size_t, C.c_size_t, P]),
             "oracle_mlp_params": (C.c_size_t, [I]),
+            "oracle_mean_at": (I, [P, P, I, D, P]),
+            "oracle_restore": (D, [D, D, D]),
+            "oracle_sample_lighting": (I, [P, P, I, I, I, I, I, D, D, I, D, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -219,3 +222,40 @@ def quantize_rgba8(y3: np.ndarray) -> np.ndarray:
     out = np.zeros(y.shape[:-1] + (4,), np.uint8)
     lib().oracle_quantize_rgba8_f64(_ptr(y), n, _ptr(out))
     return out
+
+
+# ---------------------------------------------------------------- shading side (R21-R25)
+def mean_at(times, means, t: float) -> np.ndarray:
+    """R22: per-channel mean at t, linear between bracketing bake times; raises outside."""
+    tm = np.ascontiguousarray(times, np.float64)
+    mu = np.ascontiguousarray(means, np.float64).reshape(-1, 3)
+    out = np.zeros(3, np.float64)
+    if lib().oracle_mean_at(_ptr(tm), _ptr(mu), len(tm), float(t), _ptr(out)):
+        raise ValueError("t outside the bake times")
+    return out
+
+
+def restore(x: float, g: float, mu: float) -> float:
+    return lib().oracle_restore(float(x), float(g), float(mu))
+
+
+def sample_lighting(cache: np.ndarray, page_table: np.ndarray, core: int, border: int, tiles_x: int, tiles_y: int,
+                    atlas: np.ndarray, uv: np.ndarray, bucket: int, g: float, mu: np.ndarray):
+    """cache [slots][P][P][4] u8, page_table [tiles][2] int32 (slot, bucket), atlas [n], uv [n][2],
+    mu [atlases][3]: returns (rgb [n][3] float64, resident [n] bool)."""
+    cache = np.ascontiguousarray(cache, np.uint8)
+    pt = np.ascontiguousarray(page_table, np.int32)
+    mu = np.ascontiguousarray(mu, np.float64).reshape(-1, 3)
+    n = len(uv)
+    out = np.full((n, 3), np.nan)
+    ok = np.zeros(n, bool)
+    o3 = np.zeros(3, np.float64)
+    L = lib()
+    for i in range(n):
+        a = int(atlas[i])
+        r = L.oracle_sample_lighting(_ptr(cache), _ptr(pt), core, border, tiles_x, tiles_y, a, float(uv[i][0]),
+                                     float(uv[i][1]), int(bucket), float(g), _ptr(mu[a]), _ptr(o3))
+        if r == 0:
+            out[i] = o3
+            ok[i] = True
+    return out, ok

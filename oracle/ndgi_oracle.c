@@ -553,3 +553,80 @@ void oracle_quantize_rgba8_f32(const float *y, size_t stride, size_t n, uint8_t 
         out[4 * i + 3] = 255;
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Shading side of the page cache.             */
+/*                                                                      */
+/* The physical texture (page cache) holds the decoder output y in the  */
+/* 8-bit 4-channel format per padded tile slot; during shading  */
+/* "we first sample the page table to locate each tile within the       */
+/* physical texture, then sample the physical texture",  */
+/* with filtering served by the tile's border, and the per-     */
+/* channel means stored at each bake time "are later used during        */
+/* rendering to restore the original lightmap data" after the   */
+/* gamma correction applied before training.  Readings R21-R25  */
+/* (DESIGN.md): restore x^g * mu_hat(t,c) after filtering (R21), mu_hat */
+/* linear between bracketing bake times (R22, SPEC postprocess),        */
+/* page-table entry = (slot, time bucket) (R24), sample position and    */
+/* owning tile (R25).                                                   */
+/* ------------------------------------------------------------------ */
+
+/* R22: per-channel mean at time t, linear between the bracketing bake
+ * times times[0] < ... < times[n-1]; t outside [times[0], times[n-1]]
+ * is an error (returns 1). */
+int oracle_mean_at(const double *times, const double *means, int n, double t, double out[3])
+{
+    if (n < 1 || !(t >= times[0]) || !(t <= times[n - 1])) return 1;
+    if (n == 1) {
+        for (int c = 0; c < 3; ++c) out[c] = means[c];
+        return 0;
+    }
+    int i = 0;
+    while (i < n - 2 && t > times[i + 1]) ++i;      /* times[i] <= t <= times[i+1] */
+    double lam = (t - times[i]) / (times[i + 1] - times[i]);
+    for (int c = 0; c < 3; ++c) out[c] = (1.0 - lam) * means[3 * i + c] + lam * means[3 * (i + 1) + c];
+    return 0;
+}
+
+/* R21/R23: undo the gamma correction and the mean normalisation */
+double oracle_restore(double x, double g, double mu) { return pow(x, g) * mu; }
+
+/* R25: one shading sample at (u, v) in [0,1]^2 of atlas `atlas`.
+ * cache: [slots][P][P][4] u8 (P = C + 2B), pt: [tiles][2] int32 = (slot,
+ * bucket), tile id = (atlas * tiles_y + ty) * tiles_x + tx.  The texel
+ * grid of the atlas has centres at ((i + 0.5)/W, (j + 0.5)/H); the owning
+ * tile is the one whose core contains the sample point; the bilinear taps
+ * (at most one texel outside the core) come from that tile's slot, its
+ * border supplying the outside taps.  Returns 0, or 1 when the tile is
+ * not resident for `bucket` (out untouched). */
+int oracle_sample_lighting(const uint8_t *cache, const int32_t *pt, int C, int B, int tiles_x, int tiles_y,
+                           int atlas, double u, double v, int bucket, double g, const double mu[3], double out[3])
+{
+    const int P = C + 2 * B;
+    const int W = tiles_x * C, H = tiles_y * C;
+    u = fmin(fmax(u, 0.0), 1.0);
+    v = fmin(fmax(v, 0.0), 1.0);
+    int tx = (int)floor(u * tiles_x), ty = (int)floor(v * tiles_y);
+    if (tx > tiles_x - 1) tx = tiles_x - 1;
+    if (ty > tiles_y - 1) ty = tiles_y - 1;
+    const long id = ((long)atlas * tiles_y + ty) * tiles_x + tx;
+    const int slot = pt[2 * id], b = pt[2 * id + 1];
+    if (slot < 0 || b != bucket) return 1;
+    const double lx = u * W - 0.5 - (double)tx * C;   /* in [-0.5, C - 0.5] */
+    const double ly = v * H - 0.5 - (double)ty * C;
+    const double x0 = floor(lx), y0 = floor(ly);
+    const double fx = lx - x0, fy = ly - y0;
+    const uint8_t *s = cache + (size_t)slot * P * P * 4;
+    for (int c = 0; c < 3; ++c) {
+        double q[2][2];
+        for (int dy = 0; dy < 2; ++dy)
+            for (int dx = 0; dx < 2; ++dx) {
+                const int px = (int)x0 + dx + B, py = (int)y0 + dy + B;
+                q[dy][dx] = s[((size_t)py * P + px) * 4 + c] / 255.0;
+            }
+        const double val = (1 - fx) * (1 - fy) * q[0][0] + fx * (1 - fy) * q[0][1] + (1 - fx) * fy * q[1][0] +
+                           fx * fy * q[1][1];
+        out[c] = oracle_restore(val, g, mu[c]);
+    }
+    return 0;
+}
