@@ -197,8 +197,9 @@ NDGI_API size_t ndgi_texel_bytes(ndgi_out_fmt fmt);
 
 /*
  * Synchronises the context's device and returns the number of rejected
- * requests (bad tile id or slot) since load or the last reset; resets the
- * counter when `reset` != 0.
+ * requests (bad tile id or slot) and non-resident shading samples
+ * (ndgi_sample_lighting) since load or the last reset; resets the counter
+ * when `reset` != 0.
  */
 NDGI_API ndgi_status ndgi_device_error(ndgi_ctx* ctx, uint32_t* bad_requests, int reset);
 
@@ -210,6 +211,85 @@ NDGI_API ndgi_status ndgi_free(ndgi_ctx* ctx);
 /* Validates a layout without touching CUDA (same rules as ndgi_load; FAST-mode
  * support reported through *fast_supported if non-NULL). */
 NDGI_API ndgi_status ndgi_validate_layout(const ndgi_layout* layout, int* fast_supported);
+
+/* ------------------------------------------------------------------------
+ * Shading side of the page cache
+ *
+ * P:229 "During shading, we first sample the page table to locate each tile
+ * within the physical texture, then sample the physical texture to obtain the
+ * final lighting. For tiles already resident ... we can reuse the cached
+ * content for a period"; P:521 (page table), P:524 (missing tiles, eviction),
+ * P:526 (border for filtering), P:232 (gamma + per-time channel means,
+ * restored during rendering).  Readings R21-R25 in DESIGN.md.
+ * ------------------------------------------------------------------------ */
+
+/* Page table + strict-LRU residency of `capacity` page-cache slots, host
+ * side.  `num_buckets` time buckets over t in [0,1] (SPEC's default 96, i.e.
+ * 15 minutes of a day): a tile resident for bucket b = floor(t * num_buckets)
+ * (t = 1 -> last bucket) is reused for any t in that bucket and
+ * re-decoded in place otherwise.  Not thread-safe: one host thread per
+ * ndgi_vt.  Errors: ARG (0 tiles/slots/buckets, > 2^20 buckets), NOMEM. */
+typedef struct ndgi_vt ndgi_vt;
+NDGI_API ndgi_status ndgi_vt_create(uint32_t num_tiles, uint32_t capacity, uint32_t num_buckets, ndgi_vt** out);
+NDGI_API ndgi_status ndgi_vt_free(ndgi_vt* vt);
+
+/*
+ * One frame's tile requests ("identifies missing tiles"): ids = HOST
+ * u32[n] (duplicates allowed); for every distinct id that is not resident
+ * for bucket(t) a decode job (job_ids[j], job_slots[j]), j < *n_jobs <= n,
+ * HOST arrays with room for n entries.  Slots: never-used slots first (in
+ * increasing order), then the least recently requested slot not requested in
+ * this frame; the evicted tile becomes absent.  The page table is updated as
+ * if the jobs had run: decode them (ndgi_decode_tiles(ctx, job ids, job
+ * slots, *n_jobs, capacity, *t_decode, cache, ...) with *t_decode = the
+ * bucket centre) and upload the table on the same stream before sampling.
+ * *bucket receives bucket(t) (optional).  Errors: ARG (NULL, id >=
+ * num_tiles: no state change), RANGE (t outside [0,1], or more distinct ids
+ * than slots: no state change).
+ */
+NDGI_API ndgi_status ndgi_vt_request(ndgi_vt* vt, const uint32_t* ids, uint32_t n, float t, uint32_t* job_ids,
+                                     uint32_t* job_slots, uint32_t* n_jobs, float* t_decode, int32_t* bucket);
+/* bucket(t) and its decode time (b + 1/2) / num_buckets, without touching residency */
+NDGI_API ndgi_status ndgi_vt_bucket(const ndgi_vt* vt, float t, int32_t* bucket, float* t_decode);
+/* HOST copy of the page table: int32 [num_tiles][2] = (slot, bucket), slot -1 = absent */
+NDGI_API ndgi_status ndgi_vt_page_table(const ndgi_vt* vt, int32_t* out_host);
+/* the page table -> DEVICE int32 [num_tiles][2], stream-ordered (returns once staged) */
+NDGI_API ndgi_status ndgi_vt_upload(const ndgi_vt* vt, int32_t* page_table_dev, void* stream);
+/* counters: [distinct tile requests, hits, decode jobs, evictions] */
+NDGI_API ndgi_status ndgi_vt_stats(const ndgi_vt* vt, uint64_t out[4]);
+
+/* HDR restore parameters of the lightmap sets: the decoder output is
+ * gamma-corrected and normalised by per-channel means at each bake time. */
+typedef struct ndgi_hdr {
+    float gamma;               /* g > 0: stored value x -> x^g (R23)                    */
+    uint32_t n_frames;         /* bake times                                            */
+    const float* frame_times;  /* HOST [n_frames], strictly increasing                  */
+    const float* means;        /* HOST [atlases][n_frames][3] per-channel means (R22)   */
+} ndgi_hdr;
+
+/*
+ * Shading samples of the page cache: for sample i at
+ * (u, v) = uv[i] in [0,1]^2 (clamped) of atlas atlas[i] (NULL: atlas 0), the
+ * owning tile is the one whose core contains the point on the atlas texel grid
+ * (centres at ((x + 0.5)/W, (y + 0.5)/H), W = tiles_x*C, H = tiles_y*C); its
+ * page-table entry must be (slot < num_slots, bucket); the RGBA8 slot is
+ * filtered bilinearly, the border supplying taps outside the core (R25),
+ * and restored: out = (filtered/255)^g * mu_hat(t, c) (R21), mu_hat linear
+ * between the bracketing bake times (R22).
+ *   page_table: DEVICE int32 [num_tiles][2] (ndgi_vt_upload)
+ *   cache     : DEVICE [num_slots][P][P][4] RGBA8 (ndgi_decode_tiles output)
+ *   uv        : DEVICE float [n][2];  atlas: DEVICE u32 [n] or NULL
+ *   out_rgb   : DEVICE float [n][3], linear HDR
+ * Non-resident samples (absent tile, other bucket, bad atlas/slot) get NaN
+ * and count in ndgi_device_error.  Position math in fp64, filter and restore
+ * in fp32.  Errors (synchronous): ARG (NULL, gamma <= 0, frame times not
+ * increasing, means not finite), RANGE (t outside the bake times),
+ * UNSUPPORTED (border 0 or > 64 atlases), CUDA.  n == 0 is a no-op.
+ */
+NDGI_API ndgi_status ndgi_sample_lighting(ndgi_ctx* ctx, const int32_t* page_table, int32_t bucket,
+                                          const void* cache, uint32_t num_slots, const float* uv,
+                                          const uint32_t* atlas, uint32_t n, float t, const ndgi_hdr* hdr,
+                                          float* out_rgb, void* stream);
 
 /* ---------------- test hooks (not the product path) ---------------- */
 

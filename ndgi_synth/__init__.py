@@ -286,3 +286,35 @@ def vt_batches(num_tiles: int, n: int, frames: int, seed: int = 3000):
         ids = np.argsort(keys, kind="stable")[:n].astype(np.uint32)
         out.append((ids, (0.3 + f / 96.0) % 1.0))
     return out
+
+
+# ------------------------------------------------------------------ shading side (NEXT 1)
+def page_cache_bytes(slots: int, core: int, border: int, seed: int) -> np.ndarray:
+    """Seeded random RGBA8 page cache [slots][P][P][4] (A = 255)."""
+    P = core + 2 * border
+    words = splitmix64(np.arange(slots * P * P, dtype=np.uint64) + np.uint64(seed) * np.uint64(0x9E3779B9))
+    rgba = words.view(np.uint8).reshape(slots * P * P, 8)[:, :4].copy()
+    rgba[:, 3] = 255
+    return rgba.reshape(slots, P, P, 4)
+
+
+def hdr_params(atlases: int, n_frames: int, seed: int, gamma: float = 2.2):
+    """Bake times i/(n_frames-1) (hourly bakes over t in [0,1]) and seeded
+    per-atlas, per-time, per-channel means in [0.2, 8]."""
+    times = np.linspace(0.0, 1.0, n_frames).astype(np.float32)
+    w = splitmix64(np.arange(atlases * n_frames * 3, dtype=np.uint64) + np.uint64(seed))
+    means = (0.2 + 7.8 * _unif(w)).astype(np.float32).reshape(atlases, n_frames, 3)
+    return gamma, times, means
+
+
+def shading_uv(n: int, seed: int, coherent: bool = False, width: int = 1920, height: int = 1080) -> np.ndarray:
+    """Sample positions [n][2] float32: uniform random over [0,1]^2, or a
+    screen-like coherent raster (a width x height grid over a sub-rectangle)."""
+    if not coherent:
+        w = splitmix64(np.arange(2 * n, dtype=np.uint64) + np.uint64(seed))
+        return _unif(w).astype(np.float32).reshape(n, 2)
+    ys, xs = np.mgrid[0:height, 0:width]
+    u = 0.1 + 0.5 * (xs.ravel() + 0.5) / width
+    v = 0.2 + 0.5 * (ys.ravel() + 0.5) / height
+    uv = np.stack([u, v], 1).astype(np.float32)
+    return np.resize(uv, (n, 2))

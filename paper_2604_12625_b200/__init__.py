@@ -42,6 +42,10 @@ class ndgi_layout(C.Structure):
         "gelu", "border_mode")]
 
 
+class ndgi_hdr(C.Structure):
+    _fields_ = [("gamma", C.c_float), ("n_frames", C.c_uint32), ("frame_times", C.c_void_p), ("means", C.c_void_p)]
+
+
 class ndgi_params(C.Structure):
     _fields_ = [("uv", C.c_void_p), ("uvt", C.c_void_p), ("ut", C.c_void_p), ("vt", C.c_void_p),
                 ("mlp", C.c_void_p)]
@@ -67,6 +71,14 @@ _SIGS = {
     "ndgi_debug_mma_latency": (_I, [_U32, C.POINTER(C.c_double)]),
     "ndgi_debug_tmem_f16_probe": (_I, [_P]),
     "ndgi_debug_fused_profile": (_I, [_P, _I]),
+    "ndgi_vt_create": (_I, [_U32, _U32, _U32, C.POINTER(C.c_void_p)]),
+    "ndgi_vt_free": (_I, [_P]),
+    "ndgi_vt_request": (_I, [_P, _P, _U32, _F, _P, _P, C.POINTER(_U32), C.POINTER(_F), C.POINTER(C.c_int32)]),
+    "ndgi_vt_bucket": (_I, [_P, _F, C.POINTER(C.c_int32), C.POINTER(_F)]),
+    "ndgi_vt_page_table": (_I, [_P, _P]),
+    "ndgi_vt_upload": (_I, [_P, _P, _P]),
+    "ndgi_vt_stats": (_I, [_P, _P]),
+    "ndgi_sample_lighting": (_I, [_P, _P, C.c_int32, _P, _U32, _P, _P, _U32, _F, C.POINTER(ndgi_hdr), _P, _P]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -247,3 +259,81 @@ def upload_theta(theta: dict, device: int = 0) -> dict:
             a = a.view(np.int16)
         out[k] = torch.from_numpy(a).to(f"cuda:{device}")
     return out
+
+
+# ---------------------------------------------------------------- shading side (NEXT 1)
+class VT:
+    """ndgi_vt: page table + strict-LRU residency of the page cache (host side)."""
+
+    def __init__(self, num_tiles: int, capacity: int, num_buckets: int = 96):
+        h = C.c_void_p()
+        _check(_lib.ndgi_vt_create(int(num_tiles), int(capacity), int(num_buckets), C.byref(h)), "ndgi_vt_create")
+        self.handle, self.num_tiles, self.capacity = h, int(num_tiles), int(capacity)
+
+    def request(self, ids, t: float):
+        """ids: host sequence of tile ids -> (job_ids, job_slots, t_decode, bucket) as numpy arrays / scalars."""
+        import numpy as np
+        ids = np.ascontiguousarray(np.asarray(ids, np.uint32))
+        n = len(ids)
+        jid = np.zeros(max(n, 1), np.uint32)
+        jsl = np.zeros(max(n, 1), np.uint32)
+        nj, td, b = C.c_uint32(0), C.c_float(0), C.c_int32(0)
+        st = _lib.ndgi_vt_request(self.handle, ids.ctypes.data_as(C.c_void_p), n, float(t),
+                                  jid.ctypes.data_as(C.c_void_p), jsl.ctypes.data_as(C.c_void_p), C.byref(nj),
+                                  C.byref(td), C.byref(b))
+        _check(st, "ndgi_vt_request")
+        return jid[:nj.value].copy(), jsl[:nj.value].copy(), td.value, b.value
+
+    def bucket(self, t: float):
+        b, td = C.c_int32(0), C.c_float(0)
+        _check(_lib.ndgi_vt_bucket(self.handle, float(t), C.byref(b), C.byref(td)), "ndgi_vt_bucket")
+        return b.value, td.value
+
+    def page_table(self):
+        import numpy as np
+        out = np.zeros((self.num_tiles, 2), np.int32)
+        _check(_lib.ndgi_vt_page_table(self.handle, out.ctypes.data_as(C.c_void_p)), "ndgi_vt_page_table")
+        return out
+
+    def upload(self, page_table_dev, stream=None) -> None:
+        _check(_lib.ndgi_vt_upload(self.handle, C.c_void_p(page_table_dev.data_ptr()), _stream_ptr(stream)),
+               "ndgi_vt_upload")
+
+    def stats(self):
+        import numpy as np
+        out = np.zeros(4, np.uint64)
+        _check(_lib.ndgi_vt_stats(self.handle, out.ctypes.data_as(C.c_void_p)), "ndgi_vt_stats")
+        return dict(zip(("requests", "hits", "jobs", "evictions"), (int(x) for x in out)))
+
+    def close(self) -> None:
+        lib = _lib
+        if getattr(self, "handle", None) and lib is not None:
+            lib.ndgi_vt_free(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_hdr(gamma: float, frame_times, means):
+    """-> (ndgi_hdr, keep-alive arrays); means [atlases][n_frames][3]."""
+    import numpy as np
+    tm = np.ascontiguousarray(np.asarray(frame_times, np.float32))
+    mu = np.ascontiguousarray(np.asarray(means, np.float32))
+    h = ndgi_hdr(float(gamma), len(tm), tm.ctypes.data_as(C.c_void_p), mu.ctypes.data_as(C.c_void_p))
+    return h, (tm, mu)
+
+
+def ndgi_sample_lighting(ctx: Context, page_table, bucket: int, cache, num_slots: int, uv, atlas, n: int, t: float,
+                         hdr, out_rgb, stream=None) -> None:
+    """page_table int32 [tiles][2], cache uint8 [slots][P][P][4], uv float32 [n][2], atlas uint32/int32 [n] or None,
+    out_rgb float32 [n][3] -- CUDA tensors; hdr from make_hdr (or (ndgi_hdr, keep))."""
+    h = hdr[0] if isinstance(hdr, tuple) else hdr
+    st = _lib.ndgi_sample_lighting(ctx.handle, C.c_void_p(page_table.data_ptr()), int(bucket),
+                                   C.c_void_p(cache.data_ptr()), int(num_slots), C.c_void_p(uv.data_ptr()),
+                                   C.c_void_p(atlas.data_ptr()) if atlas is not None else None, int(n), float(t),
+                                   C.byref(h), C.c_void_p(out_rgb.data_ptr()), _stream_ptr(stream))
+    _check(st, "ndgi_sample_lighting")

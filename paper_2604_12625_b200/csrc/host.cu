@@ -20,6 +20,7 @@ cudaError_t launch_fused_ws(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_hmma(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_pipe(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
+cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 size_t wpack_tile_bytes(int H);
 cudaError_t prep_weights(const uint16_t* mlp, size_t tile_elems, int H, int fmt_uv, uint8_t* out, int num_tiles,
                          cudaStream_t s);
@@ -248,6 +249,14 @@ ndgi_status decode_full_async(ndgi_ctx* ctx, const float* ts, uint32_t nt, void*
 
 }  // namespace
 
+namespace ndgi {
+// for the other translation units of the C ABI (vt_cache.cu)
+ndgi_status set_error(ndgi_status s, const char* msg) {
+    g_last_error = msg;
+    return s;
+}
+}  // namespace ndgi
+
 extern "C" {
 
 const char* ndgi_status_string(ndgi_status s) {
@@ -430,6 +439,62 @@ ndgi_status ndgi_device_error(ndgi_ctx* ctx, uint32_t* bad_requests, int reset) 
     e = cudaMemcpy(bad_requests, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(error counter)");
     if (reset) cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_sample_lighting(ndgi_ctx* ctx, const int32_t* page_table, int32_t bucket, const void* cache,
+                                 uint32_t num_slots, const float* uv, const uint32_t* atlas, uint32_t n, float t,
+                                 const ndgi_hdr* hdr, float* out_rgb, void* stream) {
+    if (!ctx || !page_table || !cache || !uv || !out_rgb || !hdr || !hdr->frame_times || !hdr->means)
+        return fail(NDGI_ERR_ARG, "NULL argument");
+    if (num_slots == 0) return fail(NDGI_ERR_ARG, "num_slots == 0");
+    if (!std::isfinite(hdr->gamma) || hdr->gamma <= 0.0f) return fail(NDGI_ERR_ARG, "gamma must be finite and > 0");
+    if (hdr->n_frames == 0) return fail(NDGI_ERR_ARG, "n_frames == 0");
+    const ndgi_layout& L = ctx->L;
+    if (L.atlases > (uint32_t)ndgi::kMaxSampleAtlases) return fail(NDGI_ERR_UNSUPPORTED, "more than 64 atlases");
+    if (L.border < 1) return fail(NDGI_ERR_UNSUPPORTED, "sampling needs a tile border >= 1 (P:526)");
+    const float* tm = hdr->frame_times;
+    for (uint32_t i = 0; i < hdr->n_frames; ++i) {
+        if (!std::isfinite(tm[i]) || (i && !(tm[i] > tm[i - 1])))
+            return fail(NDGI_ERR_ARG, "frame_times must be finite and increasing");
+    }
+    if (!std::isfinite(t) || t < tm[0] || t > tm[hdr->n_frames - 1])
+        return fail(NDGI_ERR_RANGE, "t outside [frame_times[0], frame_times[n_frames-1]] (R22)");
+    if (n == 0) return NDGI_OK;
+    // R22: per-atlas, per-channel mean at t, linear between the bracketing bake times (fp64)
+    uint32_t i0 = 0;
+    while (hdr->n_frames > 1 && i0 < hdr->n_frames - 2 && t > tm[i0 + 1]) ++i0;
+    const double lam = hdr->n_frames > 1 ? ((double)t - tm[i0]) / ((double)tm[i0 + 1] - tm[i0]) : 0.0;
+    const uint32_t i1 = hdr->n_frames > 1 ? i0 + 1 : i0;
+    std::vector<float> mu((size_t)L.atlases * 3);
+    for (uint32_t a = 0; a < L.atlases; ++a)
+        for (int c = 0; c < 3; ++c) {
+            const double m0 = hdr->means[((size_t)a * hdr->n_frames + i0) * 3 + c];
+            const double m1 = hdr->means[((size_t)a * hdr->n_frames + i1) * 3 + c];
+            if (!std::isfinite(m0) || !std::isfinite(m1)) return fail(NDGI_ERR_ARG, "means must be finite");
+            mu[(size_t)a * 3 + c] = (float)((1.0 - lam) * m0 + lam * m1);
+        }
+    DeviceGuard g(ctx->device);
+    ndgi::SampleArgs A;
+    A.pt = page_table;
+    A.cache = static_cast<const uint8_t*>(cache);
+    A.uv = uv;
+    A.atlas = atlas;
+    A.out = out_rgb;
+    A.err = ctx->d_err;
+    A.n = n;
+    A.num_slots = num_slots;
+    A.bucket = bucket;
+    A.C = (int)L.core;
+    A.B = (int)L.border;
+    A.tiles_x = (int)L.tiles_x;
+    A.tiles_y = (int)L.tiles_y;
+    A.atlases = (int)L.atlases;
+    A.num_sms = ctx->num_sms;
+    A.g = hdr->gamma;
+    A.mu = mu.data();
+    const cudaError_t e = ndgi::launch_sample(A, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "sample launch");
     return NDGI_OK;
 }
 

@@ -57,6 +57,22 @@ struct KParams {
     uint32_t units;             // nt * n_req * strips_per_tile
 };
 
+// shading-side sampling (sample_kernel.cu)
+constexpr int kMaxSampleAtlases = 64;
+struct SampleArgs {
+    const int32_t* pt;
+    const uint8_t* cache;
+    const float* uv;
+    const uint32_t* atlas;
+    float* out;
+    uint32_t* err;
+    uint32_t n, num_slots;
+    int32_t bucket;
+    int C, B, tiles_x, tiles_y, atlases, num_sms;
+    float g;
+    const float* mu;   // host [atlases][3], mu_hat at the call's t
+};
+
 __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
 __device__ __forceinline__ float half_bits_to_float(uint16_t h) {

@@ -1,0 +1,154 @@
+"""GPU parity of the shading side: ndgi_sample_lighting
+through the C-ABI against the oracle's sampler on seeded synthetic page caches
+(no input from the CUDA decode), and the whole VT frame loop (ndgi_vt request
+-> ndgi_decode_tiles -> upload -> sample) against the oracle's own decode +
+sample.  Tolerances: the kernel takes positions in fp64 and filters/restores in
+fp32, so rel 3e-6 (+ 1e-6 * max mean) vs the fp64 oracle; end to end the FAST
+decode may move a stored byte by one step, so the comparison there is in the
+stored (gamma/mean-normalised) space, within 1.01/255."""
+import numpy as np
+import pytest
+
+import ndgi_synth as S
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2604_12625_b200 as ndgi  # noqa: E402
+
+
+def _ctx(lay, seed):
+    th = ndgi.upload_theta(S.make_theta(lay, seed))
+    return ndgi.ndgi_load(lay, th, 0), th
+
+
+def _sample(ctx, pt, bucket, cache, uv, atlas, t, hdr):
+    n = len(uv)
+    out = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    ndgi.ndgi_sample_lighting(ctx, torch.from_numpy(pt).cuda(), bucket, torch.from_numpy(cache).cuda(),
+                              cache.shape[0], torch.from_numpy(uv).cuda(),
+                              None if atlas is None else torch.from_numpy(atlas.astype(np.int32)).cuda(), n, t,
+                              hdr, out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _mu_hat(times, means, t):
+    return np.stack([oracle.mean_at(times.astype(np.float64), means[a].astype(np.float64), np.float32(t))
+                     for a in range(means.shape[0])])
+
+
+def _edge_points(lay):
+    W, H = lay["tiles_x"] * lay["core"], lay["tiles_y"] * lay["core"]
+    xs = np.concatenate([(np.arange(W) + 0.5) / W, np.arange(lay["tiles_x"] + 1) / lay["tiles_x"], [-0.2, 1.3]])
+    ys = np.concatenate([(np.arange(0, H, 7) + 0.5) / H, np.arange(lay["tiles_y"] + 1) / lay["tiles_y"]])
+    X, Y = np.meshgrid(xs, ys)
+    return np.stack([X.ravel(), Y.ravel()], 1).astype(np.float32)
+
+
+def test_sample_parity_on_synthetic_cache():
+    lay = S.layout(2, 3, 2, "L")                  # 2 atlases x (3 x 2) tiles, C = 128, B = 4
+    ctx, _ = _ctx(lay, 77)
+    T = lay["num_tiles"]
+    cache = S.page_cache_bytes(T + 2, lay["core"], lay["border"], 5)
+    pt = np.stack([(np.arange(T) * 5 + 1) % (T + 2), np.full(T, 9)], 1).astype(np.int32)
+    pt[4] = (-1, -1)                              # absent
+    pt[7, 1] = 8                                  # resident for another bucket
+    g, times, means = S.hdr_params(2, 25, 6)
+    hdr = ndgi.make_hdr(g, times, means)
+    uv = np.concatenate([S.shading_uv(20000, 3), _edge_points(lay)])
+    atlas = (np.arange(len(uv)) % 2).astype(np.uint32)
+    t = 0.437
+    got = _sample(ctx, pt, 9, cache, uv, atlas, t, hdr)
+    mu = _mu_hat(times, means, t)
+    exp, ok = oracle.sample_lighting(cache, pt, lay["core"], lay["border"], lay["tiles_x"], lay["tiles_y"], atlas,
+                                     uv.astype(np.float64), 9, g, mu)
+    assert (~ok).sum() > 100 and ok.sum() > 10000
+    np.testing.assert_array_equal(np.isnan(got).any(1), ~ok)
+    np.testing.assert_allclose(got[ok], exp[ok], rtol=3e-6, atol=1e-6 * float(means.max()))
+
+
+def test_non_resident_samples_are_counted():
+    lay, seed = S.config("c1")
+    ctx, _ = _ctx(lay, seed)
+    ndgi.ndgi_device_error(ctx, reset=True)
+    cache = S.page_cache_bytes(4, 128, 4, 1)
+    pt = np.stack([np.arange(4), np.zeros(4, int)], 1).astype(np.int32)
+    pt[1] = (-1, -1)
+    uv = S.shading_uv(5000, 9)
+    hdr = ndgi.make_hdr(*S.hdr_params(1, 2, 1))
+    got = _sample(ctx, pt, 0, cache, uv, None, 0.5, hdr)
+    owner = np.minimum((uv[:, 1] * 2).astype(int), 1) * 2 + np.minimum((uv[:, 0] * 2).astype(int), 1)
+    np.testing.assert_array_equal(np.isnan(got).any(1), owner == 1)
+    assert ndgi.ndgi_device_error(ctx, reset=True) == int((owner == 1).sum())
+
+
+def test_sample_argument_errors():
+    lay, seed = S.config("c1")
+    ctx, _ = _ctx(lay, seed)
+    cache = torch.zeros((4, 136, 136, 4), dtype=torch.uint8, device="cuda")
+    pt = torch.zeros((4, 2), dtype=torch.int32, device="cuda")
+    uv = torch.zeros((8, 2), dtype=torch.float32, device="cuda")
+    out = torch.zeros((8, 3), dtype=torch.float32, device="cuda")
+    g, times, means = S.hdr_params(1, 3, 2)
+    ok_hdr = ndgi.make_hdr(g, times, means)
+    with pytest.raises(ndgi.NdgiError) as e:                  # t outside the bake times
+        ndgi.ndgi_sample_lighting(ctx, pt, 0, cache, 4, uv, None, 8, 1.5, ok_hdr, out)
+    assert e.value.status == ndgi.ERR_RANGE
+    with pytest.raises(ndgi.NdgiError) as e:                  # gamma <= 0
+        ndgi.ndgi_sample_lighting(ctx, pt, 0, cache, 4, uv, None, 8, 0.5, ndgi.make_hdr(0.0, times, means), out)
+    assert e.value.status == ndgi.ERR_ARG
+    with pytest.raises(ndgi.NdgiError) as e:                  # bake times not increasing
+        ndgi.ndgi_sample_lighting(ctx, pt, 0, cache, 4, uv, None, 8, 0.5,
+                                  ndgi.make_hdr(g, times[::-1].copy(), means), out)
+    assert e.value.status == ndgi.ERR_ARG
+    ndgi.ndgi_sample_lighting(ctx, pt, 0, cache, 4, uv, None, 0, 0.5, ok_hdr, out)   # n = 0: no-op
+
+
+def test_vt_frame_loop_end_to_end():
+    # request -> decode the jobs into their slots at the bucket centre -> upload
+    # the page table -> shade; against the oracle's own decode of the same jobs
+    lay = S.layout(1, 4, 2, "M", uvt_depth=4, line_t=4)
+    seed = 31
+    ctx, th = _ctx(lay, seed)
+    M = oracle.Model(lay, S.make_theta(lay, seed))
+    T, cap = lay["num_tiles"], 5
+    vt = ndgi.VT(T, cap, 24)
+    cache = torch.zeros((cap, 136, 136, 4), dtype=torch.uint8, device="cuda")
+    pt_dev = torch.empty((T, 2), dtype=torch.int32, device="cuda")
+    ref_cache = np.zeros((cap, 136, 136, 4), np.uint8)
+    g, times, means = S.hdr_params(1, 25, 12)
+    hdr = ndgi.make_hdr(g, times, means)
+    rng = np.random.default_rng(0)
+    t = 0.30
+    for frame in range(6):
+        t = min(1.0, t + 0.02)
+        want = rng.choice(T, 4, replace=False)
+        jid, jsl, td, b = vt.request(want, t)
+        if len(jid):
+            ndgi.ndgi_decode_tiles(ctx, torch.from_numpy(jid.astype(np.int32)).cuda(),
+                                   torch.from_numpy(jsl.astype(np.int32)).cuda(), len(jid), cap, td, cache, "rgba8")
+            y = M.decode_tiles(jid.tolist(), td, 8)                   # oracle's own page-cache contents
+            for k, s in enumerate(jsl):
+                ref_cache[s] = oracle.quantize_rgba8(y[k].reshape(-1, 3)).reshape(136, 136, 4)
+        vt.upload(pt_dev)
+        # samples inside the requested tiles
+        tx, ty = want % 4, want // 4
+        u = (tx[:, None] + rng.uniform(0, 1, (4, 500))) / 4
+        v = (ty[:, None] + rng.uniform(0, 1, (4, 500))) / 2
+        uv = np.stack([u.ravel(), v.ravel()], 1).astype(np.float32)
+        n = len(uv)
+        out = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+        ndgi.ndgi_sample_lighting(ctx, pt_dev, b, cache, cap, torch.from_numpy(uv).cuda(), None, n, t, hdr, out)
+        got = out.cpu().numpy()
+        mu = _mu_hat(times, means, t)
+        exp, ok = oracle.sample_lighting(ref_cache, vt.page_table(), 128, 4, 4, 2, np.zeros(n, int),
+                                         uv.astype(np.float64), b, g, mu)
+        assert ok.all() and not np.isnan(got).any()
+        # compare in the stored space (undo the restore with the same mu)
+        gs = (got / mu[0]) ** (1 / g)
+        es = (exp / mu[0]) ** (1 / g)
+        assert np.abs(gs - es).max() <= 1.01 / 255
+    s = vt.stats()
+    assert s["jobs"] + s["hits"] == s["requests"]
