@@ -293,12 +293,18 @@ def run_gpu(args, rank, world, dist):
             vt = vt_latency(ndgi, torch, args)
         except Exception as exc:  # pragma: no cover
             vt = {"error": repr(exc)}
+    shading = None
+    if not args.no_shading and world == 1:
+        try:
+            shading = shading_leg(ndgi, torch, args)
+        except Exception as exc:  # pragma: no cover
+            shading = {"error": repr(exc)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
-        "clocks": clk.summary(), "vt_batch_us": vt,
+        "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading,
         "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
     }
     print(json.dumps(line), flush=True)
@@ -335,6 +341,85 @@ def vt_latency(ndgi, torch, args):
     return res
 
 
+def shading_leg(ndgi, torch, args):
+    """SURVEY §8(f) NEXT 1, measured: one 1920x1080 frame of coherent shading
+    samples over a 16 x 9-tile window of config 3's scene (~1 texel per sample).
+    (a) ndgi_sample_lighting alone, inputs resident: Gsample/s and the HBM
+    fraction of its algorithmic bytes (8 B uv + 12 B out + 4 B of page cache
+    per sample); (b) the VT frame loop -- ndgi_vt_request + ndgi_decode_tiles of
+    the jobs + ndgi_vt_upload + sample -- for a frame whose 144 tiles all miss
+    (new time bucket) and for a frame that hits."""
+    lay, seed = S.config("c3")
+    th = ndgi.upload_theta(S.make_theta(lay, seed))
+    ctx = ndgi.ndgi_load(lay, th, torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    tx0, ty0, wx, wy = 20, 30, 16, 9
+    ids = np.array([(ty0 + j) * lay["tiles_x"] + tx0 + i for j in range(wy) for i in range(wx)], np.uint32)
+    cap = 256
+    vt = ndgi.VT(lay["num_tiles"], cap, 96)
+    cache = torch.zeros((cap, 136, 136, 4), dtype=torch.uint8, device="cuda")
+    pt = torch.empty((lay["num_tiles"], 2), dtype=torch.int32, device="cuda")
+    g, times, means = S.hdr_params(lay["atlases"], 25, seed)
+    hdr = ndgi.make_hdr(g, times, means)
+    Wt, Ht = lay["tiles_x"], lay["tiles_y"]
+    ys, xs = np.mgrid[0:1080, 0:1920]
+    u = (tx0 + wx * (xs.ravel() + 0.5) / 1920) / Wt
+    v = (ty0 + wy * (ys.ravel() + 0.5) / 1080) / Ht
+    uv = torch.from_numpy(np.stack([u, v], 1).astype(np.float32)).cuda()
+    n = uv.shape[0]
+    out = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+
+    def frame(t):
+        jid, jsl, td, b = vt.request(ids, t)
+        if len(jid):
+            ndgi.ndgi_decode_tiles(ctx, torch.from_numpy(jid.astype(np.int32)).to("cuda", non_blocking=True),
+                                   torch.from_numpy(jsl.astype(np.int32)).to("cuda", non_blocking=True), len(jid),
+                                   cap, td, cache, "rgba8", "fast", stream)
+        vt.upload(pt, stream)
+        ndgi.ndgi_sample_lighting(ctx, pt, b, cache, cap, uv, None, n, t, hdr, out, stream)
+        return len(jid), b
+
+    def timed(fn, reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e-3
+
+    frame(0.40)
+    b = vt.bucket(0.40)[0]
+    for _ in range(3):
+        ndgi.ndgi_sample_lighting(ctx, pt, b, cache, cap, uv, None, n, 0.40, hdr, out, stream)
+    ks = timed(lambda: ndgi.ndgi_sample_lighting(ctx, pt, b, cache, cap, uv, None, n, 0.40, hdr, out, stream), 50)
+    assert ndgi.ndgi_device_error(ctx, reset=True) == 0
+    peaks = _peaks()
+    alg = n * (8 + 12 + 4)
+    hit_s, miss_s = [], []
+    for f in range(12):
+        t = 0.40 + 0.5 * f / 96                      # every other frame enters a new bucket
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        jobs, _ = frame(t)
+        e1.record(stream)
+        e1.synchronize()
+        (miss_s if jobs else hit_s).append(e0.elapsed_time(e1) * 1e3)
+    res = {
+        "workload": "1920x1080 coherent samples over a 16x9-tile window of c3 (144 tiles, ~1 texel/sample), "
+                    "cache 256 slots, 96 time buckets",
+        "samples": n, "sample_kernel_us": ks * 1e6, "gsample_s": n / ks / 1e9,
+        "roofline": {"bound": "hbm", "achieved": alg / ks / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": alg / ks / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes_per_sample": 24},
+        "frame_us_all_hit_p50": statistics.median(hit_s) if hit_s else None,
+        "frame_us_144_miss_p50": statistics.median(miss_s) if miss_s else None,
+        "vt_stats": vt.stats(),
+    }
+    vt.close()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -343,6 +428,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     ap.add_argument("--no-vt", action="store_true", help="skip the VT batch-latency leg")
+    ap.add_argument("--no-shading", action="store_true", help="skip the shading-side (NEXT 1) leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

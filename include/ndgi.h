@@ -253,8 +253,10 @@ NDGI_API ndgi_status ndgi_vt_request(ndgi_vt* vt, const uint32_t* ids, uint32_t 
 NDGI_API ndgi_status ndgi_vt_bucket(const ndgi_vt* vt, float t, int32_t* bucket, float* t_decode);
 /* HOST copy of the page table: int32 [num_tiles][2] = (slot, bucket), slot -1 = absent */
 NDGI_API ndgi_status ndgi_vt_page_table(const ndgi_vt* vt, int32_t* out_host);
-/* the page table -> DEVICE int32 [num_tiles][2], stream-ordered (returns once staged) */
-NDGI_API ndgi_status ndgi_vt_upload(const ndgi_vt* vt, int32_t* page_table_dev, void* stream);
+/* the page table -> DEVICE int32 [num_tiles][2], stream-ordered (returns once
+ * staged); skipped when the table is unchanged since the last upload to the
+ * same buffer (the caller must not write that buffer in between) */
+NDGI_API ndgi_status ndgi_vt_upload(ndgi_vt* vt, int32_t* page_table_dev, void* stream);
 /* counters: [distinct tile requests, hits, decode jobs, evictions] */
 NDGI_API ndgi_status ndgi_vt_stats(const ndgi_vt* vt, uint64_t out[4]);
 

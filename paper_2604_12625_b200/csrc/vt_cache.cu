@@ -36,6 +36,9 @@ struct ndgi_vt {
     std::vector<uint64_t> seen;       // per tile: id of the last request that touched it
     uint64_t req_id = 0;
     uint64_t stats[4] = {0, 0, 0, 0}; // tile requests, hits, decode jobs, evictions
+    uint64_t version = 1;             // bumped by every page-table change
+    const void* uploaded_ptr = nullptr;
+    uint64_t uploaded_version = 0;    // what uploaded_ptr holds
     std::string err;
 };
 
@@ -158,6 +161,7 @@ ndgi_status ndgi_vt_request(ndgi_vt* v, const uint32_t* ids, uint32_t n, float t
         ++nj;
         ++v->stats[2];
     }
+    if (nj) ++v->version;   // jobs (and any evictions, which come with a job) changed the table
     *n_jobs = nj;
     if (t_decode) *t_decode = (float)td;
     if (bucket) *bucket = b;
@@ -179,13 +183,19 @@ ndgi_status ndgi_vt_page_table(const ndgi_vt* v, int32_t* out_host) {
     return NDGI_OK;
 }
 
-ndgi_status ndgi_vt_upload(const ndgi_vt* v, int32_t* page_table_dev, void* stream) {
-    if (!v || !page_table_dev) return NDGI_ERR_ARG;
+ndgi_status ndgi_vt_upload(ndgi_vt* v, int32_t* page_table_dev, void* stream) {
+    if (!v || !page_table_dev) return ndgi::set_error(NDGI_ERR_ARG, "NULL argument");
+    // unchanged since the last upload to this buffer: nothing to copy (an
+    // all-hit frame costs no transfer)
+    if (v->uploaded_ptr == page_table_dev && v->uploaded_version == v->version) return NDGI_OK;
     // pageable source: the call returns once the table is staged, so the next
     // request may modify it while the copy is in flight
     const cudaError_t e = cudaMemcpyAsync(page_table_dev, v->pt.data(), v->pt.size() * sizeof(int32_t),
                                           cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream));
-    return e == cudaSuccess ? NDGI_OK : ndgi::set_error(NDGI_ERR_CUDA, cudaGetErrorString(e));
+    if (e != cudaSuccess) return ndgi::set_error(NDGI_ERR_CUDA, cudaGetErrorString(e));
+    v->uploaded_ptr = page_table_dev;
+    v->uploaded_version = v->version;
+    return NDGI_OK;
 }
 
 ndgi_status ndgi_vt_stats(const ndgi_vt* v, uint64_t out[4]) {

@@ -2,8 +2,10 @@
 through the C-ABI against the oracle's sampler on seeded synthetic page caches
 (no input from the CUDA decode), and the whole VT frame loop (ndgi_vt request
 -> ndgi_decode_tiles -> upload -> sample) against the oracle's own decode +
-sample.  Tolerances: the kernel takes positions in fp64 and filters/restores in
-fp32, so rel 3e-6 (+ 1e-6 * max mean) vs the fp64 oracle; end to end the FAST
+sample.  Tolerances: the kernel takes positions in fp64, filters in fp32 and
+restores x^g as 2^(g log2 x) on the MUFU (lg2/ex2.approx: relative error
+<= ~3e-6 for x >= 1/255, g = 2.2), so rel 1e-5 (+ 1e-6 * max mean) vs the
+fp64 oracle; end to end the FAST
 decode may move a stored byte by one step, so the comparison there is in the
 stored (gamma/mean-normalised) space, within 1.01/255."""
 import numpy as np
@@ -66,7 +68,7 @@ def test_sample_parity_on_synthetic_cache():
                                      uv.astype(np.float64), 9, g, mu)
     assert (~ok).sum() > 100 and ok.sum() > 10000
     np.testing.assert_array_equal(np.isnan(got).any(1), ~ok)
-    np.testing.assert_allclose(got[ok], exp[ok], rtol=3e-6, atol=1e-6 * float(means.max()))
+    np.testing.assert_allclose(got[ok], exp[ok], rtol=1e-5, atol=1e-6 * float(means.max()))
 
 
 def test_non_resident_samples_are_counted():
