@@ -60,14 +60,20 @@ def _traffic():
         return None
 
 
-def _workload_config(world: int, tiles_per_rank: int) -> dict:
+def _workload_config(world: int, tiles_per_rank: int, workload: str = "c2") -> dict:
+    if workload == "c4":
+        desc = ("c4: FarmLand-scale scene, 4 x 8192^2 atlases = 16384 NDGI-M tiles of 128^2 (BC7 F_uv/F_uvt, u8 "
+                "lines, f16 MLP h=16) sharded k % N over the GPUs (strong scaling), decoded at 24 times t=i/24 per "
+                "step (decode_full into each rank's compact atlas, RGBA8)")
+    else:
+        desc = ("c2: 4096^2 lightmap atlas (32x32 NDGI-M tiles of 128^2, BC7 F_uv/F_uvt, u8 lines, "
+                "f16 MLP h=16) decoded at 24 times t=i/24 per step (decode_full, RGBA8)")
     return {
-        "workload": "c2: 4096^2 lightmap atlas (32x32 NDGI-M tiles of 128^2, BC7 F_uv/F_uvt, u8 lines, "
-                    "f16 MLP h=16) decoded at 24 times t=i/24 per step (decode_full, RGBA8)",
+        "workload": desc,
         "tiles_per_gpu": tiles_per_rank, "times_per_step": N_T, "core": 128, "profile": "M",
         "written_texels_per_step": tiles_per_rank * 128 * 128 * N_T * world,
         "scene_tiles": tiles_per_rank * world, "parallelism": f"tile-sharded x{world} (k % N)",
-        "l2": "flushed between timed steps (256 MiB write); Theta 36.9 MB/GPU",
+        "l2": f"flushed between timed steps (256 MiB write); Theta {tiles_per_rank * 36006 / 1e6:.1f} MB/GPU",
     }
 
 
@@ -187,10 +193,19 @@ def run_gpu(args, rank, world, dist):
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
-    lay0, seed = S.config("c2")
     from paper_2604_12625_b200 import parallel as par
-    tiles_per_rank = lay0["num_tiles"]
-    global_ids = par.shard_tiles(tiles_per_rank * world, world, rank)   # tile k on rank k % N
+    if args.workload == "c4":
+        # strong scaling of config 4: the 16384-tile scene sharded k % N; each
+        # rank decodes its shard into a compact 64-tile-wide atlas
+        _, seed = S.config("c4")
+        scene = 16384
+        tiles_per_rank = scene // world
+        global_ids = par.shard_tiles(scene, world, rank)
+        lay0 = S.layout(1, 64, tiles_per_rank // 64, "M")
+    else:
+        lay0, seed = S.config("c2")
+        tiles_per_rank = lay0["num_tiles"]
+        global_ids = par.shard_tiles(tiles_per_rank * world, world, rank)   # tile k on rank k % N
     th_np = S.make_theta(lay0, seed, tiles=global_ids)
     lay = dict(lay0)
     theta = ndgi.upload_theta(th_np, dev)
@@ -232,6 +247,8 @@ def run_gpu(args, rank, world, dist):
     # ---------------- end-to-end through the host-buffer API (Theta H2D + decode + D2H)
     e2e = None
     try:
+        if args.workload == "c4":
+            raise RuntimeError("skipped for c4: 24 GiB of pinned host output per step")
         host_theta = {k: v.cpu().pin_memory() for k, v in theta.items()}
         host_out = torch.empty((N_T, per_t * 4), dtype=torch.uint8).pin_memory()
         h2d = sum(v.numel() * v.element_size() for v in host_theta.values()) + 4 * N_T
@@ -302,7 +319,7 @@ def run_gpu(args, rank, world, dist):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank),
+        "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank, args.workload),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading,
         "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
@@ -429,6 +446,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     ap.add_argument("--no-vt", action="store_true", help="skip the VT batch-latency leg")
     ap.add_argument("--no-shading", action="store_true", help="skip the shading-side (NEXT 1) leg")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+                    help="c2: 1,024 tiles per GPU (weak scaling, default); c4: the 16,384-tile scene sharded (strong)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
