@@ -276,6 +276,31 @@ def run_gpu(args, rank, world, dist):
     except Exception as exc:  # pragma: no cover - reported, not hidden
         e2e = {"value": None, "unit": UNIT, "error": repr(exc)}
 
+    # ---------------- F_uv through the texture unit's BC7 decoder
+    texunit = None
+    if world == 1 and not args.no_texunit:
+        try:
+            def tstep():
+                ndgi.ndgi_decode_full_batch(ctx, TS, out, "rgba8", "fast_texunit", stream)
+            for _ in range(3):
+                flush.zero_()
+                tstep()
+            tms = []
+            for _ in range(max(3, min(args.steps, 10))):
+                flush.zero_()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                tstep()
+                b_.record(stream)
+                b_.synchronize()
+                tms.append(a_.elapsed_time(b_))
+            t_ms = statistics.median(tms)
+            texunit = {"mode": "NDGI_MODE_FAST_TEXUNIT", "value": texels_per_step / (t_ms * 1e-3) / 1e9, "unit": UNIT,
+                       "ms_per_step": t_ms, "vs_software_bc7": ms_per_step / t_ms,
+                       "note": "same workload and output (bit-identical, tested); F_uv decoded by the texture unit"}
+        except Exception as exc:  # pragma: no cover
+            texunit = {"error": repr(exc)}
+
     if rank != 0:
         return
     # ---------------- roofline of the fused kernel (rank 0)
@@ -321,7 +346,7 @@ def run_gpu(args, rank, world, dist):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank, args.workload),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
-        "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading,
+        "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading, "texunit": texunit,
         "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
     }
     print(json.dumps(line), flush=True)
@@ -446,6 +471,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     ap.add_argument("--no-vt", action="store_true", help="skip the VT batch-latency leg")
     ap.add_argument("--no-shading", action="store_true", help="skip the shading-side (NEXT 1) leg")
+    ap.add_argument("--no-texunit", action="store_true", help="skip the texture-unit F_uv comparator (NEXT 2)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
                     help="c2: 1,024 tiles per GPU (weak scaling, default); c4: the 16,384-tile scene sharded (strong)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

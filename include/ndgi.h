@@ -84,7 +84,15 @@ typedef enum {
     NDGI_MODE_FAST = 0,
     /* scalar fp32 reference kernel, accurate erff/tanhf GELU per layout.gelu;
      * parity bar: max-abs <= 1e-5.                                            */
-    NDGI_MODE_REF_FP32 = 1
+    NDGI_MODE_REF_FP32 = 1,
+    /* NDGI_MODE_FAST with F_uv fetched through the B200 texture unit's BC7
+     * decoder -- the paper's runtime mechanism -- instead of the
+     * kernel's software decoder (an in-box comparator).
+     * Needs a FAST layout with fmt_uv == BC7 and <= 64 atlases (UNSUPPORTED
+     * otherwise).  The first call builds one BC7 texture per atlas (a second,
+     * context-owned copy of F_uv: 16 KB per C = 128 tile).  The hardware
+     * decode is bit-exact, so the output equals NDGI_MODE_FAST's bit for bit. */
+    NDGI_MODE_FAST_TEXUNIT = 2
 } ndgi_mode;
 
 /*

@@ -31,7 +31,7 @@ FMT = {"bc7": 0, "u8": 1, "f16": 2}
 OUT = {"rgba8": 0, "rgba16f": 1, "rgba32f": 2}
 GELU = {"erf": 0, "tanh": 1}
 BORDER = {"mirror": 0, "eval_clamp": 1}
-MODE = {"fast": 0, "ref_fp32": 1}
+MODE = {"fast": 0, "ref_fp32": 1, "fast_texunit": 2}
 TEXEL_BYTES = {"rgba8": 4, "rgba16f": 8, "rgba32f": 16}
 
 

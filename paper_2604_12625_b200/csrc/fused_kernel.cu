@@ -175,6 +175,33 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         // decoded F_uv chunk, row-major [chunk_rows][C] RGBA8 (each warp decodes
         // the blocks of its own 32 columns)
         uint32_t* sUv = reinterpret_cast<uint32_t*>(smem + L.uvc);
+        // FMT_BC7_TEX: this tile's F_uv in its atlas's BC7 texture (texel centres)
+        cudaTextureObject_t uvtex = 0;
+        float tex_x0 = 0.f, tex_y0 = 0.f;
+        if constexpr (FMT_UV == FMT_BC7_TEX) {
+            const int ttx = k % p.tiles_x, tty = (k / p.tiles_x) % p.tiles_y, ta = k / (p.tiles_x * p.tiles_y);
+            uvtex = p.uvtex[ta];
+            tex_x0 = (float)(ttx * C) + 0.5f + (float)tid;
+            tex_y0 = (float)(tty * C) + 0.5f;
+        }
+        // F_uv texel (row, blk*128 + tid) as two f16x2 holding the integers q (R8)
+        auto uv_texel = [&](int row, int jr, int blk, uint32_t& lo, uint32_t& hi) {
+            if constexpr (FMT_UV == FMT_BC7) {
+                u8x4_to_h2(sUv[jr * C + blk * kThreads + tid], lo, hi);
+            } else if constexpr (FMT_UV == FMT_BC7_TEX) {
+                // hardware BC7 decode returns q/255 (UNORM); x255 lands within 2^-16
+                // of q, which the f16 rounding makes exact
+                const float4 v = tex2D<float4>(uvtex, tex_x0 + (float)(blk * kThreads), tex_y0 + (float)row);
+                lo = pack_f16x2(v.x * 255.f, v.y * 255.f);
+                hi = pack_f16x2(v.z * 255.f, v.w * 255.f);
+            } else if constexpr (FMT_UV == FMT_U8) {
+                u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + blk * kThreads + tid), lo, hi);
+            } else {
+                const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)row * C + blk * kThreads + tid);
+                lo = hv.x;
+                hi = hv.y;
+            }
+        };
         // MMA descriptors of this unit's weights
         // layers 1, 2: f16 accumulators for h = 16 (the GELU input is f16 anyway);
         // layer 3 (the output y): fp32
@@ -271,15 +298,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             uint32_t a1[8];
             a1[0] = hlerp2(hlerp2(t00.x, t10.x, cc.z), hlerp2(t01.x, t11.x, cc.z), rt.z);
             a1[1] = hlerp2(hlerp2(t00.y, t10.y, cc.z), hlerp2(t01.y, t11.y, cc.z), rt.z);
-            if (FMT_UV == FMT_BC7) {
-                u8x4_to_h2(sUv[jr * C + blk * kThreads + tid], a1[2], a1[3]);
-            } else if (FMT_UV == FMT_U8) {
-                u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + blk * kThreads + tid), a1[2], a1[3]);
-            } else {
-                const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)row * C + blk * kThreads + tid);
-                a1[2] = hv.x;
-                a1[3] = hv.y;
-            }
+            uv_texel(row, jr, blk, a1[2], a1[3]);
             a1[4] = cc.w;
             a1[5] = rt.w;
             a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
@@ -312,15 +331,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 uint32_t a1[8];
                 a1[0] = hlerp2(y0lo, y1lo, rt.z);
                 a1[1] = hlerp2(y0hi, y1hi, rt.z);
-                if (FMT_UV == FMT_BC7) {
-                    u8x4_to_h2(sUv[(jr + s) * C + tid], a1[2], a1[3]);
-                } else if (FMT_UV == FMT_U8) {
-                    u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)(row + s) * C + tid), a1[2], a1[3]);
-                } else {
-                    const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)(row + s) * C + tid);
-                    a1[2] = hv.x;
-                    a1[3] = hv.y;
-                }
+                uv_texel(row + s, jr + s, 0, a1[2], a1[3]);
                 a1[4] = cc.w;
                 a1[5] = rt.w;
                 a1[6] = 0x00003C00u;
@@ -544,6 +555,7 @@ int fused_ctas_per_sm(int H) { return H == 16 ? FusedCfg<16>::MIN_CTAS : FusedCf
 
 template <int H, int CT>
 static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t s) {
+    if (p.fmt_uv == FMT_BC7_TEX) return launch_fused_t<H, FMT_BC7_TEX, CT>(p, num_sms, s);
     if (p.fmt_uv == FMT_BC7) return launch_fused_t<H, FMT_BC7, CT>(p, num_sms, s);
     if (p.fmt_uv == FMT_U8) return launch_fused_t<H, FMT_U8, CT>(p, num_sms, s);
     return launch_fused_t<H, FMT_F16, CT>(p, num_sms, s);

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,9 @@ cudaError_t launch_fused_hmma(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_pipe(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
+cudaError_t uv_textures_build(const void* uv, int atlases, int tiles_x, int tiles_y, int C, cudaArray_t* arrays,
+                              unsigned long long* texs);
+void uv_textures_free(int atlases, cudaArray_t* arrays, unsigned long long* texs);
 size_t wpack_tile_bytes(int H);
 cudaError_t prep_weights(const uint16_t* mlp, size_t tile_elems, int H, int fmt_uv, uint8_t* out, int num_tiles,
                          cudaStream_t s);
@@ -39,6 +43,11 @@ struct ndgi_ctx {
     int num_sms;
     uint32_t* d_err;
     uint8_t* wpack;   // prepacked tcgen05 B operands per tile (FAST layouts), owned
+    // NDGI_MODE_FAST_TEXUNIT: per-atlas BC7 F_uv textures, built on first use
+    std::mutex tex_mu;
+    bool tex_ready;
+    cudaArray_t uvarr[ndgi::kMaxTexAtlases];
+    unsigned long long uvtex[ndgi::kMaxTexAtlases];
     // host-buffer path
     cudaStream_t hstream[2];
     cudaEvent_t hevent[2];
@@ -199,7 +208,27 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
     int fast = 0;
     validate(&ctx->L, &fast);
     cudaError_t e;
-    if (mode == NDGI_MODE_FAST) {
+    if (mode == NDGI_MODE_FAST_TEXUNIT) {
+        if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
+        if (ctx->L.fmt_uv != NDGI_FMT_BC7 || ctx->L.atlases > (uint32_t)ndgi::kMaxTexAtlases)
+            return fail(NDGI_ERR_UNSUPPORTED, "NDGI_MODE_FAST_TEXUNIT needs BC7 F_uv and <= 64 atlases");
+        {
+            std::lock_guard<std::mutex> lock(ctx->tex_mu);
+            if (!ctx->tex_ready) {
+                e = ndgi::uv_textures_build(ctx->P.uv, (int)ctx->L.atlases, (int)ctx->L.tiles_x, (int)ctx->L.tiles_y,
+                                            (int)ctx->L.core, ctx->uvarr, ctx->uvtex);
+                if (e != cudaSuccess) {
+                    ndgi::uv_textures_free((int)ctx->L.atlases, ctx->uvarr, ctx->uvtex);
+                    return cuda_fail(e, "building the BC7 F_uv textures");
+                }
+                ctx->tex_ready = true;
+            }
+        }
+        for (uint32_t a = 0; a < ctx->L.atlases; ++a) p.uvtex[a] = ctx->uvtex[a];
+        p.fmt_uv = ndgi::FMT_BC7_TEX;
+        choose_strips(p, ctx->num_sms, 4);
+        e = ndgi::launch_fused(p, ctx->num_sms, s);
+    } else if (mode == NDGI_MODE_FAST) {
         if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
         // NDGI_KERNEL selects the measured h = 16 alternatives (DESIGN.md
         // §6.1 schedule experiments): ws, hmma, pipe
@@ -223,7 +252,7 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
     return NDGI_OK;
 }
 
-bool mode_ok(int m) { return m == NDGI_MODE_FAST || m == NDGI_MODE_REF_FP32; }
+bool mode_ok(int m) { return m == NDGI_MODE_FAST || m == NDGI_MODE_REF_FP32 || m == NDGI_MODE_FAST_TEXUNIT; }
 bool out_ok(int f) { return f >= NDGI_OUT_RGBA8 && f <= NDGI_OUT_RGBA32F; }
 
 ndgi_status decode_full_async(ndgi_ctx* ctx, const float* ts, uint32_t nt, void* out, ndgi_out_fmt fmt,
@@ -504,6 +533,7 @@ ndgi_status ndgi_free(ndgi_ctx* ctx) {
     cudaDeviceSynchronize();
     cudaFree(ctx->d_err);
     if (ctx->wpack) cudaFree(ctx->wpack);
+    if (ctx->tex_ready) ndgi::uv_textures_free((int)ctx->L.atlases, ctx->uvarr, ctx->uvtex);
     for (int i = 0; i < 2; ++i) {
         if (ctx->stage[i]) cudaFree(ctx->stage[i]);
         if (ctx->hstream[i]) cudaStreamDestroy(ctx->hstream[i]);

@@ -8,6 +8,9 @@
 namespace ndgi {
 
 enum : int { FMT_BC7 = 0, FMT_U8 = 1, FMT_F16 = 2 };
+// kernel-internal: BC7 F_uv fetched through the texture unit (NDGI_MODE_FAST_TEXUNIT)
+constexpr int FMT_BC7_TEX = 3;
+constexpr int kMaxTexAtlases = 64;
 enum : int { OUT_RGBA8 = 0, OUT_RGBA16F = 1, OUT_RGBA32F = 2 };
 enum : int { GELU_ERF = 0, GELU_TANH = 1 };
 enum : int { BORDER_MIRROR = 0, BORDER_EVAL_CLAMP = 1 };
@@ -36,6 +39,7 @@ struct KParams {
     const uint8_t* vt;
     const uint16_t* mlp;
     const uint8_t* wpack;       // per-tile prepacked tcgen05 B operands (ndgi_load), or nullptr
+    unsigned long long uvtex[kMaxTexAtlases];   // NDGI_MODE_FAST_TEXUNIT: BC7 F_uv texture per atlas
     size_t uv_tile_bytes, uvt_tile_bytes, uvt_slice_bytes, line_tile_bytes, mlp_tile_elems;
     // per-call constants (call setup), one set per query time,
     // computed on the host in fp64

@@ -220,6 +220,31 @@ def test_cross_format_u8_equals_bc7():
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("payload", ["smooth", "mixed"])
+def test_texture_unit_fetch_equals_software_decode(payload):
+    # NDGI_MODE_FAST_TEXUNIT (F_uv through the texture unit's BC7 decoder) is
+    # bit-identical to NDGI_MODE_FAST on all outputs, incl. all-mode payloads,
+    # several atlases, decode_tiles with borders and small-batch strips
+    lay = S.layout(2, 2, 2, "M", uvt_depth=4, line_t=4)
+    th = S.make_theta(lay, 41, payload)
+    ctx = _load(lay, th)
+    for fmt in ("rgba8", "rgba32f"):
+        np.testing.assert_array_equal(gpu_full(ctx, [0.2, 0.7], fmt, "fast_texunit"), gpu_full(ctx, [0.2, 0.7], fmt))
+    ids = [5, 0, 7, 2]
+    np.testing.assert_array_equal(gpu_tiles(ctx, ids, 0.33, "rgba8", "fast_texunit"), gpu_tiles(ctx, ids, 0.33, "rgba8"))
+    np.testing.assert_array_equal(gpu_tiles(ctx, [3], 0.9, "rgba32f", "fast_texunit"), gpu_tiles(ctx, [3], 0.9))
+
+
+def test_texture_unit_mode_needs_bc7():
+    lay, seed = S.config("c1")
+    lay8 = dict(lay, fmt_uv="u8")
+    th = S.make_theta(lay8, seed)
+    ctx = _load(lay8, th)
+    with pytest.raises(ndgi.NdgiError) as e:
+        gpu_full(ctx, 0.5, "rgba8", "fast_texunit")
+    assert e.value.status == ndgi.ERR_UNSUPPORTED
+
+
 def test_batch_equals_single_calls():
     lay, seed = S.config("c1")
     th = S.make_theta(lay, seed)
