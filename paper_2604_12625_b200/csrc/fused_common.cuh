@@ -171,6 +171,24 @@ __device__ __forceinline__ void gelu_epilogue2_h16(uint32_t d0, uint32_t a0, uin
     ptx::tmem_st_x8(a1, h);
 }
 
+// ---- windowed F_uvt (large R3, C = 128): per-warp window of the tau-blended
+// slice covering the F_uvt texels one F_uv chunk of this warp's 32 columns
+// can touch.  wxb / wyb = window width / height in 4x4 blocks (margin 2 for
+// the bilinear neighbour and block misalignment).
+struct UvtWindow {
+    int wxb, wyb;
+    uint32_t pitch, bytes;   // bytes per window row, per warp window
+};
+__host__ __device__ inline UvtWindow uvt_window(int R3, int C, int chunk_rows) {
+    UvtWindow w;
+    w.wxb = (32 * R3 / C) / 4 + 2;
+    w.wyb = (chunk_rows * R3 / C) / 4 + 2;
+    while (w.wyb & (w.wyb - 1)) ++w.wyb;   // ring of a power-of-two number of block rows
+    w.pitch = (uint32_t)w.wxb * 4u * 8u;
+    w.bytes = (uint32_t)w.wyb * 4u * w.pitch;
+    return w;
+}
+
 // ---- load-time weight prepack ------------------------------------------------
 // Per tile, the t-independent part of the three tcgen05 B operands with the
 // GELU folds of DESIGN.md §6.1, already in the smem layout (bofs), followed by
@@ -256,9 +274,13 @@ __device__ __forceinline__ void copy_prepacked_weights(const KParams& p, const T
 // B operands (with the folds of DESIGN.md §6.1), the tau-blended F_uvt slice,
 // V_ut per column and the per-row gather table (F_uvt y taps, V_vt).
 // Executed by threads tid = 0 .. nthr-1 of the CTA.
+// win_pitch == 0: the whole tau-blended F_uvt slice goes to smem (row offsets
+// y * R3 * 8); > 0: the kernel stages per-warp ring windows of win_rows (a
+// power of two) F_uvt rows itself and the row table holds ring-row offsets
 template <int H, int FMT_UV, int C, bool TC_WEIGHTS = true>
 __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc, int k, uint8_t* smem,
-                                              const FusedSmem& L, int tid, int nthr) {
+                                              const FusedSmem& L, int tid, int nthr, uint32_t win_pitch = 0,
+                                              int win_rows = 0) {
     using Cfg = FusedCfg<H>;
     const int R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);
@@ -310,7 +332,9 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
             // F_uvt slices k0, k1 blended with tau (R4, R17) -> f16x4 [R3][R3], values in [0,1]
             const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
             const float tau = tc.tau, omt = 1.0f - tau;
-            if (p.fmt_uvt == FMT_BC7) {
+            if (win_pitch) {
+                // windowed: staged per chunk by the kernel
+            } else if (p.fmt_uvt == FMT_BC7) {
                 const int nbx = R3 >> 2, nb = nbx * nbx;
                 const uint4* s0 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k0);
                 const uint4* s1 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k1);
@@ -386,8 +410,10 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                     const float sy = fmaf((float)i + 0.5f, sc3, -0.5f);
                     const float fly = floorf(sy);
                     const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
-                    sRow[i] = make_uint4((uint32_t)(y0 * R3) * 8u, (uint32_t)(y1 * R3) * 8u, pack_f16x2(sy - fly, sy - fly),
-                                         pack_f16x2(c[0], c[1]));
+                    // whole slice: row y at y * R3 * 8; window: ring row y mod (win_rows)
+                    const uint32_t r0 = win_pitch ? (uint32_t)(y0 & (win_rows - 1)) * win_pitch : (uint32_t)y0 * R3 * 8u;
+                    const uint32_t r1 = win_pitch ? (uint32_t)(y1 & (win_rows - 1)) * win_pitch : (uint32_t)y1 * R3 * 8u;
+                    sRow[i] = make_uint4(r0, r1, pack_f16x2(sy - fly, sy - fly), pack_f16x2(c[0], c[1]));
                 }
             }
         }

@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "fused_common.cuh"
 
@@ -62,7 +63,9 @@ __device__ int g_ndgi_res[256];   // resident CTAs per SM (profiling builds only
 
 // FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
 // no format switch, row pointers instead of 64-bit index arithmetic
-template <int H, int FMT_UV, int CT, bool FULL8>
+// WIN: F_uvt staged per chunk in per-warp windows instead of the whole slice
+// (large R3: the H profile's 32 KB slice would halve residency)
+template <int H, int FMT_UV, int CT, bool FULL8, bool WIN>
 __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_kernel(const __grid_constant__ KParams p) {
     using Cfg = FusedCfg<H>;
     constexpr int S = Cfg::SLOTS;
@@ -94,6 +97,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 
     const int B = p.B, P = p.P, R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
+    static_assert(!WIN || CT == 128, "windowed F_uvt is built for C = 128");
+    const UvtWindow win = uvt_window(R3, C, chunk_rows);
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
     const uint32_t tm_lane = tmem + lane_base;
 
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         {
             PROF_T0();
             copy_prepacked_weights<H>(p, tc, k, smem, L, tid, kThreads);
-            unit_prologue<H, FMT_UV, C, false>(p, tc, k, smem, L, tid, kThreads);
+            unit_prologue<H, FMT_UV, C, false>(p, tc, k, smem, L, tid, kThreads, WIN ? win.pitch : 0u, win.wyb * 4);
             PROF_ADD(5);
         }
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
@@ -167,10 +172,22 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const int i = b * kThreads + tid;
             const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
             const float flx = floorf(sx);
-            sCol[i] = make_uint4(L.uvt + (uint32_t)clampi((int)flx, 0, R3 - 1) * 8u,
-                                 L.uvt + (uint32_t)clampi((int)flx + 1, 0, R3 - 1) * 8u, pack_f16x2(sx - flx, sx - flx),
-                                 sUt[i]);
+            const int x0 = clampi((int)flx, 0, R3 - 1), x1 = clampi((int)flx + 1, 0, R3 - 1);
+            if constexpr (WIN) {
+                // this warp's window starts at the block column of its lane 0
+                const int wx0 = __shfl_sync(0xffffffffu, x0, 0) & ~3;
+                const uint32_t wb = L.uvt + (uint32_t)warp * win.bytes;
+                sCol[i] = make_uint4(wb + (uint32_t)(x0 - wx0) * 8u, wb + (uint32_t)(x1 - wx0) * 8u,
+                                     pack_f16x2(sx - flx, sx - flx), sUt[i]);
+            } else {
+                sCol[i] = make_uint4(L.uvt + (uint32_t)x0 * 8u, L.uvt + (uint32_t)x1 * 8u, pack_f16x2(sx - flx, sx - flx),
+                                     sUt[i]);
+            }
         }
+        // WIN: window block column of this warp (lane 0's first x tap)
+        const int wbx0 = WIN ? (__shfl_sync(0xffffffffu, clampi((int)floorf(fmaf((float)tid + 0.5f, sc3, -0.5f)), 0, R3 - 1), 0) >> 2) : 0;
+        const uint8_t* const wbase = smem;   // F_uvt taps: row offsets are ring rows (WIN) or slice rows
+        (void)wbx0;
         const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
         // decoded F_uv chunk, row-major [chunk_rows][C] RGBA8 (each warp decodes
         // the blocks of its own 32 columns)
@@ -237,6 +254,97 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             __syncwarp();
         };
 
+        // WIN: this warp's ring window of the tau-blended F_uvt slice: wyb*4
+        // (a power of two) F_uvt rows x wxb*4 columns, F_uvt row y in ring row
+        // y mod (wyb*4); per chunk only the block rows not yet resident are
+        // decoded (same blend arithmetic as unit_prologue, so bit-identical to
+        // the whole-slice path)
+        int w_lo = 1, w_hi = 0;   // resident block rows [w_lo, w_hi] (empty)
+        auto stage_window = [&](int jc, int nrows) {
+            const int ymin = clampi((int)floorf(fmaf((float)jc + 0.5f, sc3, -0.5f)), 0, R3 - 1);
+            const int ymax = clampi((int)floorf(fmaf((float)(jc + nrows - 1) + 0.5f, sc3, -0.5f)) + 1, 0, R3 - 1);
+            const int blo = ymin >> 2, bhi = ymax >> 2;
+            const int nbm = R3 >> 2, ring = win.wyb;
+            const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
+            const float tau = tc.tau, omt = 1.0f - tau;
+            uint2* wdst = reinterpret_cast<uint2*>(smem + L.uvt + (uint32_t)warp * win.bytes);
+            const int WX = win.wxb * 4;
+            // new block rows: [blo, bhi] minus the resident [w_lo, w_hi] (monotone strips)
+            const int n0 = (w_hi >= w_lo && blo >= w_lo && blo <= w_hi) ? w_hi + 1 : blo;
+            const int nnew = bhi - n0 + 1;
+            __syncwarp();   // this warp's gathers of the previous chunk are done
+            if (nnew > 0) {
+                if (p.fmt_uvt == FMT_BC7) {
+                    // one BC7 block per lane (both slices' blocks: 2 * nnew * wxb <= 48
+                    // decodes), raw RGBA8 into this warp's part of the F_uv chunk
+                    // buffer (free between chunks: 16 rows x 128 B), then all lanes
+                    // blend texels into the ring
+                    const int nblk = nnew * win.wxb;             // block positions
+                    uint8_t* scratch = reinterpret_cast<uint8_t*>(sUv) + warp * 128;   // row r at + r * C * 4
+                    for (int g0 = 0; g0 < nblk; g0 += 16) {      // 16 positions = 32 blocks per round
+                        const int ng = nblk - g0 < 16 ? nblk - g0 : 16;
+                        {
+                            const int q = lane < 2 * ng ? lane : 0;   // spare lanes: duplicate, no store
+                            const int pos = g0 + (q >> 1), sl = q & 1;
+                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
+                            const int gbx = wbx0 + qx < nbm ? wbx0 + qx : nbm - 1;
+                            const uint4* src = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0));
+                            uint32_t t[16];
+                            bc7_decode(__ldg(src + br * nbm + gbx), [&](int i, uint32_t v) { t[i] = v; });
+                            if (lane < 2 * ng) {
+                                // scratch slot q: 64 B at row q >> 1, byte (q & 1) * 64
+                                uint4* d = reinterpret_cast<uint4*>(scratch + (size_t)(q >> 1) * C * 4 + (q & 1) * 64);
+#pragma unroll
+                                for (int r = 0; r < 4; ++r) d[r] = make_uint4(t[4 * r], t[4 * r + 1], t[4 * r + 2], t[4 * r + 3]);
+                            }
+                        }
+                        __syncwarp();
+                        for (int e = lane; e < ng * 16; e += 32) {
+                            const int pos = g0 + (e >> 4), i = e & 15;
+                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
+                            if (wbx0 + qx >= nbm) continue;
+                            const uint32_t* sp = reinterpret_cast<const uint32_t*>(scratch + (size_t)(e >> 4) * C * 4);
+                            const uint32_t q0v = sp[i], q1v = sp[16 + i];
+                            float c[4];
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[qq] = (omt * (float)((q0v >> (8 * qq)) & 0xffu) + tau * (float)((q1v >> (8 * qq)) & 0xffu)) *
+                                        (1.0f / 255.0f);
+                            wdst[((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)] =
+                                make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+                        }
+                        __syncwarp();
+                    }
+                } else {
+                    const int ntex = nnew * 4 * WX;
+                    for (int e = lane; e < ntex; e += 32) {
+                        const int gy = n0 * 4 + e / WX, gx = wbx0 * 4 + e % WX;
+                        if (gx >= R3) continue;
+                        const int g = gy * R3 + gx;
+                        float c[4];
+                        if (p.fmt_uvt == FMT_U8) {
+                            const uint32_t q0 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k0) + g);
+                            const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + g);
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[qq] = (omt * (float)((q0 >> (8 * qq)) & 0xffu) + tau * (float)((q1 >> (8 * qq)) & 0xffu)) *
+                                        (1.0f / 255.0f);
+                        } else {
+                            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * g;
+                            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k1) + 4 * g;
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
+                        }
+                        wdst[((gy & (4 * ring - 1))) * WX + e % WX] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+                    }
+                }
+            }
+            __syncwarp();
+            w_lo = blo;
+            w_hi = bhi;
+        };
+
         // one layer for all S items of the step: A written by all 128 threads ->
         // CTA barrier -> one elected lane of warp 0 issues S x (K/16) MMAs and
         // commits them to d_ready -> everyone waits for the accumulators
@@ -291,10 +399,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         auto gather = [&](int row, int jr, int blk, int s) {
             const uint4 rt = sRow[row];                  // y0 row byte offset, y1 row byte offset, fy, V_vt
             const uint4 cc = sCol[blk * kThreads + tid]; // x0, x1 byte offsets (from smem base), fx, V_ut
-            const uint2 t00 = *reinterpret_cast<const uint2*>(smem + rt.x + cc.x);
-            const uint2 t10 = *reinterpret_cast<const uint2*>(smem + rt.x + cc.y);
-            const uint2 t01 = *reinterpret_cast<const uint2*>(smem + rt.y + cc.x);
-            const uint2 t11 = *reinterpret_cast<const uint2*>(smem + rt.y + cc.y);
+            const uint2 t00 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.x);
+            const uint2 t10 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.y);
+            const uint2 t01 = *reinterpret_cast<const uint2*>(wbase + rt.y + cc.x);
+            const uint2 t11 = *reinterpret_cast<const uint2*>(wbase + rt.y + cc.y);
             uint32_t a1[8];
             a1[0] = hlerp2(hlerp2(t00.x, t10.x, cc.z), hlerp2(t01.x, t11.x, cc.z), rt.z);
             a1[1] = hlerp2(hlerp2(t00.y, t10.y, cc.z), hlerp2(t01.y, t11.y, cc.z), rt.z);
@@ -313,8 +421,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const uint4 rt0 = sRow[row], rt1 = sRow[row + 1];
             const uint4 cc = sCol[tid];
             auto xlerp = [&](uint32_t yoff, uint32_t& lo, uint32_t& hi) {
-                const uint2 a = *reinterpret_cast<const uint2*>(smem + yoff + cc.x);
-                const uint2 b = *reinterpret_cast<const uint2*>(smem + yoff + cc.y);
+                const uint2 a = *reinterpret_cast<const uint2*>(wbase + yoff + cc.x);
+                const uint2 b = *reinterpret_cast<const uint2*>(wbase + yoff + cc.y);
                 lo = hlerp2(a.x, b.x, cc.z);
                 hi = hlerp2(a.y, b.y, cc.z);
             };
@@ -414,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         const int crows = p.strip_rows < chunk_rows ? p.strip_rows : chunk_rows;
         const int chunk_items = crows * BPR;
         for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
+        if constexpr (WIN) stage_window(j_begin + c0 / BPR, crows);   // uses the F_uv chunk buffer as scratch
         if (FMT_UV == FMT_BC7) decode_chunk(j_begin + c0 / BPR, crows);
         for (int it = c0; it < c0 + chunk_items; it += S) {
             PROF_T0();
@@ -464,26 +573,33 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 // size: computed once (attribute calls cost microseconds, which a small VT
 // batch would otherwise pay on every call).
 struct LaunchCfg {
-    int dev = -1;
-    uint32_t smem = 0;
-    int occ = 0;
+    const void* kern;
+    int dev;
+    uint32_t smem;
+    int occ;
 };
 
 template <typename K>
 static cudaError_t fused_launch_cfg(K kern, uint32_t smem, int tmem_cols, int& occ_out) {
-    constexpr int kMaxDev = 16;
     static std::mutex mu;
-    static LaunchCfg cache[kMaxDev];
+    static std::vector<LaunchCfg> cache;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
-    LaunchCfg& c = cache[dev % kMaxDev];
-    if (c.dev == dev && c.smem == smem) {
-        occ_out = c.occ;
-        return cudaSuccess;
+    // the dynamic-smem limit is per-kernel state: keep it at the largest size
+    // this kernel has been configured for (a smaller later setting would make
+    // a cached larger configuration fail to launch)
+    uint32_t attr = smem;
+    for (const LaunchCfg& c : cache) {
+        if (c.kern != reinterpret_cast<const void*>(kern) || c.dev != dev) continue;
+        if (c.smem == smem) {
+            occ_out = c.occ;
+            return cudaSuccess;
+        }
+        if (c.smem > attr) attr = c.smem;
     }
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
@@ -505,9 +621,7 @@ static cudaError_t fused_launch_cfg(K kern, uint32_t smem, int tmem_cols, int& o
     if (getenv("NDGI_VERBOSE"))
         fprintf(stderr, "[ndgi] fused launch cfg: occ=%d (regs %d, local %zu) smem=%u\n", occ, fa.numRegs,
                 fa.localSizeBytes, smem);
-    c.dev = dev;
-    c.smem = smem;
-    c.occ = occ;
+    cache.push_back(LaunchCfg{reinterpret_cast<const void*>(kern), dev, smem, occ});
     occ_out = occ;
     return cudaSuccess;
 }
@@ -516,14 +630,23 @@ template <int H, int FMT_UV, int CT>
 static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
     const FusedSmem L = fused_smem_layout<H>(CT, p.R3);
     const bool full8 = p.full && p.out_fmt == OUT_RGBA8;
-    auto kern = full8 ? ndgi_fused_kernel<H, FMT_UV, CT, true> : ndgi_fused_kernel<H, FMT_UV, CT, false>;
+    // windowed F_uvt when the whole slice would cost residency (h = 16, C = 128)
+    constexpr bool kWinOk = H == 16 && CT == 128;
+    const bool win = kWinOk && p.R3 > 32;
+    uint32_t smem = L.total;
+    if (win) smem = L.uvt + 4u * uvt_window(p.R3, CT, kChunkTexels / CT).bytes;
+    auto pick = [&](auto f8, auto w) {
+        return ndgi_fused_kernel<H, FMT_UV, CT, decltype(f8)::value, decltype(w)::value && kWinOk>;
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    auto kern = full8 ? (win ? pick(T_{}, T_{}) : pick(T_{}, F_{})) : (win ? pick(F_{}, T_{}) : pick(F_{}, F_{}));
     int occ = 0;
-    cudaError_t e = full8 ? fused_launch_cfg(ndgi_fused_kernel<H, FMT_UV, CT, true>, L.total, FusedCfg<H>::TM_COLS, occ)
-                          : fused_launch_cfg(ndgi_fused_kernel<H, FMT_UV, CT, false>, L.total, FusedCfg<H>::TM_COLS, occ);
+    cudaError_t e = fused_launch_cfg(kern, smem, FusedCfg<H>::TM_COLS, occ);
     if (e != cudaSuccess) return e;
     const uint32_t cap = (uint32_t)(num_sms * occ);
     const uint32_t grid = p.units < cap ? p.units : cap;
-    kern<<<grid, kThreads, L.total, s>>>(p);
+    kern<<<grid, kThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -148,7 +148,9 @@ FAST_CASES = {
     "f16": (S.layout(1, 2, 1, "M", uvt_depth=5, line_t=7, fmt_uv="f16", fmt_uvt="f16", fmt_line="f16"), "smooth"),
     "M64": (S.layout(1, 2, 1, "M64", uvt_depth=4, line_t=4), "smooth"),
     "L-tanh": (S.layout(1, 2, 1, "L", gelu="tanh"), "smooth"),
-    "H": (S.layout(1, 1, 2, "H"), "mixed"),
+    "H": (S.layout(1, 1, 2, "H"), "mixed"),          # R3 = 64: windowed F_uvt (BC7 windows)
+    "H-u8": (S.layout(1, 2, 1, "H", fmt_uv="u8", fmt_uvt="u8"), "smooth"),
+    "H-f16": (S.layout(1, 2, 1, "H", fmt_uv="f16", fmt_uvt="f16", fmt_line="f16"), "smooth"),
     "C256": (S.layout(1, 1, 1, "M", core=256, uv_res=256), "smooth"),
 }
 
@@ -265,6 +267,20 @@ def test_small_batches_strips():
         got = gpu_tiles(ctx, ids, 0.9, "rgba32f")
         exp = M.decode_tiles(ids, 0.9, NTHR)
         mx, mean = _err(got, exp)
+        assert mx <= FAST_MAX and mean <= FAST_MEAN
+
+
+def test_windowed_uvt_small_strips():
+    # H profile (windowed F_uvt) through decode_tiles: 4-row strips (n = 1),
+    # 8-row strips and whole tiles, against the oracle
+    lay = S.layout(1, 2, 2, "H")
+    th = S.make_theta(lay, 17, "mixed")
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    for ids in ([1], [3, 0], list(range(4)) * 300):
+        got = gpu_tiles(ctx, ids, 0.61, "rgba32f")
+        exp = M.decode_tiles(ids[:4], 0.61, NTHR)
+        mx, mean = _err(got[:4], exp)
         assert mx <= FAST_MAX and mean <= FAST_MEAN
 
 
