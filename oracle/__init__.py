@@ -75,6 +75,8 @@ def lib():
             "oracle_quantize_rgba8_f32": (None, [P, C.c_size_t, C.c_size_t, P]),
             "oracle_mlp_params": (C.c_size_t, [I]),
             "oracle_mean_at": (I, [P, P, I, D, P]),
+            "oracle_bc7_encode_mode6": (None, [P, P]),
+            "oracle_bc7_encode_image_mode6": (None, [P, I, I, P]),
             "oracle_restore": (D, [D, D, D]),
             "oracle_sample_lighting": (I, [P, P, I, I, I, I, I, D, D, I, D, P, P]),
         }
@@ -259,3 +261,21 @@ def sample_lighting(cache: np.ndarray, page_table: np.ndarray, core: int, border
             out[i] = o3
             ok[i] = True
     return out, ok
+
+
+# ---------------------------------------------------------------- BC7 mode-6 encoder (R26)
+def bc7_encode_block_mode6(px: np.ndarray) -> np.ndarray:
+    """16 RGBA8 texels (texel = 4*row + col) -> one 16-byte mode-6 block."""
+    px = np.ascontiguousarray(np.asarray(px, np.uint8).reshape(64))
+    out = np.zeros(16, np.uint8)
+    lib().oracle_bc7_encode_mode6(_ptr(px), _ptr(out))
+    return out
+
+
+def bc7_encode_image_mode6(rgba: np.ndarray) -> np.ndarray:
+    """[h][w][4] RGBA8 (h, w multiples of 4) -> [h/4 * w/4][16] blocks, row-major."""
+    rgba = np.ascontiguousarray(rgba, np.uint8)
+    h, w = rgba.shape[:2]
+    out = np.zeros(((h // 4) * (w // 4), 16), np.uint8)
+    lib().oracle_bc7_encode_image_mode6(_ptr(rgba), w, h, _ptr(out))
+    return out

@@ -630,3 +630,154 @@ int oracle_sample_lighting(const uint8_t *cache, const int32_t *pt, int C, int B
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* BC7 mode-6 encoder ("after training,  */
+/* we not only quantize them to 8-bit, but also apply the BC7          */
+/* compression algorithm", "followed by quantization and BC7     */
+/* compression"; SPEC S:371-385 principal-axis endpoints + nearest     */
+/* indices).  Reading R26 makes it exact integer          */
+/* arithmetic, so the GPU encoder must match it bit for bit:           */
+/*   1. 16*cov = 16*sum(p p^T) - sum(p) sum(p)^T (int64, exact);       */
+/*   2. principal axis by 4 power iterations from the column of the     */
+/*      largest-variance channel, each step w = M v then v = w with     */
+/*      magnitudes shifted right until max|v| < 2^20 (sign kept);       */
+/*   3. endpoints = the texels with the smallest / largest projection   */
+/*      p.v (first index on ties), each quantised to 7 bits + p-bit:    */
+/*      q = clamp((e - p + 1) >> 1, 0, 127) per channel, value 2q + p,  */
+/*      p in {0, 1} minimising the squared error (p = 0 on ties);       */
+/*   4. per texel the 4-bit index minimising the squared error of the   */
+/*      decoder's own interpolation (smallest index on ties);           */
+/*   5. if texel 0's index has its MSB set (mode 6 anchor), swap the    */
+/*      endpoints and replace every index w by 15 - w (W4 is symmetric, */
+/*      so the decoded block is unchanged);                             */
+/*   6. pack LSB-first: mode 6 (0x40), R0 R1 G0 G1 B0 B1 A0 A1 (7 b),  */
+/*      P0, P1, texel 0 index (3 b), texels 1..15 (4 b).                */
+/* ------------------------------------------------------------------ */
+static int bitlen64(uint64_t x) { int n = 0; while (x) { ++n; x >>= 1; } return n; }
+
+static void quant_endpoint_m6(const int e[4], int val[4], int *pbit)
+{
+    int best = -1;
+    for (int p = 0; p < 2; ++p) {
+        int v[4], err = 0;
+        for (int c = 0; c < 4; ++c) {
+            int q = (e[c] - p + 1) >> 1;
+            if (q < 0) q = 0;
+            if (q > 127) q = 127;
+            v[c] = 2 * q + p;
+            err += (v[c] - e[c]) * (v[c] - e[c]);
+        }
+        if (best < 0 || err < best) {
+            best = err;
+            *pbit = p;
+            for (int c = 0; c < 4; ++c) val[c] = v[c];
+        }
+    }
+}
+
+typedef struct { uint8_t *b; int pos; } bitwriter;
+static void put(bitwriter *w, int v, int n)
+{
+    for (int i = 0; i < n; ++i) {
+        if ((v >> i) & 1) w->b[w->pos >> 3] |= (uint8_t)(1u << (w->pos & 7));
+        w->pos++;
+    }
+}
+
+void oracle_bc7_encode_mode6(const uint8_t px[64], uint8_t out[16])
+{
+    int64_t S[4] = {0, 0, 0, 0}, Q[4][4];
+    memset(Q, 0, sizeof(Q));
+    for (int i = 0; i < 16; ++i)
+        for (int c = 0; c < 4; ++c) {
+            S[c] += px[4 * i + c];
+            for (int d = 0; d < 4; ++d) Q[c][d] += (int64_t)px[4 * i + c] * px[4 * i + d];
+        }
+    int64_t M[4][4];
+    for (int c = 0; c < 4; ++c)
+        for (int d = 0; d < 4; ++d) M[c][d] = 16 * Q[c][d] - S[c] * S[d];
+    /* step 2 */
+    int cs = 0;
+    for (int c = 1; c < 4; ++c)
+        if (M[c][c] > M[cs][cs]) cs = c;
+    int64_t v[4];
+    for (int c = 0; c < 4; ++c) v[c] = M[c][cs];
+    for (int it = 0; it <= 4; ++it) {
+        int64_t w[4];
+        if (it == 0) {
+            for (int c = 0; c < 4; ++c) w[c] = v[c];
+        } else {
+            for (int c = 0; c < 4; ++c) {
+                w[c] = 0;
+                for (int d = 0; d < 4; ++d) w[c] += M[c][d] * v[d];
+            }
+        }
+        uint64_t mx = 0;
+        for (int c = 0; c < 4; ++c) {
+            uint64_t a = (uint64_t)(w[c] < 0 ? -w[c] : w[c]);
+            if (a > mx) mx = a;
+        }
+        if (mx == 0) {   /* constant block or v in the null space: keep v (or (1,1,1,1)) */
+            if (it == 0) for (int c = 0; c < 4; ++c) v[c] = 1;
+            break;
+        }
+        const int s = bitlen64(mx) > 20 ? bitlen64(mx) - 20 : 0;
+        for (int c = 0; c < 4; ++c) {
+            const uint64_t a = (uint64_t)(w[c] < 0 ? -w[c] : w[c]) >> s;
+            v[c] = w[c] < 0 ? -(int64_t)a : (int64_t)a;
+        }
+    }
+    /* step 3 */
+    int imin = 0, imax = 0;
+    int64_t dmin = 0, dmax = 0;
+    for (int i = 0; i < 16; ++i) {
+        int64_t d = 0;
+        for (int c = 0; c < 4; ++c) d += (int64_t)px[4 * i + c] * v[c];
+        if (i == 0 || d < dmin) { dmin = d; imin = i; }
+        if (i == 0 || d > dmax) { dmax = d; imax = i; }
+    }
+    int e0[4], e1[4], E0[4], E1[4], p0, p1;
+    for (int c = 0; c < 4; ++c) { e0[c] = px[4 * imin + c]; e1[c] = px[4 * imax + c]; }
+    quant_endpoint_m6(e0, E0, &p0);
+    quant_endpoint_m6(e1, E1, &p1);
+    /* step 4 */
+    int idx[16];
+    for (int i = 0; i < 16; ++i) {
+        int best = -1;
+        for (int w = 0; w < 16; ++w) {
+            int err = 0;
+            for (int c = 0; c < 4; ++c) {
+                const int d = interp(E0[c], E1[c], BC7_W4[w]) - px[4 * i + c];
+                err += d * d;
+            }
+            if (best < 0 || err < best) { best = err; idx[i] = w; }
+        }
+    }
+    /* step 5 */
+    if (idx[0] >= 8) {
+        for (int c = 0; c < 4; ++c) { int t = E0[c]; E0[c] = E1[c]; E1[c] = t; }
+        int t = p0; p0 = p1; p1 = t;
+        for (int i = 0; i < 16; ++i) idx[i] = 15 - idx[i];
+    }
+    /* step 6 */
+    memset(out, 0, 16);
+    bitwriter bw = {out, 0};
+    put(&bw, 1 << 6, 7);
+    for (int c = 0; c < 4; ++c) { put(&bw, E0[c] >> 1, 7); put(&bw, E1[c] >> 1, 7); }
+    put(&bw, p0, 1);
+    put(&bw, p1, 1);
+    put(&bw, idx[0], 3);
+    for (int i = 1; i < 16; ++i) put(&bw, idx[i], 4);
+}
+
+void oracle_bc7_encode_image_mode6(const uint8_t *rgba, int w, int h, uint8_t *blocks)
+{
+    for (int by = 0; by < h / 4; ++by)
+        for (int bx = 0; bx < w / 4; ++bx) {
+            uint8_t px[64];
+            for (int i = 0; i < 16; ++i)
+                memcpy(px + 4 * i, rgba + ((size_t)(4 * by + i / 4) * w + 4 * bx + i % 4) * 4, 4);
+            oracle_bc7_encode_mode6(px, blocks + ((size_t)by * (w / 4) + bx) * 16);
+        }
+}
