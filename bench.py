@@ -341,12 +341,18 @@ def run_gpu(args, rank, world, dist):
             shading = shading_leg(ndgi, torch, args)
         except Exception as exc:  # pragma: no cover
             shading = {"error": repr(exc)}
+    encode = None
+    if not args.no_encode and world == 1:
+        try:
+            encode = encode_leg(ndgi, torch, args)
+        except Exception as exc:  # pragma: no cover
+            encode = {"error": repr(exc)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank, args.workload),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
-        "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading, "texunit": texunit,
+        "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading, "texunit": texunit, "bc7_encode": encode,
         "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
     }
     print(json.dumps(line), flush=True)
@@ -462,6 +468,36 @@ def shading_leg(ndgi, torch, args):
     return res
 
 
+def encode_leg(ndgi, torch, args):
+    """SURVEY §8(f) NEXT 3, measured: ndgi_bc7_encode_mode6 on an 8192^2 RGBA8
+    feature map (a smooth field with noisy rows), inputs resident; Gtexel/s of
+    input texels and the HBM fraction of its 5 B/texel (4 in, 1 out)."""
+    h = w = 8192
+    yy = torch.arange(h, device="cuda", dtype=torch.float32)[:, None] / h
+    xx = torch.arange(w, device="cuda", dtype=torch.float32)[None, :] / w
+    chans = [torch.clamp(torch.round(255 * (0.5 + 0.3 * torch.sin(2 * np.pi * (a * xx + b * yy) + ph))), 0, 255)
+             for a, b, ph in ((1.3, 2.1, 0.3), (0.7, 2.9, 1.1), (2.2, 0.6, 2.0), (1.9, 1.4, 4.0))]
+    img = torch.stack(chans, -1).to(torch.uint8).contiguous()
+    img[::7] = torch.randint(0, 256, img[::7].shape, device="cuda", dtype=torch.uint8)
+    out = torch.empty(((h // 4) * (w // 4), 16), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        ndgi.ndgi_bc7_encode_mode6(img, out, stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record(stream)
+    for _ in range(reps):
+        ndgi.ndgi_bc7_encode_mode6(img, out, stream)
+    e1.record(stream)
+    e1.synchronize()
+    s_ = e0.elapsed_time(e1) / reps * 1e-3
+    peaks = _peaks()
+    return {"workload": "8192^2 RGBA8 map (smooth field, every 7th row noise) -> BC7 mode 6",
+            "ms": s_ * 1e3, "gtexel_s": h * w / s_ / 1e9,
+            "hbm": {"achieved": 5 * h * w / s_ / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": 5 * h * w / s_ / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes_per_texel": 5}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -472,6 +508,7 @@ def main():
     ap.add_argument("--no-vt", action="store_true", help="skip the VT batch-latency leg")
     ap.add_argument("--no-shading", action="store_true", help="skip the shading-side (NEXT 1) leg")
     ap.add_argument("--no-texunit", action="store_true", help="skip the texture-unit F_uv comparator (NEXT 2)")
+    ap.add_argument("--no-encode", action="store_true", help="skip the BC7 encoder leg (NEXT 3)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
                     help="c2: 1,024 tiles per GPU (weak scaling, default); c4: the 16,384-tile scene sharded (strong)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

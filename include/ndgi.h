@@ -301,6 +301,20 @@ NDGI_API ndgi_status ndgi_sample_lighting(ndgi_ctx* ctx, const int32_t* page_tab
                                           const uint32_t* atlas, uint32_t n, float t, const ndgi_hdr* hdr,
                                           float* out_rgb, void* stream);
 
+/* ------------------------------------------------------------------------
+ * BC7 encoder: the step before the path, turning
+ * 8-bit feature maps into the BC7 payloads ndgi_load takes ("apply the
+ * BC7 compression algorithm, which encodes each 4x4 texel block").
+ * Mode 6 (single subset, RGBA, 7-bit endpoints + p-bits, 4-bit indices),
+ * defined in exact integer arithmetic by reading R26, so the
+ * result is deterministic and equal to the oracle's encoder bit for bit.
+ *   rgba  : DEVICE [h][w][4] u8, row-major (16-byte aligned)
+ *   blocks: DEVICE [h/4][w/4][16 B], block (bx, by) at (by * w/4 + bx) * 16
+ * Errors: ARG (NULL, w or h not a positive multiple of 4), RANGE (> 65536),
+ * CUDA.  Asynchronous on `stream`.
+ * ------------------------------------------------------------------------ */
+NDGI_API ndgi_status ndgi_bc7_encode_mode6(const void* rgba, uint32_t w, uint32_t h, void* blocks, void* stream);
+
 /* ---------------- test hooks (not the product path) ---------------- */
 
 /* Bit-exact BC7 map decode: blocks (DEVICE, (w/4)*(h/4) blocks row-major) ->

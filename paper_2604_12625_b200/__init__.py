@@ -78,6 +78,7 @@ _SIGS = {
     "ndgi_vt_page_table": (_I, [_P, _P]),
     "ndgi_vt_upload": (_I, [_P, _P, _P]),
     "ndgi_vt_stats": (_I, [_P, _P]),
+    "ndgi_bc7_encode_mode6": (_I, [_P, _U32, _U32, _P, _P]),
     "ndgi_sample_lighting": (_I, [_P, _P, C.c_int32, _P, _U32, _P, _P, _U32, _F, C.POINTER(ndgi_hdr), _P, _P]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -337,3 +338,12 @@ def ndgi_sample_lighting(ctx: Context, page_table, bucket: int, cache, num_slots
                                    C.c_void_p(atlas.data_ptr()) if atlas is not None else None, int(n), float(t),
                                    C.byref(h), C.c_void_p(out_rgb.data_ptr()), _stream_ptr(stream))
     _check(st, "ndgi_sample_lighting")
+
+
+# ---------------------------------------------------------------- BC7 encoder (NEXT 3)
+def ndgi_bc7_encode_mode6(rgba, blocks, stream=None) -> None:
+    """rgba: CUDA uint8 [h][w][4]; blocks: CUDA uint8 [h/4 * w/4][16] (or any 16-B-per-block buffer)."""
+    h, w = int(rgba.shape[0]), int(rgba.shape[1])
+    st = _lib.ndgi_bc7_encode_mode6(C.c_void_p(rgba.data_ptr()), w, h, C.c_void_p(blocks.data_ptr()),
+                                    _stream_ptr(stream))
+    _check(st, "ndgi_bc7_encode_mode6")

@@ -1,0 +1,218 @@
+// bc7_encode.cu -- BC7 mode-6 encoder on the GPU (the
+// step before the path, turning 8-bit feature maps into BC7 payloads).
+//
+// P:180 "after training, we not only quantize them to 8-bit, but also apply the
+// BC7 compression algorithm, which encodes each 4x4 texel block"
+// "followed by quantization and BC7 compression to produce the final compressed
+// results".  Reading R26 defines the encoder in exact integer
+// arithmetic (principal axis by shifted power iteration, extreme texels as
+// endpoints, best p-bits, nearest indices, anchor swap), so this kernel matches
+// oracle_bc7_encode_mode6 bit for bit.
+//
+// One thread per 4x4 block, grid-stride.  A warp reads 32 adjacent blocks = 4
+// rows of 512 contiguous bytes (16-B loads) and writes 512 contiguous bytes.
+// The nearest-index search uses |a - b|^2 = |a|^2 + |b|^2 - 2 a.b with a.b as
+// one dp4a per palette entry: |b|^2 is the same for every candidate, so the
+// argmin (and its ties) are those of the squared error itself.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ndgi {
+
+__constant__ int kW4[16] = {0, 4, 9, 13, 17, 21, 26, 30, 34, 38, 43, 47, 51, 55, 60, 64};
+
+__device__ __forceinline__ int ch(uint32_t t, int c) { return (int)((t >> (8 * c)) & 0xffu); }
+
+// 7 bits + p-bit for one endpoint (R26 step 3)
+__device__ __forceinline__ void quant_m6(uint32_t e, int (&val)[4], int& pbit) {
+    int best = -1;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        int v[4], err = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            int q = (ch(e, c) - p + 1) >> 1;
+            q = q < 0 ? 0 : (q > 127 ? 127 : q);
+            v[c] = 2 * q + p;
+            const int d = v[c] - ch(e, c);
+            err += d * d;
+        }
+        if (best < 0 || err < best) {
+            best = err;
+            pbit = p;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) val[c] = v[c];
+        }
+    }
+}
+
+// LSB-first write of n bits of v at bit position pos into 4 words
+__device__ __forceinline__ void put_bits(uint32_t (&w)[4], int& pos, uint32_t v, int n) {
+    const int i = pos >> 5, o = pos & 31;
+    w[i] |= v << o;
+    if (o + n > 32) w[i + 1] |= v >> (32 - o);
+    pos += n;
+}
+
+__global__ void __launch_bounds__(256) bc7_encode_mode6_kernel(const uint8_t* __restrict__ rgba, int w, int h,
+                                                              uint4* __restrict__ out) {
+    const int wb = w >> 2;
+    const size_t nb = (size_t)wb * (h >> 2);
+    for (size_t b = blockIdx.x * (size_t)blockDim.x + threadIdx.x; b < nb; b += (size_t)gridDim.x * blockDim.x) {
+        const int bx = (int)(b % wb), by = (int)(b / wb);
+        uint32_t t[16];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(rgba + ((size_t)(4 * by + r) * w + 4 * bx) * 4));
+            t[4 * r] = q.x;
+            t[4 * r + 1] = q.y;
+            t[4 * r + 2] = q.z;
+            t[4 * r + 3] = q.w;
+        }
+        // 1. 16 * covariance, exact (|entries| < 2^25)
+        int S[4] = {0, 0, 0, 0}, Q[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int r = ch(t[i], 0), g = ch(t[i], 1), bl = ch(t[i], 2), a = ch(t[i], 3);
+            S[0] += r; S[1] += g; S[2] += bl; S[3] += a;
+            Q[0] += r * r; Q[1] += r * g; Q[2] += r * bl; Q[3] += r * a;
+            Q[4] += g * g; Q[5] += g * bl; Q[6] += g * a;
+            Q[7] += bl * bl; Q[8] += bl * a; Q[9] += a * a;
+        }
+        int M[4][4];
+        {
+            int k = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int d = c; d < 4; ++d) {
+                    M[c][d] = 16 * Q[k++] - S[c] * S[d];
+                    M[d][c] = M[c][d];
+                }
+        }
+        // 2. principal axis: 4 power iterations from the largest-variance column,
+        // magnitudes shifted below 2^20 at every step (sign kept)
+        int cs = 0;
+#pragma unroll
+        for (int c = 1; c < 4; ++c)
+            if (M[c][c] > M[cs][cs]) cs = c;
+        long long v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = M[c][cs];
+#pragma unroll 1
+        for (int it = 0; it <= 4; ++it) {
+            long long wv[4];
+            if (it == 0) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) wv[c] = v[c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    wv[c] = 0;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) wv[c] += (long long)M[c][d] * v[d];
+                }
+            }
+            unsigned long long mx = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const unsigned long long a = (unsigned long long)(wv[c] < 0 ? -wv[c] : wv[c]);
+                mx = a > mx ? a : mx;
+            }
+            if (mx == 0) {
+                if (it == 0)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) v[c] = 1;
+                break;
+            }
+            const int bl = 64 - __clzll((long long)mx);
+            const int s = bl > 20 ? bl - 20 : 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const unsigned long long a = (unsigned long long)(wv[c] < 0 ? -wv[c] : wv[c]) >> s;
+                v[c] = wv[c] < 0 ? -(long long)a : (long long)a;
+            }
+        }
+        // 3. extreme texels along the axis (|p.v| < 2^30), first index on ties
+        const int v0 = (int)v[0], v1 = (int)v[1], v2 = (int)v[2], v3 = (int)v[3];
+        int imin = 0, imax = 0, dmin = 0, dmax = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int d = ch(t[i], 0) * v0 + ch(t[i], 1) * v1 + ch(t[i], 2) * v2 + ch(t[i], 3) * v3;
+            if (i == 0 || d < dmin) { dmin = d; imin = i; }
+            if (i == 0 || d > dmax) { dmax = d; imax = i; }
+        }
+        uint32_t emin = t[0], emax = t[0];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            emin = i == imin ? t[i] : emin;
+            emax = i == imax ? t[i] : emax;
+        }
+        int E0[4], E1[4], p0, p1;
+        quant_m6(emin, E0, p0);
+        quant_m6(emax, E1, p1);
+        // 4. palette (the decoder's own interpolation) and nearest index per texel
+        // key_k(texel) = 16 * (|a_k|^2 - 2 a_k.b) + k: its minimum over k is the
+        // smallest squared error, ties to the smallest index (|key| < 2^24)
+        uint32_t pal[16];
+        int key0[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            uint32_t pw = 0;
+            int n2 = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int x = ((64 - kW4[k]) * E0[c] + kW4[k] * E1[c] + 32) >> 6;
+                pw |= (uint32_t)x << (8 * c);
+                n2 += x * x;
+            }
+            pal[k] = pw;
+            key0[k] = 16 * n2 + k;
+        }
+        int idx[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            int best = 0x7fffffff;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) best = min(best, key0[k] - 32 * (int)__dp4a(pal[k], t[i], 0u));
+            idx[i] = best & 15;
+        }
+        // 5. anchor: texel 0's index must fit in 3 bits
+        if (idx[0] >= 8) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { const int x = E0[c]; E0[c] = E1[c]; E1[c] = x; }
+            const int x = p0; p0 = p1; p1 = x;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) idx[i] = 15 - idx[i];
+        }
+        // 6. pack
+        uint32_t wd[4] = {0u, 0u, 0u, 0u};
+        int pos = 0;
+        put_bits(wd, pos, 1u << 6, 7);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            put_bits(wd, pos, (uint32_t)(E0[c] >> 1), 7);
+            put_bits(wd, pos, (uint32_t)(E1[c] >> 1), 7);
+        }
+        put_bits(wd, pos, (uint32_t)p0, 1);
+        put_bits(wd, pos, (uint32_t)p1, 1);
+        put_bits(wd, pos, (uint32_t)idx[0], 3);
+#pragma unroll
+        for (int i = 1; i < 16; ++i) put_bits(wd, pos, (uint32_t)idx[i], 4);
+        out[b] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+}
+
+cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s) {
+    const size_t nb = (size_t)(w / 4) * (h / 4);
+    size_t grid = (nb + 255) / 256;
+    const size_t cap = (size_t)num_sms * 8;
+    if (grid > cap) grid = cap;
+    if (grid == 0) grid = 1;
+    bc7_encode_mode6_kernel<<<(unsigned)grid, 256, 0, s>>>(static_cast<const uint8_t*>(rgba), w, h,
+                                                          static_cast<uint4*>(blocks));
+    return cudaGetLastError();
+}
+
+}  // namespace ndgi

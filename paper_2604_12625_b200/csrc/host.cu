@@ -22,6 +22,7 @@ cudaError_t launch_fused_hmma(const KParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_fused_pipe(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
+cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s);
 cudaError_t uv_textures_build(const void* uv, int atlases, int tiles_x, int tiles_y, int C, cudaArray_t* arrays,
                               unsigned long long* texs);
 void uv_textures_free(int atlases, cudaArray_t* arrays, unsigned long long* texs);
@@ -525,6 +526,18 @@ ndgi_status ndgi_sample_lighting(ndgi_ctx* ctx, const int32_t* page_table, int32
     const cudaError_t e = ndgi::launch_sample(A, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "sample launch");
     return NDGI_OK;
+}
+
+ndgi_status ndgi_bc7_encode_mode6(const void* rgba, uint32_t w, uint32_t h, void* blocks, void* stream) {
+    if (!rgba || !blocks) return fail(NDGI_ERR_ARG, "NULL rgba or blocks");
+    if (w == 0 || h == 0 || w % 4 || h % 4) return fail(NDGI_ERR_ARG, "w and h must be positive multiples of 4");
+    if (w > (1u << 16) || h > (1u << 16)) return fail(NDGI_ERR_RANGE, "w or h > 65536");
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "device query");
+    e = ndgi::launch_bc7_encode_mode6(rgba, (int)w, (int)h, blocks, sms, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 encode launch");
 }
 
 ndgi_status ndgi_free(ndgi_ctx* ctx) {
