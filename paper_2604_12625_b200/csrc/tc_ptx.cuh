@@ -102,7 +102,19 @@ __device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
 
 // hot-loop wait without the poll counter: the whole loop is TRYWAIT + branch
 // (the CUTLASS-style wait); used where the issuing code is unconditional
+#ifndef NDGI_SPIN_HINT_NS
+#define NDGI_SPIN_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
+#if NDGI_SPIN_HINT_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "NDGI_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra NDGI_WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity), "n"(NDGI_SPIN_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "NDGI_WAIT_%=:\n\t"
@@ -110,6 +122,7 @@ __device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
         "@!p bra NDGI_WAIT_%=;\n\t}" ::"r"(bar),
         "r"(parity)
         : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
