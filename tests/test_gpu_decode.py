@@ -351,6 +351,36 @@ def test_c2_fullsize_sampled():
             assert mx <= FAST_MAX and mean <= FAST_MEAN
 
 
+def test_c2_bench_launch_all_texels_of_one_time():
+    """The exact launch bench.py times (config 2, decode_full_batch over the 24
+    times, RGBA8, the FULL8 kernel): every texel of one time against the
+    oracle's own RGBA8 quantisation (<= 1 level, R12), and 100 sampled texels of
+    each of the other 23 times."""
+    lay, seed = S.config("c2")
+    th = S.make_theta(lay, seed)
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    ts = [i / 24 for i in range(24)]
+    q = gpu_full(ctx, ts, "rgba8")                        # [24][1][4096][4096][4]
+    t_full = 13
+    exp = oracle.quantize_rgba8(M.decode_full(ts[t_full], NTHR).reshape(-1, 3)).reshape(q.shape[1:])
+    d = np.abs(q[t_full].astype(int) - exp.astype(int))
+    assert d.max() <= 1 and (d[..., 3] == 0).all()
+    assert (d[..., :3] == 0).mean() > 0.99
+    rng = np.random.default_rng(7)
+    C = 128
+    for ti, t in enumerate(ts):
+        if ti == t_full:
+            continue
+        for _ in range(100):
+            k = int(rng.integers(0, 1024))
+            i, j = (int(v) for v in rng.integers(0, C, 2))
+            tx, ty = k % 32, k // 32
+            e = oracle.quantize_rgba8(M.texel(k, i + 4, j + 4, t).reshape(1, 3))[0]
+            g = q[ti, 0, ty * C + j, tx * C + i]
+            assert np.abs(g.astype(int) - e.astype(int)).max() <= 1
+
+
 def test_host_buffer_path():
     lay, seed = S.config("c1")
     th = S.make_theta(lay, seed)
