@@ -76,6 +76,8 @@ def lib():
             "oracle_mlp_params": (C.c_size_t, [I]),
             "oracle_mean_at": (I, [P, P, I, D, P]),
             "oracle_bc7_encode_mode6": (None, [P, P]),
+            "oracle_train_grad": (D, [P, P, I, P, P, P, I, P]),
+            "oracle_adam": (None, [P, P, P, P, I, I, D, D, D, D]),
             "oracle_bc7_encode_image_mode6": (None, [P, I, I, P]),
             "oracle_restore": (D, [D, D, D]),
             "oracle_sample_lighting": (I, [P, P, I, I, I, I, I, D, D, I, D, P, P]),
@@ -179,6 +181,16 @@ class Model:
             raise ValueError("oracle_decode_tiles: tile id out of range")
         return out
 
+    def train_grad(self, k: int, theta: np.ndarray, uvt: np.ndarray, target: np.ndarray):
+        """R27: (loss, dloss/dtheta) of tile k's MLP (fp64 master theta) over samples uvt [S][3]."""
+        theta = np.ascontiguousarray(theta, np.float64)
+        uvt = np.ascontiguousarray(uvt, np.float64)
+        target = np.ascontiguousarray(target, np.float64)
+        g = np.zeros_like(theta)
+        loss = lib().oracle_train_grad(C.byref(self.L), C.byref(self.M), int(k), _ptr(theta), _ptr(uvt), _ptr(target),
+                                       len(uvt), _ptr(g))
+        return loss, g
+
     def decode_full(self, t: float, nthreads: int = 1) -> np.ndarray:
         L = self.lay
         C_ = L["core"]
@@ -279,3 +291,11 @@ def bc7_encode_image_mode6(rgba: np.ndarray) -> np.ndarray:
     out = np.zeros(((h // 4) * (w // 4), 16), np.uint8)
     lib().oracle_bc7_encode_image_mode6(_ptr(rgba), w, h, _ptr(out))
     return out
+
+
+def adam(theta, m, v, g, step: int, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8) -> None:
+    """In place, PyTorch's Adam order with bias correction (R27)."""
+    for a in (theta, m, v):
+        assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    g = np.ascontiguousarray(g, np.float64)
+    lib().oracle_adam(_ptr(theta), _ptr(m), _ptr(v), _ptr(g), len(theta), int(step), lr, b1, b2, eps)

@@ -781,3 +781,98 @@ void oracle_bc7_encode_image_mode6(const uint8_t *rgba, int w, int h, uint8_t *b
             oracle_bc7_encode_mode6(px, blocks + ((size_t)by * (w / 4) + bx) * 16);
         }
 }
+
+/* ------------------------------------------------------------------ */
+/* Fine-tuning step of G_Phi on frozen features (SURVEY.md §8(f) NEXT  */
+/* 4, the last stage of the paper's training: "In the final training   */
+/* stage, we freeze the feature maps and fine-tune the MLP under       */
+/* simulated quantization and BC compression" -- here the features are */
+/* the real quantized / BC7 maps -- "We use the Adam optimizer ... and  */
+/* use L2 loss", GELU on the hidden layers).  Reading R27: the   */
+/* loss of a tile is the mean over samples and RGB channels of the     */
+/* squared error; parameters are the fp64 master copy theta in the      */
+/* layout of the f16 MLP blob [W1 | b1 | W2 | b2 | W3 | b3]; Adam with  */
+/* bias correction, PyTorch's update order.                            */
+/* ------------------------------------------------------------------ */
+static double gelu_grad(double z, int variant)
+{
+    if (variant == OR_GELU_TANH) {
+        const double k = 0.7978845608028654, a = 0.044715;
+        const double u = k * (z + a * z * z * z), th = tanh(u);
+        return 0.5 * (1.0 + th) + 0.5 * z * (1.0 - th * th) * k * (1.0 + 3.0 * a * z * z);
+    }
+    return 0.5 * (1.0 + erf(z * 0.7071067811865476)) + z * exp(-0.5 * z * z) * 0.3989422804014327;
+}
+
+/* loss and dloss/dtheta of one tile k over S samples (u, v, t) with targets */
+double oracle_train_grad(const oracle_layout *L, const oracle_maps *M, int k, const double *theta, const double *uvt,
+                         const double *target, int S, double *grad)
+{
+    const int h = L->hidden, P = (int)oracle_mlp_params(h);
+    const double *W1 = theta, *b1 = W1 + 16 * h, *W2 = b1 + h, *b2 = W2 + h * h, *W3 = b2 + h, *b3 = W3 + 3 * h;
+    double *gW1 = grad, *gb1 = gW1 + 16 * h, *gW2 = gb1 + h, *gb2 = gW2 + h * h, *gW3 = gb2 + h, *gb3 = gW3 + 3 * h;
+    memset(grad, 0, sizeof(double) * P);
+    double loss = 0.0;
+    double x[16], z1[256], g1[256], z2[256], g2[256], y[3], dy[3], dg2[256], dz2[256], dg1[256], dz1[256];
+    for (int s = 0; s < S; ++s) {
+        oracle_features(L, M, k, uvt[3 * s], uvt[3 * s + 1], uvt[3 * s + 2], x);
+        for (int o = 0; o < h; ++o) {
+            double a = b1[o];
+            for (int i = 0; i < 16; ++i) a += W1[o * 16 + i] * x[i];
+            z1[o] = a;
+            g1[o] = oracle_gelu(a, L->gelu);
+        }
+        for (int o = 0; o < h; ++o) {
+            double a = b2[o];
+            for (int i = 0; i < h; ++i) a += W2[o * h + i] * g1[i];
+            z2[o] = a;
+            g2[o] = oracle_gelu(a, L->gelu);
+        }
+        for (int o = 0; o < 3; ++o) {
+            double a = b3[o];
+            for (int i = 0; i < h; ++i) a += W3[o * h + i] * g2[i];
+            y[o] = a;
+            const double d = y[o] - target[3 * s + o];
+            loss += d * d;
+            dy[o] = 2.0 * d / (3.0 * S);
+        }
+        for (int o = 0; o < 3; ++o) {
+            gb3[o] += dy[o];
+            for (int i = 0; i < h; ++i) gW3[o * h + i] += dy[o] * g2[i];
+        }
+        for (int i = 0; i < h; ++i) {
+            double a = 0.0;
+            for (int o = 0; o < 3; ++o) a += W3[o * h + i] * dy[o];
+            dg2[i] = a;
+            dz2[i] = a * gelu_grad(z2[i], L->gelu);
+        }
+        for (int o = 0; o < h; ++o) {
+            gb2[o] += dz2[o];
+            for (int i = 0; i < h; ++i) gW2[o * h + i] += dz2[o] * g1[i];
+        }
+        for (int i = 0; i < h; ++i) {
+            double a = 0.0;
+            for (int o = 0; o < h; ++o) a += W2[o * h + i] * dz2[o];
+            dg1[i] = a;
+            dz1[i] = a * gelu_grad(z1[i], L->gelu);
+        }
+        for (int o = 0; o < h; ++o) {
+            gb1[o] += dz1[o];
+            for (int i = 0; i < 16; ++i) gW1[o * 16 + i] += dz1[o] * x[i];
+        }
+    }
+    return loss / (3.0 * S);
+}
+
+/* one Adam step (PyTorch order): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+ * theta -= lr * (m / (1 - b1^step)) / (sqrt(v / (1 - b2^step)) + eps) */
+void oracle_adam(double *theta, double *m, double *v, const double *g, int P, int step, double lr, double b1,
+                 double b2, double eps)
+{
+    const double c1 = 1.0 - pow(b1, step), c2 = 1.0 - pow(b2, step);
+    for (int i = 0; i < P; ++i) {
+        m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+        v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+        theta[i] -= lr * (m[i] / c1) / (sqrt(v[i] / c2) + eps);
+    }
+}
