@@ -315,6 +315,37 @@ NDGI_API ndgi_status ndgi_sample_lighting(ndgi_ctx* ctx, const int32_t* page_tab
  * ------------------------------------------------------------------------ */
 NDGI_API ndgi_status ndgi_bc7_encode_mode6(const void* rgba, uint32_t w, uint32_t h, void* blocks, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Fine-tuning of the per-tile decoders: the paper's
+ * last training stage, "we freeze the feature maps and fine-tune the MLP
+ * under simulated quantization and BC compression" with Adam and an L2 loss
+ * (P:234); reading R27.  The features are the context's stored (quantized /
+ * BC7) maps sampled at (u, v, t) like the decode samples them; the trainer
+ * owns an fp32 master copy of every tile's MLP (initialised from the
+ * context's f16 weights) and the Adam state (beta 0.9 / 0.999, eps 1e-8,
+ * bias correction with each tile's own step count).  h = 16 only
+ * (UNSUPPORTED otherwise).  The context's own f16 weights and prepacked
+ * operands are not changed: export and create a new context to decode with
+ * the fine-tuned weights.
+ * ------------------------------------------------------------------------ */
+typedef struct ndgi_train ndgi_train;
+NDGI_API ndgi_status ndgi_train_create(ndgi_ctx* ctx, ndgi_train** out);
+/* One step for n tiles: DEVICE tile_ids u32[n], samples float[n][S][3]
+ * (u, v, t in [0,1]), targets float[n][S][3] (RGB); loss: DEVICE float[n]
+ * (mean squared error of each tile before the update) or NULL.  Tiles with
+ * an id >= num_tiles are skipped and counted (ndgi_device_error); a tile may
+ * appear once per step.  Errors: ARG, RANGE (n > 2^20, S > 2^24), CUDA. */
+NDGI_API ndgi_status ndgi_train_step(ndgi_train* tr, const uint32_t* tile_ids, uint32_t n, const float* samples,
+                                     const float* targets, uint32_t S, float lr, float* loss, void* stream);
+/* the last step's gradients (mean-loss gradient of each batch tile, before
+ * Adam) -> DEVICE float[n][P]; n <= that step's batch (RANGE otherwise) */
+NDGI_API ndgi_status ndgi_train_last_grad(ndgi_train* tr, float* out, uint32_t n, void* stream);
+/* fp32 master weights -> DEVICE float[num_tiles][P] (P = 595 for h = 16, blob order) */
+NDGI_API ndgi_status ndgi_train_weights(ndgi_train* tr, float* out, void* stream);
+/* master weights rounded to f16 -> DEVICE [num_tiles][P] (an ndgi_params.mlp buffer) */
+NDGI_API ndgi_status ndgi_train_export_f16(ndgi_train* tr, uint16_t* mlp, void* stream);
+NDGI_API ndgi_status ndgi_train_free(ndgi_train* tr);
+
 /* ---------------- test hooks (not the product path) ---------------- */
 
 /* Bit-exact BC7 map decode: blocks (DEVICE, (w/4)*(h/4) blocks row-major) ->

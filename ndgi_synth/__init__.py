@@ -318,3 +318,24 @@ def shading_uv(n: int, seed: int, coherent: bool = False, width: int = 1920, hei
     v = 0.2 + 0.5 * (ys.ravel() + 0.5) / height
     uv = np.stack([u, v], 1).astype(np.float32)
     return np.resize(uv, (n, 2))
+
+
+# ------------------------------------------------------------------ fine-tuning (NEXT 4)
+def train_batch(tiles, S: int, seed: int, n_times: int = 24):
+    """Seeded training samples for each tile: (u, v) at random texel centres of
+    a 128^2 core, t at one of n_times bake times (P:531 hourly bakes), and a
+    synthetic target lightmap value per sample: a smooth per-tile RGB field that
+    drifts with t (values in [0.1, 0.9]).  Returns float32 samples, targets [n][S][3]."""
+    tiles = np.asarray(tiles, np.int64)
+    n = len(tiles)
+    keys = _tile_keys(seed, 77, tiles)
+    w = splitmix64(keys[:, None] * np.uint64(0x100000001B3) + np.arange(3 * S, dtype=np.uint64)[None, :])
+    r = _unif(w).reshape(n, S, 3)
+    i = np.floor(r[..., 0] * 128)
+    j = np.floor(r[..., 1] * 128)
+    f = np.floor(r[..., 2] * n_times)
+    u, v, t = (i + 0.5) / 128, (j + 0.5) / 128, f / n_times
+    pw = _unif(splitmix64(keys[:, None] + np.arange(9, dtype=np.uint64)[None, :] * np.uint64(0x9E37)))   # [n][9]
+    tg = np.stack([0.5 + 0.4 * np.sin(2 * np.pi * ((0.5 + 2 * pw[:, None, c]) * u + (0.5 + 2 * pw[:, None, 3 + c]) * v
+                                                    + pw[:, None, 6 + c] + 0.5 * t)) for c in range(3)], -1)
+    return np.stack([u, v, t], -1).astype(np.float32), tg.astype(np.float32)

@@ -79,6 +79,12 @@ _SIGS = {
     "ndgi_vt_upload": (_I, [_P, _P, _P]),
     "ndgi_vt_stats": (_I, [_P, _P]),
     "ndgi_bc7_encode_mode6": (_I, [_P, _U32, _U32, _P, _P]),
+    "ndgi_train_create": (_I, [_P, C.POINTER(C.c_void_p)]),
+    "ndgi_train_step": (_I, [_P, _P, _U32, _P, _P, _U32, _F, _P, _P]),
+    "ndgi_train_weights": (_I, [_P, _P, _P]),
+    "ndgi_train_last_grad": (_I, [_P, _P, _U32, _P]),
+    "ndgi_train_export_f16": (_I, [_P, _P, _P]),
+    "ndgi_train_free": (_I, [_P]),
     "ndgi_sample_lighting": (_I, [_P, _P, C.c_int32, _P, _U32, _P, _P, _U32, _F, C.POINTER(ndgi_hdr), _P, _P]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -347,3 +353,46 @@ def ndgi_bc7_encode_mode6(rgba, blocks, stream=None) -> None:
     st = _lib.ndgi_bc7_encode_mode6(C.c_void_p(rgba.data_ptr()), w, h, C.c_void_p(blocks.data_ptr()),
                                     _stream_ptr(stream))
     _check(st, "ndgi_bc7_encode_mode6")
+
+
+# ---------------------------------------------------------------- fine-tuning (NEXT 4)
+class Trainer:
+    """ndgi_train: fp32 master weights + Adam state of every tile's MLP (R27)."""
+
+    def __init__(self, ctx: Context):
+        h = C.c_void_p()
+        _check(_lib.ndgi_train_create(ctx.handle, C.byref(h)), "ndgi_train_create")
+        self.handle, self.ctx = h, ctx
+        self.P = 16 * ctx.lay["hidden"] + ctx.lay["hidden"] * ctx.lay["hidden"] + 5 * ctx.lay["hidden"] + 3
+
+    def step(self, tile_ids, samples, targets, lr: float = 1e-3, loss=None, stream=None) -> None:
+        """tile_ids CUDA int32/uint32 [n]; samples, targets CUDA float32 [n][S][3]; loss CUDA float32 [n] or None."""
+        n, S = int(samples.shape[0]), int(samples.shape[1])
+        st = _lib.ndgi_train_step(self.handle, C.c_void_p(tile_ids.data_ptr()), n, C.c_void_p(samples.data_ptr()),
+                                  C.c_void_p(targets.data_ptr()), S, float(lr),
+                                  C.c_void_p(loss.data_ptr()) if loss is not None else None, _stream_ptr(stream))
+        _check(st, "ndgi_train_step")
+
+    def last_grad(self, out, stream=None) -> None:
+        """out: CUDA float32 [n][P] (n <= the last step's batch)."""
+        _check(_lib.ndgi_train_last_grad(self.handle, C.c_void_p(out.data_ptr()), int(out.shape[0]),
+                                         _stream_ptr(stream)), "ndgi_train_last_grad")
+
+    def weights(self, out, stream=None) -> None:
+        _check(_lib.ndgi_train_weights(self.handle, C.c_void_p(out.data_ptr()), _stream_ptr(stream)), "ndgi_train_weights")
+
+    def export_f16(self, mlp, stream=None) -> None:
+        _check(_lib.ndgi_train_export_f16(self.handle, C.c_void_p(mlp.data_ptr()), _stream_ptr(stream)),
+               "ndgi_train_export_f16")
+
+    def close(self) -> None:
+        lib = _lib
+        if getattr(self, "handle", None) and lib is not None:
+            lib.ndgi_train_free(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -23,6 +23,11 @@ cudaError_t launch_fused_pipe(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s);
+cudaError_t launch_train_grad(const TrainArgs& a, int H, cudaStream_t s);
+cudaError_t launch_adam(float* theta, float* m, float* v, int* steps, const float* grad, const uint32_t* tile_ids,
+                        int n, int P, int num_tiles, float lr, float b1, float b2, float eps, cudaStream_t s);
+cudaError_t launch_convert_f16_f32(const uint16_t* in, float* out, size_t n, cudaStream_t s);
+cudaError_t launch_convert_f32_f16(const float* in, uint16_t* out, size_t n, cudaStream_t s);
 cudaError_t uv_textures_build(const void* uv, int atlases, int tiles_x, int tiles_y, int C, cudaArray_t* arrays,
                               unsigned long long* texs);
 void uv_textures_free(int atlases, cudaArray_t* arrays, unsigned long long* texs);
@@ -538,6 +543,150 @@ ndgi_status ndgi_bc7_encode_mode6(const void* rgba, uint32_t w, uint32_t h, void
     if (e != cudaSuccess) return cuda_fail(e, "device query");
     e = ndgi::launch_bc7_encode_mode6(rgba, (int)w, (int)h, blocks, sms, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 encode launch");
+}
+
+// ---- fine-tuning ----------------------------------------
+struct ndgi_train {
+    ndgi_ctx* ctx;
+    int P;
+    float *theta, *m, *v, *grad, *loss;
+    int* steps;
+    uint32_t cap;   // batch capacity of grad / loss
+};
+
+ndgi_status ndgi_train_create(ndgi_ctx* ctx, ndgi_train** out) {
+    if (!ctx || !out) return fail(NDGI_ERR_ARG, "NULL ctx or out");
+    if (ctx->L.hidden != 16) return fail(NDGI_ERR_UNSUPPORTED, "fine-tuning is built for h = 16");
+    DeviceGuard g(ctx->device);
+    ndgi_train* t = new (std::nothrow) ndgi_train();
+    if (!t) return fail(NDGI_ERR_NOMEM, "host allocation");
+    t->ctx = ctx;
+    t->P = (int)mlp_elems(ctx->L.hidden);
+    const size_t n = (size_t)ctx->L.num_tiles * t->P;
+    cudaError_t e = cudaMalloc(&t->theta, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&t->m, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&t->v, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&t->steps, (size_t)ctx->L.num_tiles * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(t->m, 0, n * 4);
+    if (e == cudaSuccess) e = cudaMemset(t->v, 0, n * 4);
+    if (e == cudaSuccess) e = cudaMemset(t->steps, 0, (size_t)ctx->L.num_tiles * sizeof(int));
+    if (e == cudaSuccess) e = ndgi::launch_convert_f16_f32(ctx->P.mlp, t->theta, n, 0);   // fp32 master copy
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(t->theta);
+        cudaFree(t->m);
+        cudaFree(t->v);
+        cudaFree(t->steps);
+        delete t;
+        return cuda_fail(e, "ndgi_train_create");
+    }
+    *out = t;
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, const float* samples,
+                            const float* targets, uint32_t S, float lr, float* loss, void* stream) {
+    if (!t || !tile_ids || !samples || !targets) return fail(NDGI_ERR_ARG, "NULL argument");
+    if (n == 0 || S == 0) return fail(NDGI_ERR_ARG, "n == 0 or S == 0");
+    if (n > (1u << 20) || S > (1u << 24)) return fail(NDGI_ERR_RANGE, "n > 2^20 or S > 2^24");
+    if (!std::isfinite(lr) || lr < 0.0f) return fail(NDGI_ERR_ARG, "lr must be finite and >= 0");
+    ndgi_ctx* ctx = t->ctx;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSuccess;
+    if (n > t->cap) {
+        cudaFree(t->grad);
+        cudaFree(t->loss);
+        t->grad = nullptr;
+        t->loss = nullptr;
+        t->cap = 0;
+        e = cudaMalloc(&t->grad, (size_t)n * t->P * 4);
+        if (e == cudaSuccess) e = cudaMalloc(&t->loss, (size_t)n * 4);
+        if (e != cudaSuccess) return cuda_fail(e, "train scratch");
+        t->cap = n;
+    }
+    e = cudaMemsetAsync(t->grad, 0, (size_t)n * t->P * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(t->loss, 0, (size_t)n * 4, s);
+    if (e != cudaSuccess) return cuda_fail(e, "train scratch clear");
+    const ndgi_layout& L = ctx->L;
+    ndgi::TrainArgs a{};
+    a.uv = static_cast<const uint8_t*>(ctx->P.uv);
+    a.uvt = static_cast<const uint8_t*>(ctx->P.uvt);
+    a.ut = static_cast<const uint8_t*>(ctx->P.ut);
+    a.vt = static_cast<const uint8_t*>(ctx->P.vt);
+    a.uv_tile_bytes = map2d_bytes(L.fmt_uv, L.uv_res, L.uv_res, 4);
+    a.uvt_slice_bytes = map2d_bytes(L.fmt_uvt, L.uvt_res, L.uvt_res, 4);
+    a.uvt_tile_bytes = a.uvt_slice_bytes * L.uvt_depth;
+    a.line_tile_bytes = map2d_bytes(L.fmt_line, L.line_res, L.line_t, 2);
+    a.fmt_uv = (int)L.fmt_uv;
+    a.fmt_uvt = (int)L.fmt_uvt;
+    a.fmt_line = (int)L.fmt_line;
+    a.R_uv = (int)L.uv_res;
+    a.R3 = (int)L.uvt_res;
+    a.D = (int)L.uvt_depth;
+    a.U = (int)L.line_res;
+    a.T = (int)L.line_t;
+    a.gelu = (int)L.gelu;
+    a.num_tiles = (int)L.num_tiles;
+    a.tile_ids = tile_ids;
+    a.samples = samples;
+    a.targets = targets;
+    a.n = (int)n;
+    a.S = (int)S;
+    // enough CTAs for two waves at 128 threads, >= 128 samples per CTA
+    const uint32_t want = (2u * (uint32_t)ctx->num_sms * 8u + n - 1) / n;
+    const uint32_t maxc = S / 128 > 0 ? S / 128 : 1;
+    a.chunks = (int)(want < 1 ? 1 : (want > maxc ? maxc : want));
+    a.theta = t->theta;
+    a.grad = t->grad;
+    a.loss = t->loss;
+    a.err = ctx->d_err;
+    e = ndgi::launch_train_grad(a, (int)L.hidden, s);
+    if (e == cudaSuccess)
+        e = ndgi::launch_adam(t->theta, t->m, t->v, t->steps, t->grad, tile_ids, (int)n, t->P, (int)L.num_tiles, lr,
+                              0.9f, 0.999f, 1e-8f, s);
+    if (e == cudaSuccess && loss) e = cudaMemcpyAsync(loss, t->loss, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "train step");
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_train_last_grad(ndgi_train* t, float* out, uint32_t n, void* stream) {
+    if (!t || !out) return fail(NDGI_ERR_ARG, "NULL argument");
+    if (n == 0 || n > t->cap) return fail(NDGI_ERR_RANGE, "n must be in [1, the last step's batch]");
+    DeviceGuard g(t->ctx->device);
+    const cudaError_t e = cudaMemcpyAsync(out, t->grad, (size_t)n * t->P * 4, cudaMemcpyDeviceToDevice,
+                                          static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "train grad copy");
+}
+
+ndgi_status ndgi_train_weights(ndgi_train* t, float* out, void* stream) {
+    if (!t || !out) return fail(NDGI_ERR_ARG, "NULL argument");
+    DeviceGuard g(t->ctx->device);
+    const cudaError_t e = cudaMemcpyAsync(out, t->theta, (size_t)t->ctx->L.num_tiles * t->P * 4,
+                                          cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "train weights copy");
+}
+
+ndgi_status ndgi_train_export_f16(ndgi_train* t, uint16_t* mlp, void* stream) {
+    if (!t || !mlp) return fail(NDGI_ERR_ARG, "NULL argument");
+    DeviceGuard g(t->ctx->device);
+    const cudaError_t e = ndgi::launch_convert_f32_f16(t->theta, mlp, (size_t)t->ctx->L.num_tiles * t->P,
+                                                       static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "train export");
+}
+
+ndgi_status ndgi_train_free(ndgi_train* t) {
+    if (!t) return fail(NDGI_ERR_ARG, "NULL argument");
+    DeviceGuard g(t->ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(t->theta);
+    cudaFree(t->m);
+    cudaFree(t->v);
+    cudaFree(t->steps);
+    cudaFree(t->grad);
+    cudaFree(t->loss);
+    delete t;
+    return NDGI_OK;
 }
 
 ndgi_status ndgi_free(ndgi_ctx* ctx) {

@@ -77,6 +77,24 @@ struct SampleArgs {
     const float* mu;   // host [atlases][3], mu_hat at the call's t
 };
 
+// fine-tuning step (train_kernel.cu)
+struct TrainArgs {
+    // maps (as KParams)
+    const uint8_t *uv, *uvt, *ut, *vt;
+    size_t uv_tile_bytes, uvt_tile_bytes, uvt_slice_bytes, line_tile_bytes;
+    int fmt_uv, fmt_uvt, fmt_line, R_uv, R3, D, U, T, gelu, num_tiles;
+    // batch
+    const uint32_t* tile_ids;   // [n]
+    const float* samples;       // [n][S][3] (u, v, t)
+    const float* targets;       // [n][S][3]
+    int n, S, chunks;
+    // state
+    float* theta;               // [num_tiles][P] fp32 master weights
+    float* grad;                // [n][P] (zeroed by the host)
+    float* loss;                // [n] (zeroed by the host), mean squared error
+    uint32_t* err;
+};
+
 __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
 __device__ __forceinline__ float half_bits_to_float(uint16_t h) {

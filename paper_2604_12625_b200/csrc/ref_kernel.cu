@@ -12,51 +12,9 @@
 //   V_uv = S(F_uv; u, v), V_ut = S(F_ut; u, t), V_vt = S(F_vt; v, t)   R5
 //   x = [V_uvt, V_uv, V_ut, V_vt, gamma(t)]  R6
 //   y = W3 gelu(W2 gelu(W1 x + b1) + b2) + b3
-#include "bc7_device.cuh"
-#include "ndgi_common.cuh"
+#include "ref_common.cuh"
 
 namespace ndgi {
-
-struct Map2D {
-    const uint8_t* base;
-    int fmt, rx, ry, nc;
-};
-
-// all channels of texel (a, b), dequantised (R8)
-__device__ __forceinline__ void fetch_texel(const Map2D& m, int a, int b, float* out) {
-    if (m.fmt == FMT_BC7) {
-        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(m.base) + (b >> 2) * (m.rx >> 2) + (a >> 2));
-        const uint32_t v = bc7_texel(raw, 4 * (b & 3) + (a & 3));
-        for (int c = 0; c < m.nc; ++c) out[c] = (float)((v >> (8 * c)) & 0xffu) / 255.0f;
-    } else if (m.fmt == FMT_U8) {
-        const uint8_t* p = m.base + ((size_t)b * m.rx + a) * m.nc;
-        for (int c = 0; c < m.nc; ++c) out[c] = (float)p[c] / 255.0f;
-    } else {
-        const uint16_t* p = reinterpret_cast<const uint16_t*>(m.base) + ((size_t)b * m.rx + a) * m.nc;
-        for (int c = 0; c < m.nc; ++c) out[c] = half_bits_to_float(p[c]);
-    }
-}
-
-// texel-centre bilinear with clamp (R1)
-__device__ void bilinear(const Map2D& m, float a, float b, float* out) {
-    const float sx = a * (float)m.rx - 0.5f, sy = b * (float)m.ry - 0.5f;
-    const float fx0 = floorf(sx), fy0 = floorf(sy);
-    const float fx = sx - fx0, fy = sy - fy0;
-    const int x0 = clampi((int)fx0, 0, m.rx - 1), x1 = clampi((int)fx0 + 1, 0, m.rx - 1);
-    const int y0 = clampi((int)fy0, 0, m.ry - 1), y1 = clampi((int)fy0 + 1, 0, m.ry - 1);
-    float t00[4], t10[4], t01[4], t11[4];
-    fetch_texel(m, x0, y0, t00);
-    fetch_texel(m, x1, y0, t10);
-    fetch_texel(m, x0, y1, t01);
-    fetch_texel(m, x1, y1, t11);
-    const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
-    for (int c = 0; c < m.nc; ++c) out[c] = w00 * t00[c] + w10 * t10[c] + w01 * t01[c] + w11 * t11[c];
-}
-
-__device__ __forceinline__ float gelu_ref(float z, int variant) {
-    if (variant == GELU_TANH) return 0.5f * z * (1.0f + tanhf(0.7978845608028654f * (z + 0.044715f * z * z * z)));
-    return 0.5f * z * (1.0f + erff(z * 0.7071067811865476f));
-}
 
 __device__ void eval_texel(const KParams& p, const TConst& tc, int k, int i, int j, float* y) {
     const float u = ((float)i + 0.5f) / (float)p.C, v = ((float)j + 0.5f) / (float)p.C;

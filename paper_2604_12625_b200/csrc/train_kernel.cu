@@ -1,0 +1,239 @@
+// train_kernel.cu -- fine-tuning step of G_Phi on frozen features (SURVEY.md
+// §8(f) NEXT 4, the paper's last training stage: "we freeze the feature maps
+// and fine-tune the MLP under simulated quantization and BC compression",
+// "We use the Adam optimizer ... and use L2 loss"; reading R27).
+//
+// Many per-tile models in one launch (the paper batches its per-tile MLPs
+// with baddbmm): CTA = (tile of the batch, chunk of its samples), 128 threads,
+// one sample per thread per iteration.  Per sample, in fp32 on the CUDA cores:
+// the 16 features at (u, v, t) from the stored maps exactly as the reference
+// decode samples them (BC7 decoded per tap), forward through the tile's fp32
+// master MLP (weights in smem), squared error against the target, and the
+// backward pass; each gradient component is summed over the warp's 32 samples
+// with shuffles and added once per warp into the CTA's smem accumulator, which
+// goes to the global per-tile gradient with one atomic per component per CTA.
+// A second kernel applies Adam per tile (bias correction with the tile's own
+// step count).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ref_common.cuh"
+
+namespace ndgi {
+
+__device__ __forceinline__ float gelu_grad_ref(float z, int variant) {
+    if (variant == GELU_TANH) {
+        const float k = 0.7978845608028654f, a = 0.044715f;
+        const float th = tanhf(k * (z + a * z * z * z));
+        return 0.5f * (1.0f + th) + 0.5f * z * (1.0f - th * th) * k * (1.0f + 3.0f * a * z * z);
+    }
+    return 0.5f * (1.0f + erff(z * 0.7071067811865476f)) + z * expf(-0.5f * z * z) * 0.3989422804014327f;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int H>
+__global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_constant__ TrainArgs a) {
+    constexpr int P = 16 * H + H + H * H + H + 3 * H + 3;
+    __shared__ float sW[P];
+    __shared__ float sG[P];
+    __shared__ float sLoss;
+    const int r = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t k = __ldg(a.tile_ids + r);
+    if (k >= (uint32_t)a.num_tiles) {
+        if (chunk == 0 && tid == 0) atomicAdd(a.err, 1u);
+        return;   // uniform
+    }
+    for (int i = tid; i < P; i += blockDim.x) {
+        sW[i] = a.theta[(size_t)k * P + i];
+        sG[i] = 0.f;
+    }
+    if (tid == 0) sLoss = 0.f;
+    __syncthreads();
+    const float *W1 = sW, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
+    float *gW1 = sG, *gb1 = gW1 + 16 * H, *gW2 = gb1 + H, *gb2 = gW2 + H * H, *gW3 = gb2 + H, *gb3 = gW3 + 3 * H;
+
+    const int per = (a.S + a.chunks - 1) / a.chunks;
+    const int s0 = chunk * per, s1 = min(a.S, s0 + per);
+    const float inv = 2.0f / (3.0f * (float)a.S);
+    Map2D uvm{a.uv + a.uv_tile_bytes * k, a.fmt_uv, a.R_uv, a.R_uv, 4};
+    Map2D utm{a.ut + a.line_tile_bytes * k, a.fmt_line, a.U, a.T, 2};
+    Map2D vtm{a.vt + a.line_tile_bytes * k, a.fmt_line, a.U, a.T, 2};
+    const uint8_t* vol = a.uvt + a.uvt_tile_bytes * k;
+
+    // the warp iterates in lockstep (inactive lanes contribute zeros) so the
+    // shuffle reductions see all 32 lanes
+    for (int base = s0; base < s1; base += blockDim.x) {
+        const int s = base + tid;
+        const bool act = s < s1;
+        float x[16], z1[H], g1[H], z2[H], g2[H], dy[3];
+        float lossv = 0.f;
+        if (act) {
+            const float* q = a.samples + ((size_t)r * a.S + s) * 3;
+            const float u = q[0], v = q[1], t = q[2];
+            // V_uvt: tau-blend of two slices (R4), V_uv, V_ut, V_vt (R5), gamma (Eq. 4)
+            const float sd = t * (float)a.D - 0.5f, fl = floorf(sd), tau = sd - fl;
+            const int k0 = clampi((int)fl, 0, a.D - 1), k1 = clampi((int)fl + 1, 0, a.D - 1);
+            Map2D m0{vol + a.uvt_slice_bytes * k0, a.fmt_uvt, a.R3, a.R3, 4};
+            Map2D m1{vol + a.uvt_slice_bytes * k1, a.fmt_uvt, a.R3, a.R3, 4};
+            float p0[4], p1[4];
+            bilinear(m0, u, v, p0);
+            bilinear(m1, u, v, p1);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) x[c] = (1.0f - tau) * p0[c] + tau * p1[c];
+            bilinear(uvm, u, v, x + 4);
+            bilinear(utm, u, t, x + 8);
+            bilinear(vtm, v, t, x + 10);
+            x[12] = sinpif(t);
+            x[13] = cospif(t);
+            x[14] = sinpif(2.0f * t);
+            x[15] = cospif(2.0f * t);
+            // forward
+#pragma unroll
+            for (int o = 0; o < H; ++o) {
+                float acc = b1[o];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) acc = fmaf(W1[o * 16 + i], x[i], acc);
+                z1[o] = acc;
+                g1[o] = gelu_ref(acc, a.gelu);
+            }
+#pragma unroll
+            for (int o = 0; o < H; ++o) {
+                float acc = b2[o];
+#pragma unroll
+                for (int i = 0; i < H; ++i) acc = fmaf(W2[o * H + i], g1[i], acc);
+                z2[o] = acc;
+                g2[o] = gelu_ref(acc, a.gelu);
+            }
+            const float* tg = a.targets + ((size_t)r * a.S + s) * 3;
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                float acc = b3[o];
+#pragma unroll
+                for (int i = 0; i < H; ++i) acc = fmaf(W3[o * H + i], g2[i], acc);
+                const float d = acc - tg[o];
+                lossv = fmaf(d, d, lossv);
+                dy[o] = d * inv;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = 0.f;
+#pragma unroll
+            for (int o = 0; o < H; ++o) z1[o] = g1[o] = z2[o] = g2[o] = 0.f;
+            dy[0] = dy[1] = dy[2] = 0.f;
+        }
+        // backward, each gradient component summed over the warp
+        lossv = warp_sum(lossv);
+        if (lane == 0) atomicAdd(&sLoss, lossv);
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            const float sb = warp_sum(dy[o]);
+            if (lane == 0) atomicAdd(&gb3[o], sb);
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const float sw = warp_sum(dy[o] * g2[i]);
+                if (lane == 0) atomicAdd(&gW3[o * H + i], sw);
+            }
+        }
+        float dz2[H];
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            float acc = 0.f;
+#pragma unroll
+            for (int o = 0; o < 3; ++o) acc = fmaf(W3[o * H + i], dy[o], acc);
+            dz2[i] = act ? acc * gelu_grad_ref(z2[i], a.gelu) : 0.f;
+        }
+#pragma unroll
+        for (int o = 0; o < H; ++o) {
+            const float sb = warp_sum(dz2[o]);
+            if (lane == 0) atomicAdd(&gb2[o], sb);
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const float sw = warp_sum(dz2[o] * g1[i]);
+                if (lane == 0) atomicAdd(&gW2[o * H + i], sw);
+            }
+        }
+        float dz1[H];
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            float acc = 0.f;
+#pragma unroll
+            for (int o = 0; o < H; ++o) acc = fmaf(W2[o * H + i], dz2[o], acc);
+            dz1[i] = act ? acc * gelu_grad_ref(z1[i], a.gelu) : 0.f;
+        }
+#pragma unroll
+        for (int o = 0; o < H; ++o) {
+            const float sb = warp_sum(dz1[o]);
+            if (lane == 0) atomicAdd(&gb1[o], sb);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float sw = warp_sum(dz1[o] * x[i]);
+                if (lane == 0) atomicAdd(&gW1[o * 16 + i], sw);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < P; i += blockDim.x) atomicAdd(a.grad + (size_t)r * P + i, sG[i]);
+    if (tid == 0) atomicAdd(a.loss + r, sLoss / (3.0f * (float)a.S));
+}
+
+// Adam (PyTorch order, bias correction with the tile's own step count)
+__global__ void ndgi_adam_kernel(float* theta, float* m, float* v, int* steps, const float* grad,
+                                 const uint32_t* tile_ids, int n, int P, int num_tiles, float lr, float b1, float b2,
+                                 float eps) {
+    const int r = blockIdx.x;
+    const uint32_t k = __ldg(tile_ids + r);
+    if (k >= (uint32_t)num_tiles) return;
+    const int step = steps[k] + 1;
+    const float c1 = 1.0f - powf(b1, (float)step), c2 = 1.0f - powf(b2, (float)step);
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const size_t e = (size_t)k * P + i;
+        const float g = grad[(size_t)r * P + i];
+        const float mi = b1 * m[e] + (1.0f - b1) * g;
+        const float vi = b2 * v[e] + (1.0f - b2) * g * g;
+        m[e] = mi;
+        v[e] = vi;
+        theta[e] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) steps[k] = step;
+}
+
+__global__ void ndgi_f16_to_f32_kernel(const uint16_t* in, float* out, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = half_bits_to_float(in[i]);
+}
+__global__ void ndgi_f32_to_f16_kernel(const float* in, uint16_t* out, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = __half_as_ushort(__float2half_rn(in[i]));
+}
+
+cudaError_t launch_train_grad(const TrainArgs& a, int H, cudaStream_t s) {
+    const unsigned grid = (unsigned)(a.n * a.chunks);
+    if (H != 16) return cudaErrorNotSupported;   // h = 64 would spill its activations (future: tensor cores)
+    ndgi_train_grad_kernel<16><<<grid, 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam(float* theta, float* m, float* v, int* steps, const float* grad, const uint32_t* tile_ids,
+                        int n, int P, int num_tiles, float lr, float b1, float b2, float eps, cudaStream_t s) {
+    ndgi_adam_kernel<<<n, 256, 0, s>>>(theta, m, v, steps, grad, tile_ids, n, P, num_tiles, lr, b1, b2, eps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_convert_f16_f32(const uint16_t* in, float* out, size_t n, cudaStream_t s) {
+    ndgi_f16_to_f32_kernel<<<1024, 256, 0, s>>>(in, out, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_convert_f32_f16(const float* in, uint16_t* out, size_t n, cudaStream_t s) {
+    ndgi_f32_to_f16_kernel<<<1024, 256, 0, s>>>(in, out, n);
+    return cudaGetLastError();
+}
+
+}  // namespace ndgi
