@@ -347,12 +347,18 @@ def run_gpu(args, rank, world, dist):
             encode = encode_leg(ndgi, torch, args)
         except Exception as exc:  # pragma: no cover
             encode = {"error": repr(exc)}
+    finetune = None
+    if not args.no_finetune and world == 1:
+        try:
+            finetune = finetune_leg(ndgi, torch, args)
+        except Exception as exc:  # pragma: no cover
+            finetune = {"error": repr(exc)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank, args.workload),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
-        "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading, "texunit": texunit, "bc7_encode": encode,
+        "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading, "texunit": texunit, "bc7_encode": encode, "finetune": finetune,
         "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
     }
     print(json.dumps(line), flush=True)
@@ -498,6 +504,42 @@ def encode_leg(ndgi, torch, args):
                     "frac": 5 * h * w / s_ / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes_per_texel": 5}}
 
 
+def finetune_leg(ndgi, torch, args):
+    """SURVEY §8(f) NEXT 4, measured: one fine-tuning step (R27) of all 1,024
+    per-tile decoders of config 2, 4,096 samples per tile (the paper's batch of
+    2^12): features from the BC7 maps, forward + backward + Adam.
+    samples/s, and the fraction of the fp32 FMA peak its MLP arithmetic
+    (3 x the forward MACs per sample) would need."""
+    lay, seed = S.config("c2")
+    th = ndgi.upload_theta(S.make_theta(lay, seed))
+    ctx = ndgi.ndgi_load(lay, th, torch.cuda.current_device())
+    tr = ndgi.Trainer(ctx)
+    tiles = list(range(lay["num_tiles"]))
+    Sn = 4096
+    smp, tgt = S.train_batch(tiles, Sn, 12)
+    ids = torch.tensor(tiles, dtype=torch.int32, device="cuda")
+    smp_t, tgt_t = torch.from_numpy(smp).cuda(), torch.from_numpy(tgt).cuda()
+    stream = torch.cuda.current_stream()
+    for _ in range(2):
+        tr.step(ids, smp_t, tgt_t, 1e-3, None, stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record(stream)
+    for _ in range(reps):
+        tr.step(ids, smp_t, tgt_t, 1e-3, None, stream)
+    e1.record(stream)
+    e1.synchronize()
+    s_ = e0.elapsed_time(e1) / reps * 1e-3
+    n = len(tiles) * Sn
+    h = lay["hidden"]
+    flops = n * 3 * 2 * (16 * h + h * h + 3 * h)
+    fma_peak = 148 * 128 * 2 * _peaks().get("sm_max_mhz", 1965.0) * 1e6 / 1e12   # TFLOP/s fp32 (nominal)
+    tr.close()
+    return {"workload": "1024 tiles x 4096 samples (c2, BC7 features), forward + backward + Adam, h = 16",
+            "ms_per_step": s_ * 1e3, "msample_s": n / s_ / 1e6,
+            "mlp_tflops": flops / s_ / 1e12, "fp32_peak_tflops": fma_peak, "frac": flops / s_ / 1e12 / fma_peak}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -509,6 +551,7 @@ def main():
     ap.add_argument("--no-shading", action="store_true", help="skip the shading-side (NEXT 1) leg")
     ap.add_argument("--no-texunit", action="store_true", help="skip the texture-unit F_uv comparator (NEXT 2)")
     ap.add_argument("--no-encode", action="store_true", help="skip the BC7 encoder leg (NEXT 3)")
+    ap.add_argument("--no-finetune", action="store_true", help="skip the fine-tuning leg (NEXT 4)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
                     help="c2: 1,024 tiles per GPU (weak scaling, default); c4: the 16,384-tile scene sharded (strong)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
