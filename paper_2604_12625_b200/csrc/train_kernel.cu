@@ -37,14 +37,22 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Gradient sums without per-component warp reductions: per warp iteration the
+// 32 samples' activation vectors are staged in smem (row = sample), and each
+// lane owns fixed gradient components (8 consecutive inputs of one output of
+// W1 and of W2, 2 of W3, one bias of each layer), accumulated in registers over
+// all of the CTA's samples; one smem atomic per component per warp at the end.
 template <int H>
 __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_constant__ TrainArgs a) {
+    static_assert(H == 16, "lane-owned gradient components are laid out for h = 16");
     constexpr int P = 16 * H + H + H * H + H + 3 * H + 3;
     __shared__ float sW[P];
     __shared__ float sG[P];
     __shared__ float sLoss;
+    __shared__ __align__(16) float sA[4][32][16];   // per warp: the "output" vector of each sample
+    __shared__ __align__(16) float sB[4][32][16];   // per warp: the "input" vector of each sample
     const int r = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t k = __ldg(a.tile_ids + r);
     if (k >= (uint32_t)a.num_tiles) {
         if (chunk == 0 && tid == 0) atomicAdd(a.err, 1u);
@@ -67,8 +75,17 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
     Map2D vtm{a.vt + a.line_tile_bytes * k, a.fmt_line, a.U, a.T, 2};
     const uint8_t* vol = a.uvt + a.uvt_tile_bytes * k;
 
-    // the warp iterates in lockstep (inactive lanes contribute zeros) so the
-    // shuffle reductions see all 32 lanes
+    // lane-owned components: W1/W2 output o = lane / 2, inputs i0 .. i0 + 7;
+    // W3 (lanes < 24) output lane / 8, inputs 2 (lane % 8), +1; biases b1/b2 (lanes < 16), b3 (lanes < 3)
+    const int oo = lane >> 1, i0 = (lane & 1) * 8;
+    const int o3 = lane >> 3, i3 = (lane & 7) * 2;
+    float acc1[8], acc2[8], acc3[2] = {0.f, 0.f}, accb1 = 0.f, accb2 = 0.f, accb3 = 0.f, accl = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc1[q] = acc2[q] = 0.f;
+    float(*A)[16] = sA[warp];
+    float(*Bv)[16] = sB[warp];
+
+    // lanes outside [s0, s1) stage zero vectors, so every iteration sums 32 rows
     for (int base = s0; base < s1; base += blockDim.x) {
         const int s = base + tid;
         const bool act = s < s1;
@@ -128,20 +145,9 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
             for (int o = 0; o < H; ++o) z1[o] = g1[o] = z2[o] = g2[o] = 0.f;
             dy[0] = dy[1] = dy[2] = 0.f;
         }
-        // backward, each gradient component summed over the warp
-        lossv = warp_sum(lossv);
-        if (lane == 0) atomicAdd(&sLoss, lossv);
-#pragma unroll
-        for (int o = 0; o < 3; ++o) {
-            const float sb = warp_sum(dy[o]);
-            if (lane == 0) atomicAdd(&gb3[o], sb);
-#pragma unroll
-            for (int i = 0; i < H; ++i) {
-                const float sw = warp_sum(dy[o] * g2[i]);
-                if (lane == 0) atomicAdd(&gW3[o * H + i], sw);
-            }
-        }
-        float dz2[H];
+        accl += lossv;
+        // backward: dz2, dz1 per sample (registers)
+        float dz2[H], dz1[H];
 #pragma unroll
         for (int i = 0; i < H; ++i) {
             float acc = 0.f;
@@ -150,34 +156,87 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
             dz2[i] = act ? acc * gelu_grad_ref(z2[i], a.gelu) : 0.f;
         }
 #pragma unroll
-        for (int o = 0; o < H; ++o) {
-            const float sb = warp_sum(dz2[o]);
-            if (lane == 0) atomicAdd(&gb2[o], sb);
-#pragma unroll
-            for (int i = 0; i < H; ++i) {
-                const float sw = warp_sum(dz2[o] * g1[i]);
-                if (lane == 0) atomicAdd(&gW2[o * H + i], sw);
-            }
-        }
-        float dz1[H];
-#pragma unroll
         for (int i = 0; i < H; ++i) {
             float acc = 0.f;
 #pragma unroll
             for (int o = 0; o < H; ++o) acc = fmaf(W2[o * H + i], dz2[o], acc);
             dz1[i] = act ? acc * gelu_grad_ref(z1[i], a.gelu) : 0.f;
         }
+        // sum over the warp's 32 samples: stage (A, B) = (output-side, input-side)
+        // vectors of each layer and let every lane sweep the rows for its components
+        auto stage = [&](const float* va, int na, const float* vb) {
+            __syncwarp();
 #pragma unroll
-        for (int o = 0; o < H; ++o) {
-            const float sb = warp_sum(dz1[o]);
-            if (lane == 0) atomicAdd(&gb1[o], sb);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float sw = warp_sum(dz1[o] * x[i]);
-                if (lane == 0) atomicAdd(&gW1[o * 16 + i], sw);
+            for (int q = 0; q < 16; q += 4) {
+                *reinterpret_cast<float4*>(&A[lane][q]) =
+                    make_float4(q < na ? va[q] : 0.f, q + 1 < na ? va[q + 1] : 0.f, q + 2 < na ? va[q + 2] : 0.f,
+                                q + 3 < na ? va[q + 3] : 0.f);
+                *reinterpret_cast<float4*>(&Bv[lane][q]) = make_float4(vb[q], vb[q + 1], vb[q + 2], vb[q + 3]);
             }
+            __syncwarp();
+        };
+        // layer 3: dW3 = dy g2^T, db3 = dy
+        stage(dy, 3, g2);
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+            const float ad = A[j][o3 < 3 ? o3 : 0];
+            const float2 bb = *reinterpret_cast<const float2*>(&Bv[j][i3]);
+            acc3[0] = fmaf(ad, bb.x, acc3[0]);
+            acc3[1] = fmaf(ad, bb.y, acc3[1]);
+            accb3 += A[j][lane < 3 ? lane : 0];
+        }
+        // layer 2: dW2 = dz2 g1^T, db2 = dz2
+        stage(dz2, 16, g1);
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+            const float ad = A[j][oo];
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bv[j][i0]);
+            const float4 b1v = *reinterpret_cast<const float4*>(&Bv[j][i0 + 4]);
+            acc2[0] = fmaf(ad, b0.x, acc2[0]);
+            acc2[1] = fmaf(ad, b0.y, acc2[1]);
+            acc2[2] = fmaf(ad, b0.z, acc2[2]);
+            acc2[3] = fmaf(ad, b0.w, acc2[3]);
+            acc2[4] = fmaf(ad, b1v.x, acc2[4]);
+            acc2[5] = fmaf(ad, b1v.y, acc2[5]);
+            acc2[6] = fmaf(ad, b1v.z, acc2[6]);
+            acc2[7] = fmaf(ad, b1v.w, acc2[7]);
+            accb2 += A[j][lane & 15];
+        }
+        // layer 1: dW1 = dz1 x^T, db1 = dz1
+        stage(dz1, 16, x);
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+            const float ad = A[j][oo];
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bv[j][i0]);
+            const float4 b1v = *reinterpret_cast<const float4*>(&Bv[j][i0 + 4]);
+            acc1[0] = fmaf(ad, b0.x, acc1[0]);
+            acc1[1] = fmaf(ad, b0.y, acc1[1]);
+            acc1[2] = fmaf(ad, b0.z, acc1[2]);
+            acc1[3] = fmaf(ad, b0.w, acc1[3]);
+            acc1[4] = fmaf(ad, b1v.x, acc1[4]);
+            acc1[5] = fmaf(ad, b1v.y, acc1[5]);
+            acc1[6] = fmaf(ad, b1v.z, acc1[6]);
+            acc1[7] = fmaf(ad, b1v.w, acc1[7]);
+            accb1 += A[j][lane & 15];
         }
     }
+    // this warp's sums -> the CTA accumulator -> the tile's gradient
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        atomicAdd(&gW1[oo * 16 + i0 + q], acc1[q]);
+        atomicAdd(&gW2[oo * H + i0 + q], acc2[q]);
+    }
+    if (lane < 24) {
+        atomicAdd(&gW3[o3 * H + i3], acc3[0]);
+        atomicAdd(&gW3[o3 * H + i3 + 1], acc3[1]);
+    }
+    if (lane < 16) {
+        atomicAdd(&gb1[lane], accb1);
+        atomicAdd(&gb2[lane], accb2);
+    }
+    if (lane < 3) atomicAdd(&gb3[lane], accb3);
+    accl = warp_sum(accl);
+    if (lane == 0) atomicAdd(&sLoss, accl);
     __syncthreads();
     for (int i = tid; i < P; i += blockDim.x) atomicAdd(a.grad + (size_t)r * P + i, sG[i]);
     if (tid == 0) atomicAdd(a.loss + r, sLoss / (3.0f * (float)a.S));
