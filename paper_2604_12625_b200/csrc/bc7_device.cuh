@@ -265,9 +265,29 @@ __device__ __forceinline__ void bc7_decode(uint4 raw, Sink&& sink) {
         bc7_decode_generic(raw, sink);
 }
 
-// Single-texel decode (texel = 4*row + col), generic path; used by the
-// scalar fp32 reference kernel.
+// Single texel of a mode-6 block: RGBA 7-bit endpoints at bits 7..62, p-bits
+// at 63 and 64, texel 0's 3-bit index at 65, texel i's 4-bit index at 64 + 4i.
+__device__ __forceinline__ uint32_t bc7_texel_mode6(uint4 raw, int texel) {
+    const uint64_t lo = (uint64_t)raw.x | ((uint64_t)raw.y << 32);
+    const uint64_t hi = (uint64_t)raw.z | ((uint64_t)raw.w << 32);
+    const uint32_t p0 = (uint32_t)(lo >> 63), p1 = (uint32_t)hi & 1u;
+    const uint32_t idx = texel == 0 ? (uint32_t)(hi >> 1) & 7u : (uint32_t)(hi >> (4 * texel)) & 15u;
+    const uint32_t w = (uint32_t)((idx < 8u ? kW4lo : kW4hi) >> (8u * (idx & 7u))) & 0xffu;
+    uint32_t v = 0u;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t e0 = ((uint32_t)(lo >> (7 + 14 * c)) & 127u) << 1 | p0;
+        const uint32_t e1 = ((uint32_t)(lo >> (14 + 14 * c)) & 127u) << 1 | p1;
+        v |= (((64u - w) * e0 + w * e1 + 32u) >> 6) << (8 * c);
+    }
+    return v;
+}
+
+// Single-texel decode (texel = 4*row + col): the mode-6 path for mode-6 blocks,
+// else the generic decoder; used by the scalar fp32 reference and fine-tuning
+// kernels.
 __device__ __forceinline__ uint32_t bc7_texel(uint4 raw, int texel) {
+    if (bc7_is_mode6(raw)) return bc7_texel_mode6(raw, texel);
     uint32_t v = 0u;
     bc7_decode_generic(raw, [&](int i, uint32_t rgba) { if (i == texel) v = rgba; });
     return v;
