@@ -22,6 +22,17 @@
 
 namespace ndgi {
 
+// GELU'(z) from z and g = GELU(z) without a second erf/tanh: Phi(z) = g / z
+// (erf form; 1/2 at z = 0), tanh(u) = 2 g / z - 1 (tanh form)
+__device__ __forceinline__ float gelu_grad_from(float z, float g, int variant) {
+    const float r = z != 0.0f ? __fdividef(g, z) : 0.5f;
+    if (variant == GELU_TANH) {
+        const float k = 0.7978845608028654f, a = 0.044715f, th = 2.0f * r - 1.0f;
+        return r + 0.5f * z * (1.0f - th * th) * k * (1.0f + 3.0f * a * z * z);
+    }
+    return r + z * __expf(-0.5f * z * z) * 0.3989422804014327f;
+}
+
 __device__ __forceinline__ float gelu_grad_ref(float z, int variant) {
     if (variant == GELU_TANH) {
         const float k = 0.7978845608028654f, a = 0.044715f;
@@ -153,14 +164,14 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
             float acc = 0.f;
 #pragma unroll
             for (int o = 0; o < 3; ++o) acc = fmaf(W3[o * H + i], dy[o], acc);
-            dz2[i] = act ? acc * gelu_grad_ref(z2[i], a.gelu) : 0.f;
+            dz2[i] = act ? acc * gelu_grad_from(z2[i], g2[i], a.gelu) : 0.f;
         }
 #pragma unroll
         for (int i = 0; i < H; ++i) {
             float acc = 0.f;
 #pragma unroll
             for (int o = 0; o < H; ++o) acc = fmaf(W2[o * H + i], dz2[o], acc);
-            dz1[i] = act ? acc * gelu_grad_ref(z1[i], a.gelu) : 0.f;
+            dz1[i] = act ? acc * gelu_grad_from(z1[i], g1[i], a.gelu) : 0.f;
         }
         // sum over the warp's 32 samples: stage (A, B) = (output-side, input-side)
         // vectors of each layer and let every lane sweep the rows for its components
