@@ -244,6 +244,31 @@ def run_gpu(args, rank, world, dist):
     texels_per_step = per_t * N_T * world
     value = texels_per_step / (ms_per_step * 1e-3) / 1e9
 
+    # ---------------- SURVEY §8(e) verification of a sharded run (off the timed path):
+    # the first and last local tile of every rank at t_0 gathered to all ranks
+    # (NCCL all_gather) and compared on rank 0 with the oracle's own decode
+    verify = None
+    if dist is not None:
+        try:
+            Cc = lay["core"]
+            n_loc = lay["num_tiles"]
+            img = out[0].view(lay["tiles_y"], Cc, lay["tiles_x"], Cc, 4)
+            tiles = img.permute(0, 2, 1, 3, 4).reshape(n_loc, Cc, Cc, 4)
+            sid, stl = par.gather_tile_sample(global_ids, tiles, [0, n_loc - 1], dist, "cuda")
+            if rank == 0:
+                import oracle
+                th_s = S.make_theta(lay0, seed, tiles=sid)
+                sub = dict(lay0, num_tiles=len(sid), atlases=1, tiles_x=len(sid), tiles_y=1)
+                y = oracle.Model(sub, th_s).decode_tiles(list(range(len(sid))), TS[0],
+                                                         nthreads=len(os.sched_getaffinity(0)))
+                B_ = lay0["border"]
+                ref = oracle.quantize_rgba8(np.ascontiguousarray(y[:, B_:B_ + Cc, B_:B_ + Cc]))
+                dmax = int(np.abs(ref.astype(int) - stl.astype(int)).max())
+                verify = {"tiles": [int(g) for g in sid], "t": TS[0], "max_rgba8_level_diff_vs_oracle": dmax,
+                          "ok": dmax <= 1, "how": "NCCL all_gather of 2 decoded tiles per rank, fp64 C oracle"}
+        except Exception as exc:  # pragma: no cover - reported, not hidden
+            verify = {"ok": False, "error": repr(exc)}
+
     # ---------------- end-to-end through the host-buffer API (Theta H2D + decode + D2H)
     e2e = None
     try:
@@ -359,6 +384,7 @@ def run_gpu(args, rank, world, dist):
         "vs_baseline": None, "dtype": "f16", "data": "synthetic", "config": _workload_config(world, tiles_per_rank, args.workload),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clk.summary(), "vt_batch_us": vt, "shading": shading, "texunit": texunit, "bc7_encode": encode, "finetune": finetune,
+        "verify": verify,
         "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
     }
     print(json.dumps(line), flush=True)

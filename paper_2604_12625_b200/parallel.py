@@ -76,3 +76,19 @@ def gather_digests(local_ids: np.ndarray, local_digests, num_tiles: int, dist, d
     if not seen.all():
         raise RuntimeError("some tiles were not decoded by any rank")
     return out
+
+
+def gather_tile_sample(local_ids: np.ndarray, local_tiles, pick: list[int], dist, device=None):
+    """SURVEY §8(e) verification: every rank contributes the decoded tiles at
+    local positions `pick` (same count on every rank) with their global ids;
+    all ranks receive them (all_gather) -> (global ids [world * len(pick)],
+    tiles [world * len(pick)][...]) as numpy arrays."""
+    import torch
+    world = dist.get_world_size()
+    ids = torch.as_tensor(np.asarray(local_ids)[pick], dtype=torch.int64, device=device)
+    tl = local_tiles[pick].contiguous().to(device)
+    all_ids = [torch.empty_like(ids) for _ in range(world)]
+    all_tl = [torch.empty_like(tl) for _ in range(world)]
+    dist.all_gather(all_ids, ids)
+    dist.all_gather(all_tl, tl)
+    return torch.cat(all_ids).cpu().numpy(), torch.cat(all_tl).cpu().numpy()

@@ -54,9 +54,10 @@ def _worker(rank, world, port, out):
     q = torch.from_numpy(oracle.quantize_rgba8(y))
     dg = par.tile_digests(q)
     full = par.gather_digests(mine, dg, lay["num_tiles"], dist)
+    sid, stl = par.gather_tile_sample(mine, q, [0, len(mine) - 1], dist)
     t = par.max_over_ranks(1.5 + rank, dist)
     if rank == 0:
-        out.put((full.tolist(), t))
+        out.put((full.tolist(), t, sid.tolist(), stl))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -70,7 +71,7 @@ def test_sharded_digests_match_single_process():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    full, t = q.get(timeout=120)
+    full, t, sid, stl = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -78,8 +79,13 @@ def test_sharded_digests_match_single_process():
     lay = S.layout(1, 5, 1, "M", core=8, border=2, uvt_res=4, uvt_depth=2, line_res=4, line_t=3, hidden=4)
     th = S.make_theta(lay, 77, "mixed")
     y = oracle.Model(lay, th).decode_tiles(np.arange(5), 0.4)
-    ref = par.tile_digests(torch.from_numpy(oracle.quantize_rgba8(y))).numpy()
+    q8 = oracle.quantize_rgba8(y)
+    ref = par.tile_digests(torch.from_numpy(q8)).numpy()
     np.testing.assert_array_equal(np.array(full), ref)
+    # the verification sample: first and last tile of each rank, with global ids
+    assert sid == [0, 4, 1, 3]
+    for g, tile in zip(sid, stl):
+        np.testing.assert_array_equal(tile, q8[g])
 
 
 def test_digest_detects_single_byte_change():
