@@ -65,8 +65,11 @@ __device__ int g_ndgi_res[256];   // resident CTAs per SM (profiling builds only
 // no format switch, row pointers instead of 64-bit index arithmetic
 // WIN: F_uvt staged per chunk in per-warp windows instead of the whole slice
 // (large R3: the H profile's 32 KB slice would halve residency)
-template <int H, int FMT_UV, int CT, bool FULL8, bool WIN>
+// OUTK: 0 any format / addressing, 1 (FULL8) decode_full RGBA8, 2 (TILES8)
+// decode_tiles RGBA8 (core + mirrored border with 32-bit offsets from the slot)
+template <int H, int FMT_UV, int CT, int OUTK, bool WIN>
 __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_kernel(const __grid_constant__ KParams p) {
+    constexpr bool FULL8 = OUTK == 1, TILES8 = OUTK == 2;
     using Cfg = FusedCfg<H>;
     constexpr int S = Cfg::SLOTS;
     constexpr int C = CT;                       // core texels per tile side (128 or 256)
@@ -463,6 +466,22 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 orow[(size_t)((uint32_t)(j - j_begin) * rp32) + blk * kThreads] = rgba8_fma(y0f, y1f, y2f);
                 return;
             }
+            if constexpr (TILES8) {
+                // slot-relative 32-bit offsets; mirrored copies (R3): core i -> -i, 2(C-1)-i
+                const uint32_t v = rgba8_fma(y0f, y1f, y2f);
+                uint32_t* const tb = reinterpret_cast<uint32_t*>(p.out) + out_base;
+                const int P_ = (int)rp32;
+                tb[j * P_ + i] = v;
+                const bool bx = B > 0 && ((i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2));
+                const int xm = i <= B ? -i : 2 * (C - 1) - i;
+                if (bx) tb[j * P_ + xm] = v;
+                if (B > 0 && ((j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2))) {   // CTA-uniform
+                    const int ym = j <= B ? -j : 2 * (C - 1) - j;
+                    tb[ym * P_ + i] = v;
+                    if (bx) tb[ym * P_ + xm] = v;
+                }
+                return;
+            }
             const size_t o = out_base + (size_t)j * row_pitch + i;
             if (out_fmt == OUT_RGBA8) {
                 const uint32_t v = rgba8_fma(y0f, y1f, y2f);
@@ -635,12 +654,18 @@ static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s)
     const bool win = kWinOk && p.R3 > 32;
     uint32_t smem = L.total;
     if (win) smem = L.uvt + 4u * uvt_window(p.R3, CT, kChunkTexels / CT).bytes;
-    auto pick = [&](auto f8, auto w) {
-        return ndgi_fused_kernel<H, FMT_UV, CT, decltype(f8)::value, decltype(w)::value && kWinOk>;
+    const bool tiles8 = !p.full && p.out_fmt == OUT_RGBA8;
+    auto pick = [&](auto ok, auto w) {
+        return ndgi_fused_kernel<H, FMT_UV, CT, decltype(ok)::value, decltype(w)::value && kWinOk>;
     };
+    using K0 = std::integral_constant<int, 0>;
+    using K1 = std::integral_constant<int, 1>;
+    using K2 = std::integral_constant<int, 2>;
     using T_ = std::true_type;
     using F_ = std::false_type;
-    auto kern = full8 ? (win ? pick(T_{}, T_{}) : pick(T_{}, F_{})) : (win ? pick(F_{}, T_{}) : pick(F_{}, F_{}));
+    auto kern = full8 ? (win ? pick(K1{}, T_{}) : pick(K1{}, F_{}))
+                      : tiles8 ? (win ? pick(K2{}, T_{}) : pick(K2{}, F_{}))
+                               : (win ? pick(K0{}, T_{}) : pick(K0{}, F_{}));
     int occ = 0;
     cudaError_t e = fused_launch_cfg(kern, smem, FusedCfg<H>::TM_COLS, occ);
     if (e != cudaSuccess) return e;
