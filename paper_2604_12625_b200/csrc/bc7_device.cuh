@@ -286,11 +286,18 @@ __device__ __forceinline__ uint32_t bc7_texel_mode6(uint4 raw, int texel) {
 // Single-texel decode (texel = 4*row + col): the mode-6 path for mode-6 blocks,
 // else the generic decoder; used by the scalar fp32 reference and fine-tuning
 // kernels.
-__device__ __forceinline__ uint32_t bc7_texel(uint4 raw, int texel) {
-    if (bc7_is_mode6(raw)) return bc7_texel_mode6(raw, texel);
+// the all-mode decoder as an out-of-line call: inlined at every tap of a
+// bilinear/trilinear sampler it would multiply the code size (instruction-cache
+// misses), and mode-6 payloads never reach it
+static __device__ __noinline__ uint32_t bc7_texel_generic(uint4 raw, int texel) {
     uint32_t v = 0u;
     bc7_decode_generic(raw, [&](int i, uint32_t rgba) { if (i == texel) v = rgba; });
     return v;
+}
+
+__device__ __forceinline__ uint32_t bc7_texel(uint4 raw, int texel) {
+    if (bc7_is_mode6(raw)) return bc7_texel_mode6(raw, texel);
+    return bc7_texel_generic(raw, texel);
 }
 
 }  // namespace ndgi
