@@ -656,6 +656,13 @@ int oracle_sample_lighting(const uint8_t *cache, const int32_t *pt, int C, int B
 /* ------------------------------------------------------------------ */
 static int bitlen64(uint64_t x) { int n = 0; while (x) { ++n; x >>= 1; } return n; }
 
+static int64_t floor_div64(int64_t x, int64_t y)   /* y > 0 */
+{
+    int64_t q = x / y;
+    if ((x % y != 0) && (x < 0)) q -= 1;
+    return q;
+}
+
 static void quant_endpoint_m6(const int e[4], int val[4], int *pbit)
 {
     int best = -1;
@@ -752,6 +759,59 @@ void oracle_bc7_encode_mode6(const uint8_t px[64], uint8_t out[16])
                 err += d * d;
             }
             if (best < 0 || err < best) { best = err; idx[i] = w; }
+        }
+    }
+    /* step 4b (R26): one least-squares refit of the endpoints for these
+     * indices, in exact integers -- per channel, with a = 64 - W4[idx],
+     * b = W4[idx]: [S aa, S ab; S ab, S bb] (e0, e1) = 64 (S a p, S b p),
+     * e = floor((2 num + det) / (2 det)) clamped to [0, 255], requantised
+     * (p-bits as in step 3) and re-indexed (step 4); kept only if the total
+     * squared error is strictly smaller. */
+    {
+        int64_t saa = 0, sab = 0, sbb = 0;
+        for (int i = 0; i < 16; ++i) {
+            const int64_t a = 64 - BC7_W4[idx[i]], b = BC7_W4[idx[i]];
+            saa += a * a; sab += a * b; sbb += b * b;
+        }
+        const int64_t det = saa * sbb - sab * sab;
+        if (det > 0) {
+            int f0[4], f1[4], F0[4], F1[4], q0, q1, jdx[16];
+            for (int c = 0; c < 4; ++c) {
+                int64_t r0 = 0, r1 = 0;
+                for (int i = 0; i < 16; ++i) {
+                    r0 += (int64_t)(64 - BC7_W4[idx[i]]) * px[4 * i + c] * 64;
+                    r1 += (int64_t)BC7_W4[idx[i]] * px[4 * i + c] * 64;
+                }
+                const int64_t n0 = sbb * r0 - sab * r1, n1 = saa * r1 - sab * r0;
+                int64_t e0 = floor_div64(2 * n0 + det, 2 * det), e1 = floor_div64(2 * n1 + det, 2 * det);
+                f0[c] = (int)(e0 < 0 ? 0 : (e0 > 255 ? 255 : e0));
+                f1[c] = (int)(e1 < 0 ? 0 : (e1 > 255 ? 255 : e1));
+            }
+            quant_endpoint_m6(f0, F0, &q0);
+            quant_endpoint_m6(f1, F1, &q1);
+            int64_t err_old = 0, err_new = 0;
+            for (int i = 0; i < 16; ++i) {
+                int best = -1;
+                for (int w = 0; w < 16; ++w) {
+                    int err = 0;
+                    for (int c = 0; c < 4; ++c) {
+                        const int d = interp(F0[c], F1[c], BC7_W4[w]) - px[4 * i + c];
+                        err += d * d;
+                    }
+                    if (best < 0 || err < best) { best = err; jdx[i] = w; }
+                }
+                err_new += best;
+                for (int c = 0; c < 4; ++c) {
+                    const int d = interp(E0[c], E1[c], BC7_W4[idx[i]]) - px[4 * i + c];
+                    err_old += d * d;
+                }
+            }
+            if (err_new < err_old) {
+                for (int c = 0; c < 4; ++c) { E0[c] = F0[c]; E1[c] = F1[c]; }
+                p0 = q0;
+                p1 = q1;
+                for (int i = 0; i < 16; ++i) idx[i] = jdx[i];
+            }
         }
     }
     /* step 5 */

@@ -76,7 +76,8 @@ def test_anchor_rule_and_pillow_agrees():
 
 def test_smooth_fields_quality():
     # smooth 4-channel fields (the shape of trained feature maps, SURVEY §8(d)
-    # recipe) reach >= 40 dB after encode/decode
+    # recipe) reach >= 44 dB after encode/decode (41.4 dB without the R26
+    # least-squares refit)
     y, x = np.mgrid[0:128, 0:128] / 128.0
     rng = np.random.default_rng(5)
     img = np.zeros((128, 128, 4), np.uint8)
@@ -85,4 +86,4 @@ def test_smooth_fields_quality():
         img[..., c] = np.clip(np.rint(255 * (0.5 + 0.3 * np.sin(2 * np.pi * (a * x + b * y) + phi))), 0, 255)
     dec = oracle.bc7_decode_image(oracle.bc7_encode_image_mode6(img), 128, 128)
     mse = np.mean((dec.astype(float) - img) ** 2)
-    assert 10 * np.log10(255 ** 2 / max(mse, 1e-9)) >= 40.0
+    assert 10 * np.log10(255 ** 2 / max(mse, 1e-9)) >= 44.0
