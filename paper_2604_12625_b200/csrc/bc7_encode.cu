@@ -47,6 +47,20 @@ __device__ __forceinline__ void quant_m6(uint32_t e, int (&val)[4], int& pbit) {
     }
 }
 
+// floor((2 n + det) / (2 det)) clamped to [0, 255], det > 0, without a 64-bit
+// division: a float estimate (accurate to << 1 inside [-1, 256], where the
+// clamp does not decide) corrected by one exact integer comparison each way
+__device__ __forceinline__ int round_div_clamp255(long long n, long long det) {
+    const float q = __ll2float_rn(n) / __ll2float_rn(det);
+    if (q < -1.0f) return 0;
+    if (q > 256.0f) return 255;
+    long long k = (long long)floorf(q + 0.5f);
+    const long long x = 2 * n + det, y = 2 * det;
+    if (y * k > x) --k;
+    else if (y * (k + 1) <= x) ++k;
+    return k < 0 ? 0 : (k > 255 ? 255 : (int)k);
+}
+
 // LSB-first write of n bits of v at bit position pos into 4 words
 __device__ __forceinline__ void put_bits(uint32_t (&w)[4], int& pos, uint32_t v, int n) {
     const int i = pos >> 5, o = pos & 31;
@@ -171,12 +185,81 @@ __global__ void __launch_bounds__(256) bc7_encode_mode6_kernel(const uint8_t* __
             key0[k] = 16 * n2 + k;
         }
         int idx[16];
+        int err_old = 0;   // sum over texels of (squared error - |texel|^2)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             int best = 0x7fffffff;
 #pragma unroll
             for (int k = 0; k < 16; ++k) best = min(best, key0[k] - 32 * (int)__dp4a(pal[k], t[i], 0u));
             idx[i] = best & 15;
+            err_old += best >> 4;
+        }
+        // 4b. one least-squares refit of the endpoints for these indices (R26),
+        // exact integers; kept only if the total squared error drops
+        {
+            int isaa = 0, isab = 0, isbb = 0;   // < 2^17
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int a = 64 - kW4[idx[i]], b = kW4[idx[i]];
+                isaa += a * a;
+                isab += a * b;
+                isbb += b * b;
+            }
+            const long long saa = isaa, sab = isab, sbb = isbb;
+            const long long det = saa * sbb - sab * sab;
+            if (det > 0) {
+                uint32_t fpk0 = 0u, fpk1 = 0u;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    int r0 = 0, r1 = 0;   // < 2^24
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        r0 += (64 - kW4[idx[i]]) * ch(t[i], c);
+                        r1 += kW4[idx[i]] * ch(t[i], c);
+                    }
+                    const long long n0 = sbb * (64LL * r0) - sab * (64LL * r1), n1 = saa * (64LL * r1) - sab * (64LL * r0);
+                    fpk0 |= (uint32_t)round_div_clamp255(n0, det) << (8 * c);
+                    fpk1 |= (uint32_t)round_div_clamp255(n1, det) << (8 * c);
+                }
+                int F0[4], F1[4], q0, q1;
+                quant_m6(fpk0, F0, q0);
+                quant_m6(fpk1, F1, q1);
+                uint32_t pal2[16];
+                int kk0[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    uint32_t pw = 0;
+                    int n2 = 0;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int x = ((64 - kW4[k]) * F0[c] + kW4[k] * F1[c] + 32) >> 6;
+                        pw |= (uint32_t)x << (8 * c);
+                        n2 += x * x;
+                    }
+                    pal2[k] = pw;
+                    kk0[k] = 16 * n2 + k;
+                }
+                int jdx[16], err_new = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    int best = 0x7fffffff;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) best = min(best, kk0[k] - 32 * (int)__dp4a(pal2[k], t[i], 0u));
+                    jdx[i] = best & 15;
+                    err_new += best >> 4;
+                }
+                if (err_new < err_old) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        E0[c] = F0[c];
+                        E1[c] = F1[c];
+                    }
+                    p0 = q0;
+                    p1 = q1;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) idx[i] = jdx[i];
+                }
+            }
         }
         // 5. anchor: texel 0's index must fit in 3 bits
         if (idx[0] >= 8) {
