@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "ndgi_common.cuh"
 
@@ -58,8 +59,14 @@ __device__ __forceinline__ float exp2f_fast(float x) {
 // for all K before any is consumed: the chain is latency-, not issue-bound
 constexpr int kSampleK = 4;
 
+// POW2: atlas width and height are powers of two, so the tile decision
+// floor(u * tiles_x) and u * W are exact in fp32 too and the position math
+// runs in fp32 (the fractional weights then differ from fp64 by < 2^-24);
+// otherwise fp64 (the oracle's decisions exactly)
+template <bool POW2>
 __global__ void __launch_bounds__(256) ndgi_sample_kernel(const __grid_constant__ SParams p) {
-    const double W = (double)p.tiles_x * p.C, H = (double)p.tiles_y * p.C;
+    using Pos = typename std::conditional<POW2, float, double>::type;
+    const Pos W = (Pos)p.tiles_x * (Pos)p.C, H = (Pos)p.tiles_y * (Pos)p.C;
     const size_t slot_bytes = (size_t)p.P * p.P * 4;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < p.n; base += stride * kSampleK) {
@@ -72,16 +79,16 @@ __global__ void __launch_bounds__(256) ndgi_sample_kernel(const __grid_constant_
             a[k] = (i < p.n && p.atlas) ? __ldg(p.atlas + i) : 0u;
         }
         int2 e[kSampleK];
-        double lx[kSampleK], ly[kSampleK];
+        Pos lx[kSampleK], ly[kSampleK];
 #pragma unroll
         for (int k = 0; k < kSampleK; ++k) {
-            const double u = fmin(fmax((double)q[k].x, 0.0), 1.0);   // NaN -> 0 (fmax)
-            const double v = fmin(fmax((double)q[k].y, 0.0), 1.0);
-            int tx = (int)floor(u * p.tiles_x), ty = (int)floor(v * p.tiles_y);
+            const Pos u = fmin(fmax((Pos)q[k].x, (Pos)0), (Pos)1);   // NaN -> 0 (fmax)
+            const Pos v = fmin(fmax((Pos)q[k].y, (Pos)0), (Pos)1);
+            int tx = (int)floor(u * (Pos)p.tiles_x), ty = (int)floor(v * (Pos)p.tiles_y);
             tx = tx > p.tiles_x - 1 ? p.tiles_x - 1 : tx;
             ty = ty > p.tiles_y - 1 ? p.tiles_y - 1 : ty;
-            lx[k] = u * W - 0.5 - (double)tx * p.C;   // [-0.5, C - 0.5]
-            ly[k] = v * H - 0.5 - (double)ty * p.C;
+            lx[k] = u * W - (Pos)0.5 - (Pos)tx * (Pos)p.C;   // [-0.5, C - 0.5]
+            ly[k] = v * H - (Pos)0.5 - (Pos)ty * (Pos)p.C;
             const size_t id = ((size_t)(a[k] < (uint32_t)p.atlases ? a[k] : 0u) * p.tiles_y + ty) * p.tiles_x + tx;
             e[k] = __ldg(reinterpret_cast<const int2*>(p.pt) + id);
         }
@@ -153,7 +160,10 @@ cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s) {
     const uint32_t cap = (uint32_t)a.num_sms * 8u;   // grid-stride beyond 8 CTAs (2048 threads) per SM
     if (grid > cap) grid = cap;
     if (grid == 0) grid = 1;
-    ndgi_sample_kernel<<<grid, per, 0, s>>>(p);
+    const uint32_t Wt = (uint32_t)(a.tiles_x * a.C), Ht = (uint32_t)(a.tiles_y * a.C);
+    const bool pow2 = (Wt & (Wt - 1)) == 0 && (Ht & (Ht - 1)) == 0 && Wt <= (1u << 20) && Ht <= (1u << 20);
+    if (pow2) ndgi_sample_kernel<true><<<grid, per, 0, s>>>(p);
+    else ndgi_sample_kernel<false><<<grid, per, 0, s>>>(p);
     return cudaGetLastError();
 }
 
