@@ -390,11 +390,22 @@ def run_gpu(args, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
+_C3 = {}
+
+
+def _c3_context(ndgi, torch):
+    """Config 3's scene (16,384 tiles, 590 MB of Theta), built once per process
+    for the VT and shading legs."""
+    if "ctx" not in _C3:
+        lay, seed = S.config("c3")
+        th = ndgi.upload_theta(S.make_theta(lay, seed))
+        _C3.update(lay=lay, seed=seed, th=th, ctx=ndgi.ndgi_load(lay, th, torch.cuda.current_device()))
+    return _C3["lay"], _C3["seed"], _C3["ctx"]
+
+
 def vt_latency(ndgi, torch, args):
     """Config 3: per-batch latency of ndgi_decode_tiles on a 16,384-tile scene."""
-    lay, seed = S.config("c3")
-    th = ndgi.upload_theta(S.make_theta(lay, seed))
-    ctx = ndgi.ndgi_load(lay, th, torch.cuda.current_device())
+    lay, seed, ctx = _c3_context(ndgi, torch)
     res = {}
     stream = torch.cuda.current_stream()
     for n in (8, 32, 128, 512):
@@ -429,9 +440,7 @@ def shading_leg(ndgi, torch, args):
     per sample); (b) the VT frame loop -- ndgi_vt_request + ndgi_decode_tiles of
     the jobs + ndgi_vt_upload + sample -- for a frame whose 144 tiles all miss
     (new time bucket) and for a frame that hits."""
-    lay, seed = S.config("c3")
-    th = ndgi.upload_theta(S.make_theta(lay, seed))
-    ctx = ndgi.ndgi_load(lay, th, torch.cuda.current_device())
+    lay, seed, ctx = _c3_context(ndgi, torch)
     stream = torch.cuda.current_stream()
     tx0, ty0, wx, wy = 20, 30, 16, 9
     ids = np.array([(ty0 + j) * lay["tiles_x"] + tx0 + i for j in range(wy) for i in range(wx)], np.uint32)
