@@ -77,6 +77,9 @@ def lib():
             "oracle_mean_at": (I, [P, P, I, D, P]),
             "oracle_bc7_encode_mode6": (None, [P, P]),
             "oracle_train_grad": (D, [P, P, I, P, P, P, I, P]),
+            "oracle_train_full_params": (C.c_size_t, [P]),
+            "oracle_train_full_grad": (D, [P, P, P, P, P, I, P]),
+            "oracle_train_full_project": (None, [P, P]),
             "oracle_adam": (None, [P, P, P, P, I, I, D, D, D, D]),
             "oracle_bc7_encode_image_mode6": (None, [P, I, I, P]),
             "oracle_restore": (D, [D, D, D]),
@@ -190,6 +193,23 @@ class Model:
         loss = lib().oracle_train_grad(C.byref(self.L), C.byref(self.M), int(k), _ptr(theta), _ptr(uvt), _ptr(target),
                                        len(uvt), _ptr(g))
         return loss, g
+
+    def full_params(self) -> int:
+        """R28: size of one tile's full training parameter vector."""
+        return int(lib().oracle_train_full_params(C.byref(self.L)))
+
+    def train_full_grad(self, theta: np.ndarray, uvt: np.ndarray, target: np.ndarray, noise: np.ndarray):
+        """R28: (loss, gradient) of one tile's full parameter vector (BC-simulated maps, noise, MLP)."""
+        theta = np.ascontiguousarray(theta, np.float64)
+        g = np.zeros_like(theta)
+        loss = lib().oracle_train_full_grad(C.byref(self.L), _ptr(theta), _ptr(np.ascontiguousarray(uvt, np.float64)),
+                                            _ptr(np.ascontiguousarray(target, np.float64)),
+                                            _ptr(np.ascontiguousarray(noise, np.float64)), len(uvt), _ptr(g))
+        return loss, g
+
+    def train_full_project(self, theta: np.ndarray) -> None:
+        assert theta.dtype == np.float64 and theta.flags["C_CONTIGUOUS"]
+        lib().oracle_train_full_project(C.byref(self.L), _ptr(theta))
 
     def decode_full(self, t: float, nthreads: int = 1) -> np.ndarray:
         L = self.lay

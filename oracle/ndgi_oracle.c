@@ -936,3 +936,195 @@ void oracle_adam(double *theta, double *m, double *v, const double *g, int P, in
         theta[i] -= lr * (m[i] / c1) / (sqrt(v[i] / c2) + eps);
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Full training step: BC-simulated feature   */
+/* maps (Eq. 6-7: "we divide each feature map into 4x4      */
+/* blocks, where the feature values within each block are represented  */
+/* by a set of endpoints E and weights W ... f_p = (1 - w_p) e1 +       */
+/* w_p e2"), uniform noise on the sampled vectors (Eq. 5:    */
+/* alpha = 1/256; "Noise is then added to the sampled vector     */
+/* V_uvt, V_uv"), plain line grids, the per-tile MLP, L2 loss, Adam.   */
+/* Reading R28: parameters of one tile, fp64 here, in the   */
+/* order [MLP blob | F_uv blocks | F_uvt slices' blocks | F_ut | F_vt],  */
+/* each block [e1 RGBA | e2 RGBA | w_0..w_15]; the noise draws are      */
+/* inputs (n[12] per sample, in [-0.5, 0.5)); after each Adam step the  */
+/* BC endpoints / weights and the line grids are projected onto [0,1].  */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    size_t mlp, uv, uvt, ut, vt, total;
+} full_offsets;
+
+static full_offsets full_layout(const oracle_layout *L)
+{
+    full_offsets o;
+    o.mlp = 0;
+    o.uv = oracle_mlp_params(L->hidden);
+    o.uvt = o.uv + (size_t)(L->uv_res / 4) * (L->uv_res / 4) * 24;
+    o.ut = o.uvt + (size_t)L->uvt_depth * (L->uvt_res / 4) * (L->uvt_res / 4) * 24;
+    o.vt = o.ut + (size_t)L->line_t * L->line_res * 2;
+    o.total = o.vt + (size_t)L->line_t * L->line_res * 2;
+    return o;
+}
+
+size_t oracle_train_full_params(const oracle_layout *L) { return full_layout(L).total; }
+
+/* a differentiable 2D map: BC-simulated (blocks) or plain (grid) */
+typedef struct {
+    const double *p;   /* parameters */
+    double *g;         /* their gradient (or NULL) */
+    int bc, rx, ry, nc;
+} dmap;
+
+static double dfetch(const dmap *m, int a, int b, int c)
+{
+    if (m->bc) {
+        const double *blk = m->p + ((size_t)(b / 4) * (m->rx / 4) + a / 4) * 24;
+        const double w = blk[8 + 4 * (b % 4) + (a % 4)];
+        return (1.0 - w) * blk[c] + w * blk[4 + c];    /* Eq. 7 */
+    }
+    return m->p[((size_t)b * m->rx + a) * m->nc + c];
+}
+
+static void dscatter(const dmap *m, int a, int b, int c, double gv)
+{
+    if (m->bc) {
+        const size_t base = ((size_t)(b / 4) * (m->rx / 4) + a / 4) * 24;
+        const double *blk = m->p + base;
+        const int pi = 4 * (b % 4) + (a % 4);
+        const double w = blk[8 + pi];
+        m->g[base + c] += gv * (1.0 - w);
+        m->g[base + 4 + c] += gv * w;
+        m->g[base + 8 + pi] += gv * (blk[4 + c] - blk[c]);
+        return;
+    }
+    m->g[((size_t)b * m->rx + a) * m->nc + c] += gv;
+}
+
+/* bilinear (R1) forward, or backward with upstream gradient gout[nc] */
+static void dbilinear(const dmap *m, double a, double b, double *out, const double *gout)
+{
+    double sx = a * m->rx - 0.5, sy = b * m->ry - 0.5;
+    double fx0 = floor(sx), fy0 = floor(sy);
+    double fx = sx - fx0, fy = sy - fy0;
+    int x0 = clampi((int)fx0, 0, m->rx - 1), x1 = clampi((int)fx0 + 1, 0, m->rx - 1);
+    int y0 = clampi((int)fy0, 0, m->ry - 1), y1 = clampi((int)fy0 + 1, 0, m->ry - 1);
+    const double w00 = (1 - fx) * (1 - fy), w10 = fx * (1 - fy), w01 = (1 - fx) * fy, w11 = fx * fy;
+    for (int c = 0; c < m->nc; ++c) {
+        if (gout) {
+            dscatter(m, x0, y0, c, w00 * gout[c]);
+            dscatter(m, x1, y0, c, w10 * gout[c]);
+            dscatter(m, x0, y1, c, w01 * gout[c]);
+            dscatter(m, x1, y1, c, w11 * gout[c]);
+        } else {
+            out[c] = w00 * dfetch(m, x0, y0, c) + w10 * dfetch(m, x1, y0, c) + w01 * dfetch(m, x0, y1, c)
+                   + w11 * dfetch(m, x1, y1, c);
+        }
+    }
+}
+
+/* features x[16] of one sample (forward) or their gradient scatter (backward, gx[12]) */
+static void full_features(const oracle_layout *L, const double *theta, double *grad, double u, double v, double t,
+                          const double *noise, double *x, const double *gx)
+{
+    const full_offsets o = full_layout(L);
+    const double alpha = 1.0 / 256.0;
+    const size_t slice = (size_t)(L->uvt_res / 4) * (L->uvt_res / 4) * 24;
+    double s = t * L->uvt_depth - 0.5, k0d = floor(s), tau = s - k0d;
+    int k0 = clampi((int)k0d, 0, L->uvt_depth - 1), k1 = clampi((int)k0d + 1, 0, L->uvt_depth - 1);
+    dmap m0 = {theta + o.uvt + slice * k0, grad ? grad + o.uvt + slice * k0 : NULL, 1, L->uvt_res, L->uvt_res, 4};
+    dmap m1 = {theta + o.uvt + slice * k1, grad ? grad + o.uvt + slice * k1 : NULL, 1, L->uvt_res, L->uvt_res, 4};
+    dmap muv = {theta + o.uv, grad ? grad + o.uv : NULL, 1, L->uv_res, L->uv_res, 4};
+    dmap mut = {theta + o.ut, grad ? grad + o.ut : NULL, 0, L->line_res, L->line_t, 2};
+    dmap mvt = {theta + o.vt, grad ? grad + o.vt : NULL, 0, L->line_res, L->line_t, 2};
+    if (gx) {
+        double g0[4], g1[4];
+        for (int c = 0; c < 4; ++c) { g0[c] = (1 - tau) * gx[c]; g1[c] = tau * gx[c]; }
+        dbilinear(&m0, u, v, NULL, g0);
+        dbilinear(&m1, u, v, NULL, g1);
+        dbilinear(&muv, u, v, NULL, gx + 4);
+        dbilinear(&mut, u, t, NULL, gx + 8);
+        dbilinear(&mvt, v, t, NULL, gx + 10);
+        return;
+    }
+    double a[4], b[4];
+    dbilinear(&m0, u, v, a, NULL);
+    dbilinear(&m1, u, v, b, NULL);
+    for (int c = 0; c < 4; ++c) x[c] = (1 - tau) * a[c] + tau * b[c];
+    dbilinear(&muv, u, v, x + 4, NULL);
+    dbilinear(&mut, u, t, x + 8, NULL);
+    dbilinear(&mvt, v, t, x + 10, NULL);
+    for (int i = 0; i < 12; ++i) x[i] += alpha * noise[i];   /* Eq. 5 */
+    oracle_gamma(t, x + 12);
+}
+
+/* loss and gradient over the whole parameter vector of one tile */
+double oracle_train_full_grad(const oracle_layout *L, const double *theta, const double *uvt, const double *target,
+                              const double *noise, int S, double *grad)
+{
+    const int h = L->hidden;
+    const full_offsets o = full_layout(L);
+    const double *W1 = theta, *b1 = W1 + 16 * h, *W2 = b1 + h, *b2 = W2 + h * h, *W3 = b2 + h, *b3 = W3 + 3 * h;
+    double *gW1 = grad, *gb1 = gW1 + 16 * h, *gW2 = gb1 + h, *gb2 = gW2 + h * h, *gW3 = gb2 + h, *gb3 = gW3 + 3 * h;
+    memset(grad, 0, sizeof(double) * o.total);
+    double loss = 0.0;
+    double x[16], z1[256], g1[256], z2[256], g2[256], dy[3], dz2[256], dz1[256], gx[12];
+    for (int s = 0; s < S; ++s) {
+        full_features(L, theta, NULL, uvt[3 * s], uvt[3 * s + 1], uvt[3 * s + 2], noise + 12 * s, x, NULL);
+        for (int oo = 0; oo < h; ++oo) {
+            double a = b1[oo];
+            for (int i = 0; i < 16; ++i) a += W1[oo * 16 + i] * x[i];
+            z1[oo] = a;
+            g1[oo] = oracle_gelu(a, L->gelu);
+        }
+        for (int oo = 0; oo < h; ++oo) {
+            double a = b2[oo];
+            for (int i = 0; i < h; ++i) a += W2[oo * h + i] * g1[i];
+            z2[oo] = a;
+            g2[oo] = oracle_gelu(a, L->gelu);
+        }
+        for (int oo = 0; oo < 3; ++oo) {
+            double a = b3[oo];
+            for (int i = 0; i < h; ++i) a += W3[oo * h + i] * g2[i];
+            const double d = a - target[3 * s + oo];
+            loss += d * d;
+            dy[oo] = 2.0 * d / (3.0 * S);
+        }
+        for (int oo = 0; oo < 3; ++oo) {
+            gb3[oo] += dy[oo];
+            for (int i = 0; i < h; ++i) gW3[oo * h + i] += dy[oo] * g2[i];
+        }
+        for (int i = 0; i < h; ++i) {
+            double a = 0.0;
+            for (int oo = 0; oo < 3; ++oo) a += W3[oo * h + i] * dy[oo];
+            dz2[i] = a * gelu_grad(z2[i], L->gelu);
+        }
+        for (int oo = 0; oo < h; ++oo) {
+            gb2[oo] += dz2[oo];
+            for (int i = 0; i < h; ++i) gW2[oo * h + i] += dz2[oo] * g1[i];
+        }
+        for (int i = 0; i < h; ++i) {
+            double a = 0.0;
+            for (int oo = 0; oo < h; ++oo) a += W2[oo * h + i] * dz2[oo];
+            dz1[i] = a * gelu_grad(z1[i], L->gelu);
+        }
+        for (int oo = 0; oo < h; ++oo) {
+            gb1[oo] += dz1[oo];
+            for (int i = 0; i < 16; ++i) gW1[oo * 16 + i] += dz1[oo] * x[i];
+        }
+        for (int i = 0; i < 12; ++i) {
+            double a = 0.0;
+            for (int oo = 0; oo < h; ++oo) a += W1[oo * 16 + i] * dz1[oo];
+            gx[i] = a;
+        }
+        full_features(L, theta, grad, uvt[3 * s], uvt[3 * s + 1], uvt[3 * s + 2], noise + 12 * s, NULL, gx);
+    }
+    return loss / (3.0 * S);
+}
+
+/* R28 projection after an Adam step: BC endpoints / weights and line grids onto [0,1] */
+void oracle_train_full_project(const oracle_layout *L, double *theta)
+{
+    const full_offsets o = full_layout(L);
+    for (size_t i = o.uv; i < o.total; ++i) theta[i] = fmin(fmax(theta[i], 0.0), 1.0);
+}
