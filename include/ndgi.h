@@ -337,6 +337,28 @@ NDGI_API ndgi_status ndgi_train_create(ndgi_ctx* ctx, ndgi_train** out);
  * appear once per step.  Errors: ARG, RANGE (n > 2^20, S > 2^24), CUDA. */
 NDGI_API ndgi_status ndgi_train_step(ndgi_train* tr, const uint32_t* tile_ids, uint32_t n, const float* samples,
                                      const float* targets, uint32_t S, float lr, float* loss, void* stream);
+/*
+ * Full training step (reading R28): the BC-simulated
+ * feature maps of Eq. 6-7 (per 4x4 block endpoints e1, e2 and 16 weights;
+ * texel p = (1 - w_p) e1 + w_p e2), the plain line grids and the MLP are all
+ * trained; the sampled vectors get uniform noise alpha * n (Eq. 5, alpha =
+ * 1/256); after each Adam step the map parameters are projected onto [0,1].
+ * Parameters per tile (ndgi_train_full_params(layout) floats, fp32):
+ *   [MLP blob (as ndgi_params.mlp) | F_uv blocks [(R_uv/4)^2][24] |
+ *    F_uvt blocks [D][(R3/4)^2][24] | F_ut [T][U][2] | F_vt [T][U][2]],
+ *   block = [e1 RGBA | e2 RGBA | w_0 .. w_15] (texel p = 4 * row + col).
+ * init: DEVICE float [num_tiles][P], copied.  The context supplies the layout
+ * (its feature maps are not used).  Steps take DEVICE noise float[n][S][12]
+ * (draws in [-0.5, 0.5): V_uvt 0..3, V_uv 4..7, V_ut 8..9, V_vt 10..11).
+ * ndgi_train_weights / _last_grad then move P floats per tile;
+ * ndgi_train_export_f16 exports the MLP part.  Errors as the fine-tuning calls.
+ */
+NDGI_API size_t ndgi_train_full_params(const ndgi_layout* layout);
+NDGI_API ndgi_status ndgi_train_full_create(ndgi_ctx* ctx, const float* init, ndgi_train** out);
+NDGI_API ndgi_status ndgi_train_full_step(ndgi_train* tr, const uint32_t* tile_ids, uint32_t n, const float* samples,
+                                          const float* targets, const float* noise, uint32_t S, float lr, float* loss,
+                                          void* stream);
+
 /* the last step's gradients (mean-loss gradient of each batch tile, before
  * Adam) -> DEVICE float[n][P]; n <= that step's batch (RANGE otherwise) */
 NDGI_API ndgi_status ndgi_train_last_grad(ndgi_train* tr, float* out, uint32_t n, void* stream);

@@ -85,6 +85,9 @@ _SIGS = {
     "ndgi_train_last_grad": (_I, [_P, _P, _U32, _P]),
     "ndgi_train_export_f16": (_I, [_P, _P, _P]),
     "ndgi_train_free": (_I, [_P]),
+    "ndgi_train_full_params": (C.c_size_t, [C.POINTER(ndgi_layout)]),
+    "ndgi_train_full_create": (_I, [_P, _P, C.POINTER(C.c_void_p)]),
+    "ndgi_train_full_step": (_I, [_P, _P, _U32, _P, _P, _P, _U32, _F, _P, _P]),
     "ndgi_sample_lighting": (_I, [_P, _P, C.c_int32, _P, _U32, _P, _P, _U32, _F, C.POINTER(ndgi_hdr), _P, _P]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -356,21 +359,38 @@ def ndgi_bc7_encode_mode6(rgba, blocks, stream=None) -> None:
 
 
 # ---------------------------------------------------------------- fine-tuning (NEXT 4)
+def train_full_params(lay: dict) -> int:
+    L = lay if isinstance(lay, ndgi_layout) else make_layout(lay)
+    return int(_lib.ndgi_train_full_params(C.byref(L)))
+
+
 class Trainer:
-    """ndgi_train: fp32 master weights + Adam state of every tile's MLP (R27)."""
+    """ndgi_train: fp32 parameters + Adam state of every tile -- the MLP only
+    (fine-tuning, R27) or, with full_init, MLP + BC-simulated maps + line grids (R28)."""
 
-    def __init__(self, ctx: Context):
+    def __init__(self, ctx: Context, full_init=None):
         h = C.c_void_p()
-        _check(_lib.ndgi_train_create(ctx.handle, C.byref(h)), "ndgi_train_create")
-        self.handle, self.ctx = h, ctx
-        self.P = 16 * ctx.lay["hidden"] + ctx.lay["hidden"] * ctx.lay["hidden"] + 5 * ctx.lay["hidden"] + 3
+        if full_init is None:
+            _check(_lib.ndgi_train_create(ctx.handle, C.byref(h)), "ndgi_train_create")
+            self.P = 16 * ctx.lay["hidden"] + ctx.lay["hidden"] * ctx.lay["hidden"] + 5 * ctx.lay["hidden"] + 3
+        else:
+            _check(_lib.ndgi_train_full_create(ctx.handle, C.c_void_p(full_init.data_ptr()), C.byref(h)),
+                   "ndgi_train_full_create")
+            self.P = train_full_params(ctx.lay)
+        self.handle, self.ctx, self.full = h, ctx, full_init is not None
 
-    def step(self, tile_ids, samples, targets, lr: float = 1e-3, loss=None, stream=None) -> None:
-        """tile_ids CUDA int32/uint32 [n]; samples, targets CUDA float32 [n][S][3]; loss CUDA float32 [n] or None."""
+    def step(self, tile_ids, samples, targets, lr: float = 1e-3, loss=None, stream=None, noise=None) -> None:
+        """tile_ids CUDA int32/uint32 [n]; samples, targets CUDA float32 [n][S][3]; loss CUDA float32 [n] or None;
+        noise CUDA float32 [n][S][12] (full trainer only)."""
         n, S = int(samples.shape[0]), int(samples.shape[1])
-        st = _lib.ndgi_train_step(self.handle, C.c_void_p(tile_ids.data_ptr()), n, C.c_void_p(samples.data_ptr()),
-                                  C.c_void_p(targets.data_ptr()), S, float(lr),
-                                  C.c_void_p(loss.data_ptr()) if loss is not None else None, _stream_ptr(stream))
+        lo = C.c_void_p(loss.data_ptr()) if loss is not None else None
+        if self.full:
+            st = _lib.ndgi_train_full_step(self.handle, C.c_void_p(tile_ids.data_ptr()), n,
+                                           C.c_void_p(samples.data_ptr()), C.c_void_p(targets.data_ptr()),
+                                           C.c_void_p(noise.data_ptr()) if noise is not None else None, S, float(lr), lo, _stream_ptr(stream))
+        else:
+            st = _lib.ndgi_train_step(self.handle, C.c_void_p(tile_ids.data_ptr()), n, C.c_void_p(samples.data_ptr()),
+                                      C.c_void_p(targets.data_ptr()), S, float(lr), lo, _stream_ptr(stream))
         _check(st, "ndgi_train_step")
 
     def last_grad(self, out, stream=None) -> None:

@@ -25,7 +25,8 @@ cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s);
 cudaError_t launch_train_grad(const TrainArgs& a, int H, cudaStream_t s);
 cudaError_t launch_adam(float* theta, float* m, float* v, int* steps, const float* grad, const uint32_t* tile_ids,
-                        int n, int P, int num_tiles, float lr, float b1, float b2, float eps, cudaStream_t s);
+                        int n, size_t P, int num_tiles, float lr, float b1, float b2, float eps, size_t proj,
+                        cudaStream_t s);
 cudaError_t launch_convert_f16_f32(const uint16_t* in, float* out, size_t n, cudaStream_t s);
 cudaError_t launch_convert_f32_f16(const float* in, uint16_t* out, size_t n, cudaStream_t s);
 cudaError_t uv_textures_build(const void* uv, int atlases, int tiles_x, int tiles_y, int C, cudaArray_t* arrays,
@@ -545,23 +546,52 @@ ndgi_status ndgi_bc7_encode_mode6(const void* rgba, uint32_t w, uint32_t h, void
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 encode launch");
 }
 
-// ---- fine-tuning ----------------------------------------
+// ---- training ----------------------------------------------
+// One trainer type for both stages: fine-tuning (R27, parameters = the MLP) and
+// the full step (R28, parameters = MLP + BC-simulated maps + line grids).
 struct ndgi_train {
     ndgi_ctx* ctx;
-    int P;
+    bool full;
+    size_t P;                      // parameters per tile
+    size_t off_uv, off_uvt, off_ut, off_vt;
     float *theta, *m, *v, *grad, *loss;
     int* steps;
-    uint32_t cap;   // batch capacity of grad / loss
+    uint32_t cap;                  // batch capacity of grad / loss
 };
 
-ndgi_status ndgi_train_create(ndgi_ctx* ctx, ndgi_train** out) {
-    if (!ctx || !out) return fail(NDGI_ERR_ARG, "NULL ctx or out");
-    if (ctx->L.hidden != 16) return fail(NDGI_ERR_UNSUPPORTED, "fine-tuning is built for h = 16");
+namespace {
+
+size_t full_params(const ndgi_layout& L, size_t* off) {
+    const size_t mlp = mlp_elems(L.hidden);
+    const size_t uv = mlp, uvt = uv + (size_t)(L.uv_res / 4) * (L.uv_res / 4) * 24;
+    const size_t ut = uvt + (size_t)L.uvt_depth * (L.uvt_res / 4) * (L.uvt_res / 4) * 24;
+    const size_t vt = ut + (size_t)L.line_t * L.line_res * 2;
+    const size_t total = vt + (size_t)L.line_t * L.line_res * 2;
+    if (off) {
+        off[0] = uv;
+        off[1] = uvt;
+        off[2] = ut;
+        off[3] = vt;
+    }
+    return total;
+}
+
+ndgi_status train_create(ndgi_ctx* ctx, bool full, const float* init, ndgi_train** out) {
+    if (!ctx || !out || (full && !init)) return fail(NDGI_ERR_ARG, "NULL ctx, out or init");
+    if (ctx->L.hidden != 16) return fail(NDGI_ERR_UNSUPPORTED, "training is built for h = 16");
+    if (full && (ctx->L.uv_res % 4 || ctx->L.uvt_res % 4))
+        return fail(NDGI_ERR_UNSUPPORTED, "BC-simulated maps need resolutions that are multiples of 4");
     DeviceGuard g(ctx->device);
     ndgi_train* t = new (std::nothrow) ndgi_train();
     if (!t) return fail(NDGI_ERR_NOMEM, "host allocation");
     t->ctx = ctx;
-    t->P = (int)mlp_elems(ctx->L.hidden);
+    t->full = full;
+    size_t off[4] = {0, 0, 0, 0};
+    t->P = full ? full_params(ctx->L, off) : mlp_elems(ctx->L.hidden);
+    t->off_uv = off[0];
+    t->off_uvt = off[1];
+    t->off_ut = off[2];
+    t->off_vt = off[3];
     const size_t n = (size_t)ctx->L.num_tiles * t->P;
     cudaError_t e = cudaMalloc(&t->theta, n * 4);
     if (e == cudaSuccess) e = cudaMalloc(&t->m, n * 4);
@@ -570,7 +600,10 @@ ndgi_status ndgi_train_create(ndgi_ctx* ctx, ndgi_train** out) {
     if (e == cudaSuccess) e = cudaMemset(t->m, 0, n * 4);
     if (e == cudaSuccess) e = cudaMemset(t->v, 0, n * 4);
     if (e == cudaSuccess) e = cudaMemset(t->steps, 0, (size_t)ctx->L.num_tiles * sizeof(int));
-    if (e == cudaSuccess) e = ndgi::launch_convert_f16_f32(ctx->P.mlp, t->theta, n, 0);   // fp32 master copy
+    if (e == cudaSuccess) {
+        if (full) e = cudaMemcpy(t->theta, init, n * 4, cudaMemcpyDeviceToDevice);
+        else e = ndgi::launch_convert_f16_f32(ctx->P.mlp, t->theta, n, 0);   // fp32 master copy
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(t->theta);
@@ -578,15 +611,15 @@ ndgi_status ndgi_train_create(ndgi_ctx* ctx, ndgi_train** out) {
         cudaFree(t->v);
         cudaFree(t->steps);
         delete t;
-        return cuda_fail(e, "ndgi_train_create");
+        return cuda_fail(e, "training state allocation");
     }
     *out = t;
     return NDGI_OK;
 }
 
-ndgi_status ndgi_train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, const float* samples,
-                            const float* targets, uint32_t S, float lr, float* loss, void* stream) {
-    if (!t || !tile_ids || !samples || !targets) return fail(NDGI_ERR_ARG, "NULL argument");
+ndgi_status train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, const float* samples, const float* targets,
+                       const float* noise, uint32_t S, float lr, float* loss, void* stream) {
+    if (!t || !tile_ids || !samples || !targets || (t->full && !noise)) return fail(NDGI_ERR_ARG, "NULL argument");
     if (n == 0 || S == 0) return fail(NDGI_ERR_ARG, "n == 0 or S == 0");
     if (n > (1u << 20) || S > (1u << 24)) return fail(NDGI_ERR_RANGE, "n > 2^20 or S > 2^24");
     if (!std::isfinite(lr) || lr < 0.0f) return fail(NDGI_ERR_ARG, "lr must be finite and >= 0");
@@ -641,13 +674,42 @@ ndgi_status ndgi_train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n,
     a.grad = t->grad;
     a.loss = t->loss;
     a.err = ctx->d_err;
+    a.noise = t->full ? noise : nullptr;
+    a.pfull = t->P;
+    a.off_uv = t->off_uv;
+    a.off_uvt = t->off_uvt;
+    a.off_ut = t->off_ut;
+    a.off_vt = t->off_vt;
     e = ndgi::launch_train_grad(a, (int)L.hidden, s);
     if (e == cudaSuccess)
         e = ndgi::launch_adam(t->theta, t->m, t->v, t->steps, t->grad, tile_ids, (int)n, t->P, (int)L.num_tiles, lr,
-                              0.9f, 0.999f, 1e-8f, s);
+                              0.9f, 0.999f, 1e-8f, t->full ? t->off_uv : t->P, s);
     if (e == cudaSuccess && loss) e = cudaMemcpyAsync(loss, t->loss, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "train step");
     return NDGI_OK;
+}
+
+}  // namespace
+
+ndgi_status ndgi_train_create(ndgi_ctx* ctx, ndgi_train** out) { return train_create(ctx, false, nullptr, out); }
+
+ndgi_status ndgi_train_full_create(ndgi_ctx* ctx, const float* init, ndgi_train** out) {
+    return train_create(ctx, true, init, out);
+}
+
+size_t ndgi_train_full_params(const ndgi_layout* layout) { return layout ? full_params(*layout, nullptr) : 0; }
+
+ndgi_status ndgi_train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, const float* samples,
+                            const float* targets, uint32_t S, float lr, float* loss, void* stream) {
+    if (t && t->full) return fail(NDGI_ERR_ARG, "a full trainer steps with ndgi_train_full_step");
+    return train_step(t, tile_ids, n, samples, targets, nullptr, S, lr, loss, stream);
+}
+
+ndgi_status ndgi_train_full_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, const float* samples,
+                                 const float* targets, const float* noise, uint32_t S, float lr, float* loss,
+                                 void* stream) {
+    if (t && !t->full) return fail(NDGI_ERR_ARG, "a fine-tuning trainer steps with ndgi_train_step");
+    return train_step(t, tile_ids, n, samples, targets, noise, S, lr, loss, stream);
 }
 
 ndgi_status ndgi_train_last_grad(ndgi_train* t, float* out, uint32_t n, void* stream) {
@@ -670,8 +732,15 @@ ndgi_status ndgi_train_weights(ndgi_train* t, float* out, void* stream) {
 ndgi_status ndgi_train_export_f16(ndgi_train* t, uint16_t* mlp, void* stream) {
     if (!t || !mlp) return fail(NDGI_ERR_ARG, "NULL argument");
     DeviceGuard g(t->ctx->device);
-    const cudaError_t e = ndgi::launch_convert_f32_f16(t->theta, mlp, (size_t)t->ctx->L.num_tiles * t->P,
-                                                       static_cast<cudaStream_t>(stream));
+    const size_t pm = mlp_elems(t->ctx->L.hidden);
+    cudaError_t e = cudaSuccess;
+    if (!t->full) {
+        e = ndgi::launch_convert_f32_f16(t->theta, mlp, (size_t)t->ctx->L.num_tiles * pm, static_cast<cudaStream_t>(stream));
+    } else {
+        for (uint32_t k = 0; k < t->ctx->L.num_tiles && e == cudaSuccess; ++k)   // the MLP part of each tile
+            e = ndgi::launch_convert_f32_f16(t->theta + (size_t)k * t->P, mlp + (size_t)k * pm, pm,
+                                             static_cast<cudaStream_t>(stream));
+    }
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "train export");
 }
 

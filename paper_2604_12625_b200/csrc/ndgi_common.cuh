@@ -89,7 +89,10 @@ struct TrainArgs {
     const float* targets;       // [n][S][3]
     int n, S, chunks;
     // state
-    float* theta;               // [num_tiles][P] fp32 master weights
+    float* theta;               // [num_tiles][P] fp32 master weights (FULL: [num_tiles][P_full])
+    // FULL (R28): BC-simulated maps + line grids in theta after the MLP; noise [n][S][12]
+    const float* noise;
+    size_t pfull, off_uv, off_uvt, off_ut, off_vt;
     float* grad;                // [n][P] (zeroed by the host)
     float* loss;                // [n] (zeroed by the host), mean squared error
     uint32_t* err;

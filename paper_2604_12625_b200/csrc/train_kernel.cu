@@ -48,12 +48,72 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// ---- R28: BC-simulated / plain parameter maps (full training) ----------------
+struct PMap {
+    const float* p;   // parameters
+    float* g;         // their gradient (global, atomics)
+    int bc, rx, ry, nc;
+};
+
+__device__ __forceinline__ float pfetch(const PMap& m, int a, int b, int c) {
+    if (m.bc) {
+        const float* blk = m.p + ((size_t)(b >> 2) * (m.rx >> 2) + (a >> 2)) * 24;
+        const float w = __ldg(blk + 8 + 4 * (b & 3) + (a & 3));
+        return (1.0f - w) * __ldg(blk + c) + w * __ldg(blk + 4 + c);   // Eq. 7
+    }
+    return __ldg(m.p + ((size_t)b * m.rx + a) * m.nc + c);
+}
+
+__device__ __forceinline__ void pscatter(const PMap& m, int a, int b, const float* gv) {
+    if (m.bc) {
+        const size_t base = ((size_t)(b >> 2) * (m.rx >> 2) + (a >> 2)) * 24;
+        const int pi = 4 * (b & 3) + (a & 3);
+        const float w = __ldg(m.p + base + 8 + pi);
+        float gw = 0.f;
+        for (int c = 0; c < m.nc; ++c) {
+            atomicAdd(m.g + base + c, gv[c] * (1.0f - w));
+            atomicAdd(m.g + base + 4 + c, gv[c] * w);
+            gw = fmaf(gv[c], __ldg(m.p + base + 4 + c) - __ldg(m.p + base + c), gw);
+        }
+        atomicAdd(m.g + base + 8 + pi, gw);
+        return;
+    }
+    for (int c = 0; c < m.nc; ++c) atomicAdd(m.g + ((size_t)b * m.rx + a) * m.nc + c, gv[c]);
+}
+
+// bilinear (R1) forward, or the backward scatter of gout (weights per tap)
+__device__ __forceinline__ void pbilinear(const PMap& m, float a, float b, float* out, const float* gout) {
+    const float sx = a * (float)m.rx - 0.5f, sy = b * (float)m.ry - 0.5f;
+    const float fx0 = floorf(sx), fy0 = floorf(sy);
+    const float fx = sx - fx0, fy = sy - fy0;
+    const int x0 = clampi((int)fx0, 0, m.rx - 1), x1 = clampi((int)fx0 + 1, 0, m.rx - 1);
+    const int y0 = clampi((int)fy0, 0, m.ry - 1), y1 = clampi((int)fy0 + 1, 0, m.ry - 1);
+    const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
+    if (gout) {
+        float g[4];
+        for (int c = 0; c < m.nc; ++c) g[c] = w00 * gout[c];
+        pscatter(m, x0, y0, g);
+        for (int c = 0; c < m.nc; ++c) g[c] = w10 * gout[c];
+        pscatter(m, x1, y0, g);
+        for (int c = 0; c < m.nc; ++c) g[c] = w01 * gout[c];
+        pscatter(m, x0, y1, g);
+        for (int c = 0; c < m.nc; ++c) g[c] = w11 * gout[c];
+        pscatter(m, x1, y1, g);
+        return;
+    }
+    for (int c = 0; c < m.nc; ++c)
+        out[c] = w00 * pfetch(m, x0, y0, c) + w10 * pfetch(m, x1, y0, c) + w01 * pfetch(m, x0, y1, c) +
+                 w11 * pfetch(m, x1, y1, c);
+}
+
 // Gradient sums without per-component warp reductions: per warp iteration the
 // 32 samples' activation vectors are staged in smem (row = sample), and each
 // lane owns fixed gradient components (8 consecutive inputs of one output of
 // W1 and of W2, 2 of W3, one bias of each layer), accumulated in registers over
 // all of the CTA's samples; one smem atomic per component per warp at the end.
-template <int H>
+// FULL (R28): the features come from the tile's BC-simulated maps and line
+// grids (plus the given noise), and dL/dx scatters into their gradients
+template <int H, bool FULL>
 __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_constant__ TrainArgs a) {
     static_assert(H == 16, "lane-owned gradient components are laid out for h = 16");
     constexpr int P = 16 * H + H + H * H + H + 3 * H + 3;
@@ -69,8 +129,9 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
         if (chunk == 0 && tid == 0) atomicAdd(a.err, 1u);
         return;   // uniform
     }
+    const size_t tstride = FULL ? a.pfull : (size_t)P;
     for (int i = tid; i < P; i += blockDim.x) {
-        sW[i] = a.theta[(size_t)k * P + i];
+        sW[i] = a.theta[(size_t)k * tstride + i];
         sG[i] = 0.f;
     }
     if (tid == 0) sLoss = 0.f;
@@ -108,16 +169,36 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
             // V_uvt: tau-blend of two slices (R4), V_uv, V_ut, V_vt (R5), gamma (Eq. 4)
             const float sd = t * (float)a.D - 0.5f, fl = floorf(sd), tau = sd - fl;
             const int k0 = clampi((int)fl, 0, a.D - 1), k1 = clampi((int)fl + 1, 0, a.D - 1);
-            Map2D m0{vol + a.uvt_slice_bytes * k0, a.fmt_uvt, a.R3, a.R3, 4};
-            Map2D m1{vol + a.uvt_slice_bytes * k1, a.fmt_uvt, a.R3, a.R3, 4};
             float p0[4], p1[4];
-            bilinear(m0, u, v, p0);
-            bilinear(m1, u, v, p1);
+            if constexpr (FULL) {
+                const float* th = a.theta + (size_t)k * a.pfull;
+                const size_t sl = (size_t)(a.R3 >> 2) * (a.R3 >> 2) * 24;
+                PMap m0{th + a.off_uvt + sl * k0, nullptr, 1, a.R3, a.R3, 4};
+                PMap m1{th + a.off_uvt + sl * k1, nullptr, 1, a.R3, a.R3, 4};
+                PMap muv{th + a.off_uv, nullptr, 1, a.R_uv, a.R_uv, 4};
+                PMap mut{th + a.off_ut, nullptr, 0, a.U, a.T, 2};
+                PMap mvt{th + a.off_vt, nullptr, 0, a.U, a.T, 2};
+                pbilinear(m0, u, v, p0, nullptr);
+                pbilinear(m1, u, v, p1, nullptr);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) x[c] = (1.0f - tau) * p0[c] + tau * p1[c];
-            bilinear(uvm, u, v, x + 4);
-            bilinear(utm, u, t, x + 8);
-            bilinear(vtm, v, t, x + 10);
+                for (int c = 0; c < 4; ++c) x[c] = (1.0f - tau) * p0[c] + tau * p1[c];
+                pbilinear(muv, u, v, x + 4, nullptr);
+                pbilinear(mut, u, t, x + 8, nullptr);
+                pbilinear(mvt, v, t, x + 10, nullptr);
+                const float* nz = a.noise + ((size_t)r * a.S + s) * 12;   // Eq. 5, alpha = 1/256
+#pragma unroll
+                for (int i = 0; i < 12; ++i) x[i] = fmaf(nz[i], 1.0f / 256.0f, x[i]);
+            } else {
+                Map2D m0{vol + a.uvt_slice_bytes * k0, a.fmt_uvt, a.R3, a.R3, 4};
+                Map2D m1{vol + a.uvt_slice_bytes * k1, a.fmt_uvt, a.R3, a.R3, 4};
+                bilinear(m0, u, v, p0);
+                bilinear(m1, u, v, p1);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) x[c] = (1.0f - tau) * p0[c] + tau * p1[c];
+                bilinear(uvm, u, v, x + 4);
+                bilinear(utm, u, t, x + 8);
+                bilinear(vtm, v, t, x + 10);
+            }
             x[12] = sinpif(t);
             x[13] = cospif(t);
             x[14] = sinpif(2.0f * t);
@@ -172,6 +253,41 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
 #pragma unroll
             for (int o = 0; o < H; ++o) acc = fmaf(W2[o * H + i], dz2[o], acc);
             dz1[i] = act ? acc * gelu_grad_from(z1[i], g1[i], a.gelu) : 0.f;
+        }
+        if constexpr (FULL) {
+            if (act) {   // dL/dx of the 12 sampled features -> the maps' parameters (R28)
+                float gx[12];
+#pragma unroll
+                for (int i = 0; i < 12; ++i) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int o = 0; o < H; ++o) acc = fmaf(W1[o * 16 + i], dz1[o], acc);
+                    gx[i] = acc;
+                }
+                const float* q = a.samples + ((size_t)r * a.S + s) * 3;
+                const float u = q[0], v = q[1], t = q[2];
+                const float sd = t * (float)a.D - 0.5f, fl = floorf(sd), tau = sd - fl;
+                const int k0 = clampi((int)fl, 0, a.D - 1), k1 = clampi((int)fl + 1, 0, a.D - 1);
+                const float* th = a.theta + (size_t)k * a.pfull;
+                float* gg = a.grad + (size_t)r * a.pfull;
+                const size_t sl = (size_t)(a.R3 >> 2) * (a.R3 >> 2) * 24;
+                PMap m0{th + a.off_uvt + sl * k0, gg + a.off_uvt + sl * k0, 1, a.R3, a.R3, 4};
+                PMap m1{th + a.off_uvt + sl * k1, gg + a.off_uvt + sl * k1, 1, a.R3, a.R3, 4};
+                PMap muv{th + a.off_uv, gg + a.off_uv, 1, a.R_uv, a.R_uv, 4};
+                PMap mut{th + a.off_ut, gg + a.off_ut, 0, a.U, a.T, 2};
+                PMap mvt{th + a.off_vt, gg + a.off_vt, 0, a.U, a.T, 2};
+                float g0[4], g1v[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    g0[c] = (1.0f - tau) * gx[c];
+                    g1v[c] = tau * gx[c];
+                }
+                pbilinear(m0, u, v, nullptr, g0);
+                pbilinear(m1, u, v, nullptr, g1v);
+                pbilinear(muv, u, v, nullptr, gx + 4);
+                pbilinear(mut, u, t, nullptr, gx + 8);
+                pbilinear(mvt, v, t, nullptr, gx + 10);
+            }
         }
         // sum over the warp's 32 samples: stage (A, B) = (output-side, input-side)
         // vectors of each layer and let every lane sweep the rows for its components
@@ -249,30 +365,39 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
     accl = warp_sum(accl);
     if (lane == 0) atomicAdd(&sLoss, accl);
     __syncthreads();
-    for (int i = tid; i < P; i += blockDim.x) atomicAdd(a.grad + (size_t)r * P + i, sG[i]);
+    for (int i = tid; i < P; i += blockDim.x) atomicAdd(a.grad + (size_t)r * tstride + i, sG[i]);
     if (tid == 0) atomicAdd(a.loss + r, sLoss / (3.0f * (float)a.S));
 }
 
 // Adam (PyTorch order, bias correction with the tile's own step count)
+// Adam (PyTorch order, bias correction with the tile's own step count); grid
+// (n, chunks); parameters from index `proj` on are projected onto [0,1] (R28)
 __global__ void ndgi_adam_kernel(float* theta, float* m, float* v, int* steps, const float* grad,
-                                 const uint32_t* tile_ids, int n, int P, int num_tiles, float lr, float b1, float b2,
-                                 float eps) {
+                                 const uint32_t* tile_ids, int n, size_t P, int num_tiles, float lr, float b1, float b2,
+                                 float eps, size_t proj) {
     const int r = blockIdx.x;
     const uint32_t k = __ldg(tile_ids + r);
     if (k >= (uint32_t)num_tiles) return;
     const int step = steps[k] + 1;
     const float c1 = 1.0f - powf(b1, (float)step), c2 = 1.0f - powf(b2, (float)step);
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    for (size_t i = blockIdx.y * (size_t)blockDim.x + threadIdx.x; i < P; i += (size_t)gridDim.y * blockDim.x) {
         const size_t e = (size_t)k * P + i;
         const float g = grad[(size_t)r * P + i];
         const float mi = b1 * m[e] + (1.0f - b1) * g;
         const float vi = b2 * v[e] + (1.0f - b2) * g * g;
         m[e] = mi;
         v[e] = vi;
-        theta[e] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+        float th = theta[e] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+        if (i >= proj) th = fminf(fmaxf(th, 0.0f), 1.0f);
+        theta[e] = th;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) steps[k] = step;
+}
+
+__global__ void ndgi_step_count_kernel(int* steps, const uint32_t* tile_ids, int n, int num_tiles) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t k = tile_ids[r];
+    if (k < (uint32_t)num_tiles) steps[k] += 1;
 }
 
 __global__ void ndgi_f16_to_f32_kernel(const uint16_t* in, float* out, size_t n) {
@@ -287,13 +412,20 @@ __global__ void ndgi_f32_to_f16_kernel(const float* in, uint16_t* out, size_t n)
 cudaError_t launch_train_grad(const TrainArgs& a, int H, cudaStream_t s) {
     const unsigned grid = (unsigned)(a.n * a.chunks);
     if (H != 16) return cudaErrorNotSupported;   // h = 64 would spill its activations (future: tensor cores)
-    ndgi_train_grad_kernel<16><<<grid, 128, 0, s>>>(a);
+    if (a.noise) ndgi_train_grad_kernel<16, true><<<grid, 128, 0, s>>>(a);
+    else ndgi_train_grad_kernel<16, false><<<grid, 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_adam(float* theta, float* m, float* v, int* steps, const float* grad, const uint32_t* tile_ids,
-                        int n, int P, int num_tiles, float lr, float b1, float b2, float eps, cudaStream_t s) {
-    ndgi_adam_kernel<<<n, 256, 0, s>>>(theta, m, v, steps, grad, tile_ids, n, P, num_tiles, lr, b1, b2, eps);
+                        int n, size_t P, int num_tiles, float lr, float b1, float b2, float eps, size_t proj,
+                        cudaStream_t s) {
+    const unsigned chunks = (unsigned)((P + 256 * 8 - 1) / (256 * 8));
+    ndgi_adam_kernel<<<dim3(n, chunks), 256, 0, s>>>(theta, m, v, steps, grad, tile_ids, n, P, num_tiles, lr, b1, b2,
+                                                     eps, proj);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ndgi_step_count_kernel<<<(n + 255) / 256, 256, 0, s>>>(steps, tile_ids, n, num_tiles);
     return cudaGetLastError();
 }
 
