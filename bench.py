@@ -570,9 +570,29 @@ def finetune_leg(ndgi, torch, args):
     flops = n * 3 * 2 * (16 * h + h * h + 3 * h)
     fma_peak = 148 * 128 * 2 * _peaks().get("sm_max_mhz", 1965.0) * 1e6 / 1e12   # TFLOP/s fp32 (nominal)
     tr.close()
+    # the full step (R28): BC-simulated maps + line grids + MLP, Eq. 5 noise, projection
+    P = ndgi.train_full_params(lay)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    init = torch.rand((len(tiles), P), device="cuda", generator=g)
+    init[:, :tr.P] = (init[:, :tr.P] - 0.5) * 0.6
+    noise = torch.rand((len(tiles), Sn, 12), device="cuda", generator=g) - 0.5
+    tf = ndgi.Trainer(ctx, full_init=init)
+    for _ in range(2):
+        tf.step(ids, smp_t, tgt_t, 1e-3, None, stream, noise)
+    e0.record(stream)
+    for _ in range(reps):
+        tf.step(ids, smp_t, tgt_t, 1e-3, None, stream, noise)
+    e1.record(stream)
+    e1.synchronize()
+    sf = e0.elapsed_time(e1) / reps * 1e-3
+    tf.close()
+    ctx.close()
     return {"workload": "1024 tiles x 4096 samples (c2, BC7 features), forward + backward + Adam, h = 16",
             "ms_per_step": s_ * 1e3, "msample_s": n / s_ / 1e6,
-            "mlp_tflops": flops / s_ / 1e12, "fp32_peak_tflops": fma_peak, "frac": flops / s_ / 1e12 / fma_peak}
+            "mlp_tflops": flops / s_ / 1e12, "fp32_peak_tflops": fma_peak, "frac": flops / s_ / 1e12 / fma_peak,
+            "full": {"workload": f"same batch, full step (R28): {P} fp32 parameters per tile "
+                                 "(MLP + BC-simulated maps + line grids), Eq. 5 noise, Adam + [0,1] projection",
+                     "ms_per_step": sf * 1e3, "msample_s": n / sf / 1e6}}
 
 
 def main():

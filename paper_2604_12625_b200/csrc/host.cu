@@ -555,8 +555,10 @@ struct ndgi_train {
     size_t P;                      // parameters per tile
     size_t off_uv, off_uvt, off_ut, off_vt;
     float *theta, *m, *v, *grad, *loss;
+    float* dtex;                   // full: per-row texel gradients [cap][dtex_stride]
+    size_t dtex_stride;
     int* steps;
-    uint32_t cap;                  // batch capacity of grad / loss
+    uint32_t cap;                  // batch capacity of grad / loss / dtex
 };
 
 namespace {
@@ -592,6 +594,11 @@ ndgi_status train_create(ndgi_ctx* ctx, bool full, const float* init, ndgi_train
     t->off_uvt = off[1];
     t->off_ut = off[2];
     t->off_vt = off[3];
+    t->dtex_stride = full ? (size_t)ctx->L.uv_res * ctx->L.uv_res * 4 +
+                                (size_t)ctx->L.uvt_depth * ctx->L.uvt_res * ctx->L.uvt_res * 4 +
+                                (size_t)ctx->L.line_t * ctx->L.line_res * 4
+                          : 0;
+    t->dtex_stride = (t->dtex_stride + 3) & ~(size_t)3;
     const size_t n = (size_t)ctx->L.num_tiles * t->P;
     cudaError_t e = cudaMalloc(&t->theta, n * 4);
     if (e == cudaSuccess) e = cudaMalloc(&t->m, n * 4);
@@ -630,15 +637,24 @@ ndgi_status train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, cons
     if (n > t->cap) {
         cudaFree(t->grad);
         cudaFree(t->loss);
+        cudaFree(t->dtex);
         t->grad = nullptr;
         t->loss = nullptr;
+        t->dtex = nullptr;
         t->cap = 0;
         e = cudaMalloc(&t->grad, (size_t)n * t->P * 4);
         if (e == cudaSuccess) e = cudaMalloc(&t->loss, (size_t)n * 4);
+        if (e == cudaSuccess && t->full) e = cudaMalloc(&t->dtex, (size_t)n * t->dtex_stride * 4);
         if (e != cudaSuccess) return cuda_fail(e, "train scratch");
         t->cap = n;
     }
-    e = cudaMemsetAsync(t->grad, 0, (size_t)n * t->P * 4, s);
+    if (t->full) {   // the MLP part takes atomics; ndgi_bc_grad_kernel writes the rest
+        const size_t pm = mlp_elems(ctx->L.hidden);
+        e = cudaMemset2DAsync(t->grad, t->P * 4, 0, pm * 4, n, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(t->dtex, 0, (size_t)n * t->dtex_stride * 4, s);
+    } else {
+        e = cudaMemsetAsync(t->grad, 0, (size_t)n * t->P * 4, s);
+    }
     if (e == cudaSuccess) e = cudaMemsetAsync(t->loss, 0, (size_t)n * 4, s);
     if (e != cudaSuccess) return cuda_fail(e, "train scratch clear");
     const ndgi_layout& L = ctx->L;
@@ -680,6 +696,8 @@ ndgi_status train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, cons
     a.off_uvt = t->off_uvt;
     a.off_ut = t->off_ut;
     a.off_vt = t->off_vt;
+    a.dtex = t->dtex;
+    a.dtex_stride = t->dtex_stride;
     e = ndgi::launch_train_grad(a, (int)L.hidden, s);
     if (e == cudaSuccess)
         e = ndgi::launch_adam(t->theta, t->m, t->v, t->steps, t->grad, tile_ids, (int)n, t->P, (int)L.num_tiles, lr,
@@ -754,6 +772,7 @@ ndgi_status ndgi_train_free(ndgi_train* t) {
     cudaFree(t->steps);
     cudaFree(t->grad);
     cudaFree(t->loss);
+    cudaFree(t->dtex);
     delete t;
     return NDGI_OK;
 }

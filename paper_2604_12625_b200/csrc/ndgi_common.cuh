@@ -93,6 +93,10 @@ struct TrainArgs {
     // FULL (R28): BC-simulated maps + line grids in theta after the MLP; noise [n][S][12]
     const float* noise;
     size_t pfull, off_uv, off_uvt, off_ut, off_vt;
+    // FULL: per batch row, dL/d(texel) of each map, vector atomics:
+    // [R_uv^2][4] | [D][R3^2][4] | [T][U][2] (ut) | [T][U][2] (vt)
+    float* dtex;
+    size_t dtex_stride;
     float* grad;                // [n][P] (zeroed by the host)
     float* loss;                // [n] (zeroed by the host), mean squared error
     uint32_t* err;

@@ -49,9 +49,13 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ---- R28: BC-simulated / plain parameter maps (full training) ----------------
+// Forward: texels of a BC-simulated map come from Eq. 7 per tap.  Backward:
+// dL/d(texel) goes to a per-row texel-gradient buffer with one vector atomic
+// per tap (red.global.add.v4/v2.f32); ndgi_bc_grad_kernel then turns each
+// 4x4 block's 16 texel gradients into the gradients of e1, e2 and w_p.
 struct PMap {
     const float* p;   // parameters
-    float* g;         // their gradient (global, atomics)
+    float* g;         // texel gradient buffer (global, atomics)
     int bc, rx, ry, nc;
 };
 
@@ -64,21 +68,13 @@ __device__ __forceinline__ float pfetch(const PMap& m, int a, int b, int c) {
     return __ldg(m.p + ((size_t)b * m.rx + a) * m.nc + c);
 }
 
-__device__ __forceinline__ void pscatter(const PMap& m, int a, int b, const float* gv) {
-    if (m.bc) {
-        const size_t base = ((size_t)(b >> 2) * (m.rx >> 2) + (a >> 2)) * 24;
-        const int pi = 4 * (b & 3) + (a & 3);
-        const float w = __ldg(m.p + base + 8 + pi);
-        float gw = 0.f;
-        for (int c = 0; c < m.nc; ++c) {
-            atomicAdd(m.g + base + c, gv[c] * (1.0f - w));
-            atomicAdd(m.g + base + 4 + c, gv[c] * w);
-            gw = fmaf(gv[c], __ldg(m.p + base + 4 + c) - __ldg(m.p + base + c), gw);
-        }
-        atomicAdd(m.g + base + 8 + pi, gw);
-        return;
+__device__ __forceinline__ void pscatter(const PMap& m, int a, int b, float wt, const float* gout) {
+    if (m.nc == 4) {
+        atomicAdd(reinterpret_cast<float4*>(m.g) + ((size_t)b * m.rx + a),
+                  make_float4(wt * gout[0], wt * gout[1], wt * gout[2], wt * gout[3]));
+    } else {
+        atomicAdd(reinterpret_cast<float2*>(m.g) + ((size_t)b * m.rx + a), make_float2(wt * gout[0], wt * gout[1]));
     }
-    for (int c = 0; c < m.nc; ++c) atomicAdd(m.g + ((size_t)b * m.rx + a) * m.nc + c, gv[c]);
 }
 
 // bilinear (R1) forward, or the backward scatter of gout (weights per tap)
@@ -90,15 +86,10 @@ __device__ __forceinline__ void pbilinear(const PMap& m, float a, float b, float
     const int y0 = clampi((int)fy0, 0, m.ry - 1), y1 = clampi((int)fy0 + 1, 0, m.ry - 1);
     const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy), w01 = (1.f - fx) * fy, w11 = fx * fy;
     if (gout) {
-        float g[4];
-        for (int c = 0; c < m.nc; ++c) g[c] = w00 * gout[c];
-        pscatter(m, x0, y0, g);
-        for (int c = 0; c < m.nc; ++c) g[c] = w10 * gout[c];
-        pscatter(m, x1, y0, g);
-        for (int c = 0; c < m.nc; ++c) g[c] = w01 * gout[c];
-        pscatter(m, x0, y1, g);
-        for (int c = 0; c < m.nc; ++c) g[c] = w11 * gout[c];
-        pscatter(m, x1, y1, g);
+        pscatter(m, x0, y0, w00, gout);
+        pscatter(m, x1, y0, w10, gout);
+        pscatter(m, x0, y1, w01, gout);
+        pscatter(m, x1, y1, w11, gout);
         return;
     }
     for (int c = 0; c < m.nc; ++c)
@@ -269,13 +260,15 @@ __global__ void __launch_bounds__(128) ndgi_train_grad_kernel(const __grid_const
                 const float sd = t * (float)a.D - 0.5f, fl = floorf(sd), tau = sd - fl;
                 const int k0 = clampi((int)fl, 0, a.D - 1), k1 = clampi((int)fl + 1, 0, a.D - 1);
                 const float* th = a.theta + (size_t)k * a.pfull;
-                float* gg = a.grad + (size_t)r * a.pfull;
-                const size_t sl = (size_t)(a.R3 >> 2) * (a.R3 >> 2) * 24;
-                PMap m0{th + a.off_uvt + sl * k0, gg + a.off_uvt + sl * k0, 1, a.R3, a.R3, 4};
-                PMap m1{th + a.off_uvt + sl * k1, gg + a.off_uvt + sl * k1, 1, a.R3, a.R3, 4};
-                PMap muv{th + a.off_uv, gg + a.off_uv, 1, a.R_uv, a.R_uv, 4};
-                PMap mut{th + a.off_ut, gg + a.off_ut, 0, a.U, a.T, 2};
-                PMap mvt{th + a.off_vt, gg + a.off_vt, 0, a.U, a.T, 2};
+                float* gt = a.dtex + (size_t)r * a.dtex_stride;
+                const size_t sl = (size_t)(a.R3 >> 2) * (a.R3 >> 2) * 24, tsl = (size_t)a.R3 * a.R3 * 4;
+                const size_t t_uvt = (size_t)a.R_uv * a.R_uv * 4, t_ut = t_uvt + tsl * a.D,
+                             t_vt = t_ut + (size_t)a.T * a.U * 2;
+                PMap m0{th + a.off_uvt + sl * k0, gt + t_uvt + tsl * k0, 1, a.R3, a.R3, 4};
+                PMap m1{th + a.off_uvt + sl * k1, gt + t_uvt + tsl * k1, 1, a.R3, a.R3, 4};
+                PMap muv{th + a.off_uv, gt, 1, a.R_uv, a.R_uv, 4};
+                PMap mut{th + a.off_ut, gt + t_ut, 0, a.U, a.T, 2};
+                PMap mvt{th + a.off_vt, gt + t_vt, 0, a.U, a.T, 2};
                 float g0[4], g1v[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -393,6 +386,63 @@ __global__ void ndgi_adam_kernel(float* theta, float* m, float* v, int* steps, c
     }
 }
 
+// R28 backward through Eq. 7: texel p of a block = (1 - w_p) e1 + w_p e2, so
+// dL/de1 = sum_p (1 - w_p) dF_p, dL/de2 = sum_p w_p dF_p, dL/dw_p = dF_p . (e2 - e1).
+// Grid (n, chunks), one thread per 4x4 block (F_uv's, then every F_uvt
+// slice's), then the line grids' gradients (= their texel gradients) copied.
+__global__ void ndgi_bc_grad_kernel(const TrainArgs a) {
+    const int r = blockIdx.x;
+    const uint32_t k = __ldg(a.tile_ids + r);
+    if (k >= (uint32_t)a.num_tiles) return;
+    const float* th = a.theta + (size_t)k * a.pfull;
+    float* gg = a.grad + (size_t)r * a.pfull;
+    const float* gt = a.dtex + (size_t)r * a.dtex_stride;
+    const int nbu = a.R_uv >> 2, nb3 = a.R3 >> 2;
+    const size_t n_uv = (size_t)nbu * nbu, n_uvt = (size_t)nb3 * nb3 * a.D, n_line = (size_t)a.T * a.U * 2;
+    const size_t t_uvt = (size_t)a.R_uv * a.R_uv * 4, t_ut = t_uvt + (size_t)a.R3 * a.R3 * 4 * a.D;
+    const size_t total = n_uv + n_uvt + 2 * n_line;
+    for (size_t i = blockIdx.y * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.y * blockDim.x) {
+        if (i >= n_uv + n_uvt) {   // line grids
+            const size_t j = i - n_uv - n_uvt;
+            gg[(j < n_line ? a.off_ut + j : a.off_vt + (j - n_line))] = gt[t_ut + j];
+            continue;
+        }
+        const bool uv = i < n_uv;
+        const size_t b = uv ? i : i - n_uv;
+        const int nb = uv ? nbu : nb3, R = uv ? a.R_uv : a.R3;
+        const size_t slice = b / ((size_t)nb * nb), bi = b % ((size_t)nb * nb);
+        const int bx = (int)(bi % nb), by = (int)(bi / nb);
+        const float* blk = th + (uv ? a.off_uv : a.off_uvt) + b * 24;
+        float* gb = gg + (uv ? a.off_uv : a.off_uvt) + b * 24;
+        const float4* tex = reinterpret_cast<const float4*>(gt + (uv ? 0 : t_uvt + slice * (size_t)R * R * 4));
+        float e1[4], d[4], g1[4] = {0.f, 0.f, 0.f, 0.f}, g2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            e1[c] = blk[c];
+            d[c] = blk[4 + c] - e1[c];
+        }
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            const float4 f = tex[(size_t)(4 * by + (p >> 2)) * R + 4 * bx + (p & 3)];
+            const float w = blk[8 + p];
+            g1[0] = fmaf(1.0f - w, f.x, g1[0]);
+            g1[1] = fmaf(1.0f - w, f.y, g1[1]);
+            g1[2] = fmaf(1.0f - w, f.z, g1[2]);
+            g1[3] = fmaf(1.0f - w, f.w, g1[3]);
+            g2[0] = fmaf(w, f.x, g2[0]);
+            g2[1] = fmaf(w, f.y, g2[1]);
+            g2[2] = fmaf(w, f.z, g2[2]);
+            g2[3] = fmaf(w, f.w, g2[3]);
+            gb[8 + p] = f.x * d[0] + f.y * d[1] + f.z * d[2] + f.w * d[3];
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            gb[c] = g1[c];
+            gb[4 + c] = g2[c];
+        }
+    }
+}
+
 __global__ void ndgi_step_count_kernel(int* steps, const uint32_t* tile_ids, int n, int num_tiles) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
@@ -412,8 +462,17 @@ __global__ void ndgi_f32_to_f16_kernel(const float* in, uint16_t* out, size_t n)
 cudaError_t launch_train_grad(const TrainArgs& a, int H, cudaStream_t s) {
     const unsigned grid = (unsigned)(a.n * a.chunks);
     if (H != 16) return cudaErrorNotSupported;   // h = 64 would spill its activations (future: tensor cores)
-    if (a.noise) ndgi_train_grad_kernel<16, true><<<grid, 128, 0, s>>>(a);
-    else ndgi_train_grad_kernel<16, false><<<grid, 128, 0, s>>>(a);
+    if (!a.noise) {
+        ndgi_train_grad_kernel<16, false><<<grid, 128, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    ndgi_train_grad_kernel<16, true><<<grid, 128, 0, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t blocks = (size_t)(a.R_uv >> 2) * (a.R_uv >> 2) + (size_t)(a.R3 >> 2) * (a.R3 >> 2) * a.D +
+                          (size_t)a.T * a.U * 4;
+    const unsigned chunks = (unsigned)((blocks + 255) / 256);
+    ndgi_bc_grad_kernel<<<dim3(a.n, chunks), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 
