@@ -19,6 +19,10 @@ Recipe (DESIGN.md "Input recipe"):
   other bits random (bit-exactness stress, worst-case divergence);
 * U8 / F16 maps: the smooth field quantised to u8 (F16 = fp16(q/255));
 * line maps F_ut / F_vt: smooth u8 fields over (space, time), [T][U][2];
+* BC1 / BC3 / BC5 payloads (R29, config 5's BC-format axis): endpoints
+  bracket the same smooth field at block resolution (+-delta), endpoint
+  order hashed (both BC1 colour modes, both BC4 palettes), indices hashed;
+  "mixed" = all bits random;
 * MLP: PyTorch nn.Linear default init U(+-1/sqrt(fan_in)) for W and b,
   b3 += 0.5, rounded to f16 (R11).
 """
@@ -54,7 +58,8 @@ def config(name: str) -> tuple[dict, int]:
     c1: one 256^2 lightmap = 2x2 tiles, few keyframes (D=4, T=4), profile M
     c2: one 4096^2 atlas = 32x32 tiles, profile M (Table 1 shapes)
     c3/c4: 4 x 8192^2 atlases = 16384 tiles, profile M (FarmLand scale)
-    c5:<profile>:<fmt>: c2's atlas with profile in {L,M,H,M64}, fmt in {bc7,u8,f16}
+    c5:<profile>:<fmt>: c2's atlas with profile in {L,M,H,M64}, fmt in {bc7,bc3,bc1,u8,f16}
+        (line maps: u8 with bc7, BC5 with bc3 / bc1, else the same format)
     """
     if name == "c1":
         return layout(1, 2, 2, "M", uvt_depth=4, line_t=4), 1000
@@ -66,7 +71,8 @@ def config(name: str) -> tuple[dict, int]:
         return layout(4, 64, 64, "M"), 4000
     if name.startswith("c5"):
         _, prof, fmt = name.split(":")
-        return layout(1, 32, 32, prof, fmt_uv=fmt, fmt_uvt=fmt, fmt_line="u8" if fmt == "bc7" else fmt), 5000
+        line = {"bc7": "u8", "bc1": "bc5", "bc3": "bc5"}.get(fmt, fmt)
+        return layout(1, 32, 32, prof, fmt_uv=fmt, fmt_uvt=fmt, fmt_line=line), 5000
     raise KeyError(name)
 
 
@@ -212,6 +218,59 @@ def _bc7_map(seed, stream, tiles, R, nslices, payload):
     return out
 
 
+BCN_BLOCK_BYTES = {"bc1": 8, "bc3": 16, "bc5": 16}
+
+
+def _bcn_map(seed, stream, tiles, rx, ry, nslices, fmt, payload):
+    """[tiles][nslices][ry/4][rx/4][8 or 16] BC1 / BC3 / BC5 blocks (layouts
+    in include/ndgi.h): packed from chosen endpoints and hashed indices."""
+    nbx, nby = rx // 4, ry // 4
+    nb = nbx * nby
+    bsz = BCN_BLOCK_BYTES[fmt]
+    nw = bsz // 8
+    keys = _tile_keys(seed, stream + 200, tiles)
+    if payload == "mixed":
+        w = _hash(keys, nslices * nb * nw)
+        return w.view(np.uint8).reshape(len(tiles), nslices, nby, nbx, bsz)
+    nch = 2 if fmt == "bc5" else 4
+    a, b, phi = _field_params(seed, stream, tiles, nch)
+    xs = np.tile((np.arange(nbx) + 0.5) / nbx, nby)
+    ys = np.repeat((np.arange(nby) + 0.5) / nby, nbx)
+    out = np.empty((len(tiles), nslices, nb, nw), np.uint64)
+    words = _hash(keys, nslices * nb * 4).reshape(len(tiles), nslices, nb, 4)
+    for s in range(nslices):
+        m = _smooth(a, b, phi + 0.7 * s, xs, ys)                       # [tiles][nb][nch]
+        d = (0.02 + 0.10 * _unif(words[:, s, :, 0])[..., None]).astype(np.float32)
+        lo = np.clip(np.rint((m - d) * 255), 0, 255).astype(np.uint64)
+        hi = np.clip(np.rint((m + d) * 255), 0, 255).astype(np.uint64)
+        sw = words[:, s, :, 1]                                         # endpoint-order bits
+
+        def bc4(c, bit):
+            e0, e1 = lo[..., c], hi[..., c]
+            swap = ((sw >> np.uint64(bit)) & np.uint64(1)).astype(bool)
+            a0, a1 = np.where(swap, e1, e0), np.where(swap, e0, e1)
+            return a0 | (a1 << np.uint64(8)) | ((words[:, s, :, 2 + (bit & 1)] >> np.uint64(16)) << np.uint64(16))
+
+        def bc1():
+            c = [(lo[..., 0] >> np.uint64(3) << np.uint64(11)) | (lo[..., 1] >> np.uint64(2) << np.uint64(5)) |
+                 (lo[..., 2] >> np.uint64(3)),
+                 (hi[..., 0] >> np.uint64(3) << np.uint64(11)) | (hi[..., 1] >> np.uint64(2) << np.uint64(5)) |
+                 (hi[..., 2] >> np.uint64(3))]
+            swap = (sw & np.uint64(1)).astype(bool)
+            c0, c1 = np.where(swap, c[1], c[0]), np.where(swap, c[0], c[1])
+            return c0 | (c1 << np.uint64(16)) | ((words[:, s, :, 2] >> np.uint64(32)) << np.uint64(32))
+
+        if fmt == "bc1":
+            out[:, s, :, 0] = bc1()
+        elif fmt == "bc3":
+            out[:, s, :, 0] = bc4(3, 1)
+            out[:, s, :, 1] = bc1()
+        else:
+            out[:, s, :, 0] = bc4(0, 2)
+            out[:, s, :, 1] = bc4(1, 3)
+    return out.view(np.uint8).reshape(len(tiles), nslices, nby, nbx, bsz)
+
+
 def _dense_map(seed, stream, tiles, rx, ry, nch, nslices, fmt):
     """[tiles][nslices][ry][rx][nch] u8 (or f16 of q/255) smooth field."""
     a, b, phi = _field_params(seed, stream, tiles, nch)
@@ -253,15 +312,23 @@ def make_theta(lay: dict, seed: int, payload: str = "smooth", tiles=None) -> dic
     th = {}
     if lay["fmt_uv"] == "bc7":
         th["uv"] = _bc7_map(seed, 1, tiles, R, 1, payload).reshape(len(tiles), R // 4, R // 4, 16)
+    elif lay["fmt_uv"] in BCN_BLOCK_BYTES:
+        th["uv"] = _bcn_map(seed, 1, tiles, R, R, 1, lay["fmt_uv"], payload)[:, 0]
     else:
         th["uv"] = _dense_map(seed, 1, tiles, R, R, 4, 1, lay["fmt_uv"]).reshape(len(tiles), R, R, 4)
     if lay["fmt_uvt"] == "bc7":
         th["uvt"] = _bc7_map(seed, 2, tiles, R3, D, payload)
+    elif lay["fmt_uvt"] in BCN_BLOCK_BYTES:
+        th["uvt"] = _bcn_map(seed, 2, tiles, R3, R3, D, lay["fmt_uvt"], payload)
     else:
         th["uvt"] = _dense_map(seed, 2, tiles, R3, R3, 4, D, lay["fmt_uvt"])
     U, T = lay["line_res"], lay["line_t"]
-    th["ut"] = _dense_map(seed, 3, tiles, U, T, 2, 1, lay["fmt_line"]).reshape(len(tiles), T, U, 2)
-    th["vt"] = _dense_map(seed, 4, tiles, U, T, 2, 1, lay["fmt_line"]).reshape(len(tiles), T, U, 2)
+    if lay["fmt_line"] == "bc5":
+        th["ut"] = _bcn_map(seed, 3, tiles, U, T, 1, "bc5", payload)[:, 0]
+        th["vt"] = _bcn_map(seed, 4, tiles, U, T, 1, "bc5", payload)[:, 0]
+    else:
+        th["ut"] = _dense_map(seed, 3, tiles, U, T, 2, 1, lay["fmt_line"]).reshape(len(tiles), T, U, 2)
+        th["vt"] = _dense_map(seed, 4, tiles, U, T, 2, 1, lay["fmt_line"]).reshape(len(tiles), T, U, 2)
     th["mlp"] = _mlp(seed, tiles, lay["hidden"])
     return th
 
@@ -269,7 +336,9 @@ def make_theta(lay: dict, seed: int, payload: str = "smooth", tiles=None) -> dic
 def theta_bytes(lay: dict) -> int:
     """Whole-Theta bytes per tile (all t), for BPP accounting."""
     def b2(fmt, rx, ry, nc):
-        return (rx // 4) * (ry // 4) * 16 if fmt == "bc7" else rx * ry * nc * (1 if fmt == "u8" else 2)
+        if fmt == "bc7" or fmt in BCN_BLOCK_BYTES:
+            return (rx // 4) * (ry // 4) * BCN_BLOCK_BYTES.get(fmt, 16)
+        return rx * ry * nc * (1 if fmt == "u8" else 2)
     h = lay["hidden"]
     return (b2(lay["fmt_uv"], lay["uv_res"], lay["uv_res"], 4)
             + lay["uvt_depth"] * b2(lay["fmt_uvt"], lay["uvt_res"], lay["uvt_res"], 4)

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ndgi_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-FMT = {"bc7": 0, "u8": 1, "f16": 2}
+FMT = {"bc7": 0, "u8": 1, "f16": 2, "bc1": 3, "bc3": 4, "bc5": 5}
 GELU = {"erf": 0, "tanh": 1}
 BORDER = {"mirror": 0, "eval_clamp": 1}
 
@@ -59,6 +59,10 @@ def lib():
             "oracle_half_to_double": (D, [C.c_uint16]),
             "oracle_bc7_decode_block": (I, [P, P]),
             "oracle_bc7_decode_image": (None, [P, I, I, P]),
+            "oracle_bc1_decode_block": (None, [P, P, I]),
+            "oracle_bc4_decode_block": (None, [P, P]),
+            "oracle_bc3_decode_block": (None, [P, P]),
+            "oracle_bc5_decode_block": (None, [P, P]),
             "oracle_bc7_weight": (I, [I, I]),
             "oracle_bc7_subset": (I, [I, I, I]),
             "oracle_bc7_anchor": (I, [I, I, I]),
@@ -111,6 +115,20 @@ def bc7_decode_image(blocks: np.ndarray, w: int, h: int) -> np.ndarray:
     out = np.zeros((h, w, 4), np.uint8)
     lib().oracle_bc7_decode_image(_ptr(b), w, h, _ptr(out))
     return out
+
+
+def bcn_decode_block(fmt: str, block) -> np.ndarray:
+    """R29: one BC1 / BC3 / BC4 / BC5 block -> [16][channels] uint8
+    (BC1, BC3: RGBA; BC4: 1 channel; BC5: 2 channels); texel = 4*row + col."""
+    b = np.frombuffer(bytes(block), np.uint8).copy()
+    assert len(b) == (8 if fmt in ("bc1", "bc4") else 16)
+    nch = {"bc1": 4, "bc3": 4, "bc4": 1, "bc5": 2}[fmt]
+    out = np.zeros(16 * nch, np.uint8)
+    if fmt == "bc1":
+        lib().oracle_bc1_decode_block(_ptr(b), _ptr(out), 0)
+    else:
+        getattr(lib(), f"oracle_{fmt}_decode_block")(_ptr(b), _ptr(out))
+    return out.reshape(16, nch)
 
 
 def bc7_weight(bits: int, index: int) -> int:

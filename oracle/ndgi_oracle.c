@@ -18,8 +18,8 @@
  * with GELU on the hidden layers and a linear output, weights
  * stored as f16 (R11).
  *
- * Pins (tests/test_oracle_*.py): BC7 against Pillow's independent BCn
- * decoder and hand vectors; samplers against torch grid_sample; MLP against
+ * Pins (tests/test_oracle_*.py): BC7 (and BC1/BC3/BC4/BC5) against
+ * Pillow's independent BCn decoder and hand vectors; samplers against torch grid_sample; MLP against
  * torch F.linear/F.gelu in fp64; gamma against closed forms;
  * border against torch F.pad(mode="reflect"); the whole pipeline against a
  * composition of those library routines.
@@ -34,7 +34,7 @@
 /* Layout (the oracle's own struct; mirrors the meaning, not the code, of
  * include/ndgi.h).                                                     */
 /* ------------------------------------------------------------------ */
-enum { OR_FMT_BC7 = 0, OR_FMT_U8 = 1, OR_FMT_F16 = 2 };
+enum { OR_FMT_BC7 = 0, OR_FMT_U8 = 1, OR_FMT_F16 = 2, OR_FMT_BC1 = 3, OR_FMT_BC3 = 4, OR_FMT_BC5 = 5 };
 enum { OR_GELU_ERF = 0, OR_GELU_TANH = 1 };
 enum { OR_BORDER_MIRROR = 0, OR_BORDER_EVAL_CLAMP = 1 };
 
@@ -292,6 +292,91 @@ void oracle_bc7_decode_image(const uint8_t *blocks, int w, int h, uint8_t *rgba)
 }
 
 /* ------------------------------------------------------------------ */
+/* BC1 / BC4 and their combinations BC3, BC5 ("DXTC spans BC1     */
+/* through BC7 ... BC5 for normal maps"; reading   */
+/* R29).  D3D11 block layouts, little-endian; the interpolated palette */
+/* entries use integer division (truncation), as Pillow's decoder does.*/
+/* ------------------------------------------------------------------ */
+
+/* BC1 colour block (8 bytes): c0, c1 as RGB565 (u16 LE at bytes 0, 2),
+ * then 16 2-bit indices (u32 LE at byte 4, texel i = 4*row+col at bits
+ * 2i).  565 -> 888 by bit replication.  c0 > c1 (or always, for the
+ * colour half of BC3): palette c0, c1, (2c0+c1)/3, (c0+2c1)/3; else
+ * c0, c1, (c0+c1)/2, transparent black (0,0,0,0).  A = 255 otherwise. */
+void oracle_bc1_decode_block(const uint8_t blk[8], uint8_t out[64], int always_four)
+{
+    int c[2] = {blk[0] | (blk[1] << 8), blk[2] | (blk[3] << 8)};
+    int pal[4][4];
+    for (int e = 0; e < 2; ++e) {
+        pal[e][0] = expand8(c[e] >> 11, 5);
+        pal[e][1] = expand8((c[e] >> 5) & 63, 6);
+        pal[e][2] = expand8(c[e] & 31, 5);
+        pal[e][3] = 255;
+    }
+    int four = always_four || c[0] > c[1];
+    for (int ch = 0; ch < 3; ++ch) {
+        if (four) {
+            pal[2][ch] = (2 * pal[0][ch] + pal[1][ch]) / 3;
+            pal[3][ch] = (pal[0][ch] + 2 * pal[1][ch]) / 3;
+        } else {
+            pal[2][ch] = (pal[0][ch] + pal[1][ch]) / 2;
+            pal[3][ch] = 0;
+        }
+    }
+    pal[2][3] = 255;
+    pal[3][3] = four ? 255 : 0;
+    uint32_t idx = (uint32_t)blk[4] | ((uint32_t)blk[5] << 8) | ((uint32_t)blk[6] << 16) | ((uint32_t)blk[7] << 24);
+    for (int i = 0; i < 16; ++i) {
+        int q = (idx >> (2 * i)) & 3;
+        for (int ch = 0; ch < 4; ++ch) out[4 * i + ch] = (uint8_t)pal[q][ch];
+    }
+}
+
+/* BC4 (unsigned) block (8 bytes): a0, a1 (bytes 0, 1), then 16 3-bit
+ * indices (48 bits LE from byte 2, texel i at bits 3i).  a0 > a1:
+ * palette a0, a1, ((8-j) a0 + (j-1) a1) / 7 for j = 2..7; else a0, a1,
+ * ((6-j) a0 + (j-1) a1) / 5 for j = 2..5, then 0 and 255.              */
+void oracle_bc4_decode_block(const uint8_t blk[8], uint8_t out[16])
+{
+    int a0 = blk[0], a1 = blk[1], pal[8];
+    pal[0] = a0;
+    pal[1] = a1;
+    if (a0 > a1) {
+        for (int j = 2; j < 8; ++j) pal[j] = ((8 - j) * a0 + (j - 1) * a1) / 7;
+    } else {
+        for (int j = 2; j < 6; ++j) pal[j] = ((6 - j) * a0 + (j - 1) * a1) / 5;
+        pal[6] = 0;
+        pal[7] = 255;
+    }
+    uint64_t idx = 0;
+    for (int b = 0; b < 6; ++b) idx |= (uint64_t)blk[2 + b] << (8 * b);
+    for (int i = 0; i < 16; ++i) out[i] = (uint8_t)pal[(idx >> (3 * i)) & 7];
+}
+
+/* BC3 (16 bytes): a BC4 block for A, then a BC1 colour block for RGB
+ * decoded in four-colour mode whatever the endpoint order.             */
+void oracle_bc3_decode_block(const uint8_t blk[16], uint8_t out[64])
+{
+    uint8_t a[16];
+    oracle_bc1_decode_block(blk + 8, out, 1);
+    oracle_bc4_decode_block(blk, a);
+    for (int i = 0; i < 16; ++i) out[4 * i + 3] = a[i];
+}
+
+/* BC5 (16 bytes): BC4 blocks for channel 0 (R) then channel 1 (G);
+ * out = 16 texels x 2 channels.                                        */
+void oracle_bc5_decode_block(const uint8_t blk[16], uint8_t out[32])
+{
+    uint8_t r[16], g[16];
+    oracle_bc4_decode_block(blk, r);
+    oracle_bc4_decode_block(blk + 8, g);
+    for (int i = 0; i < 16; ++i) {
+        out[2 * i] = r[i];
+        out[2 * i + 1] = g[i];
+    }
+}
+
+/* ------------------------------------------------------------------ */
 /* Feature fetch and sampling (readings R1, R2, R4, R5, R8).    */
 /* ------------------------------------------------------------------ */
 
@@ -303,11 +388,16 @@ typedef struct { const uint8_t *base; int fmt, rx, ry, nc; } map2d;
  * F16).  BC7: the whole block is decoded for every fetch.             */
 static double fetch(const map2d *m, int a, int b, int c)
 {
-    if (m->fmt == OR_FMT_BC7) {
+    if (m->fmt == OR_FMT_BC7 || m->fmt == OR_FMT_BC1 || m->fmt == OR_FMT_BC3 || m->fmt == OR_FMT_BC5) {
         uint8_t tex[64];
-        const uint8_t *blk = m->base + 16 * ((b / 4) * (m->rx / 4) + (a / 4));
-        oracle_bc7_decode_block(blk, tex);
-        return tex[4 * (4 * (b % 4) + (a % 4)) + c] / 255.0;
+        size_t bsz = m->fmt == OR_FMT_BC1 ? 8 : 16;
+        const uint8_t *blk = m->base + bsz * ((b / 4) * (m->rx / 4) + (a / 4));
+        if (m->fmt == OR_FMT_BC7) oracle_bc7_decode_block(blk, tex);
+        else if (m->fmt == OR_FMT_BC1) oracle_bc1_decode_block(blk, tex, 0);
+        else if (m->fmt == OR_FMT_BC3) oracle_bc3_decode_block(blk, tex);
+        else oracle_bc5_decode_block(blk, tex);
+        int nch = m->fmt == OR_FMT_BC5 ? 2 : 4;
+        return tex[nch * (4 * (b % 4) + (a % 4)) + c] / 255.0;   /* R8: q/255 */
     }
     size_t k = ((size_t)b * m->rx + a) * m->nc + c;
     if (m->fmt == OR_FMT_U8) return m->base[k] / 255.0;
@@ -341,7 +431,8 @@ void oracle_sample2d(const uint8_t *base, int fmt, int rx, int ry, int nc, doubl
 
 static size_t bytes_2d(int fmt, int rx, int ry, int nc)
 {
-    if (fmt == OR_FMT_BC7) return (size_t)(rx / 4) * (ry / 4) * 16;
+    if (fmt == OR_FMT_BC7 || fmt == OR_FMT_BC3 || fmt == OR_FMT_BC5) return (size_t)(rx / 4) * (ry / 4) * 16;
+    if (fmt == OR_FMT_BC1) return (size_t)(rx / 4) * (ry / 4) * 8;
     return (size_t)rx * ry * nc * (fmt == OR_FMT_U8 ? 1 : 2);
 }
 
