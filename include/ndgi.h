@@ -64,7 +64,19 @@ typedef enum {
 typedef enum {
     NDGI_FMT_BC7 = 0, /* 16-byte BC7 blocks, UNORM, value = q/255            */
     NDGI_FMT_U8 = 1,  /* raw 8-bit texels, value = q/255                     */
-    NDGI_FMT_F16 = 2  /* IEEE binary16 texels, value as stored               */
+    NDGI_FMT_F16 = 2, /* IEEE binary16 texels, value as stored               */
+    /* The other DXTC formats ("BC1 through BC7 ... BC5 for normal maps";
+     * SURVEY.md §8(f) NEXT 2, config 5's BC-format axis; reading R29).
+     * Blocks row-major, texel i = 4*row + col, little-endian fields, UNORM
+     * value = q/255; interpolated palette entries use integer division.   */
+    NDGI_FMT_BC1 = 3, /* 8-byte blocks, 4-channel maps (F_uv, F_uvt): c0, c1
+                         RGB565, 2-bit indices; c0 > c1: 4 colours, else 3 +
+                         transparent black; A = 255 / 0 (4 bpp)            */
+    NDGI_FMT_BC3 = 4, /* 16-byte blocks, 4-channel maps: BC4 block for A, then
+                         a BC1 colour block decoded with 4 colours (8 bpp)  */
+    NDGI_FMT_BC5 = 5  /* 16-byte blocks, 2-channel line maps (F_ut, F_vt):
+                         BC4 blocks for channel 0 then channel 1 (8 bpp);
+                         BC4 = a0, a1, 3-bit indices, 8 or 6+{0,255} values */
 } ndgi_feat_fmt;
 
 /* page-cache texel format (reading R12) */

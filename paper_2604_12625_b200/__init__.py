@@ -27,7 +27,7 @@ _lib = C.CDLL(LIB_PATH)
 
 ABI_VERSION = 1
 OK, ERR_ARG, ERR_RANGE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NOMEM, ERR_DEVICE = range(7)
-FMT = {"bc7": 0, "u8": 1, "f16": 2}
+FMT = {"bc7": 0, "u8": 1, "f16": 2, "bc1": 3, "bc3": 4, "bc5": 5}
 OUT = {"rgba8": 0, "rgba16f": 1, "rgba32f": 2}
 GELU = {"erf": 0, "tanh": 1}
 BORDER = {"mirror": 0, "eval_clamp": 1}

@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "bc7_device.cuh"
+#include "bcn_device.cuh"
 #include "ndgi_common.cuh"
 #include "tc_ptx.cuh"
 
@@ -334,14 +335,14 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
             const float tau = tc.tau, omt = 1.0f - tau;
             if (win_pitch) {
                 // windowed: staged per chunk by the kernel
-            } else if (p.fmt_uvt == FMT_BC7) {
+            } else if (fmt_block4(p.fmt_uvt)) {
                 const int nbx = R3 >> 2, nb = nbx * nbx;
-                const uint4* s0 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k0);
-                const uint4* s1 = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * tc.k1);
+                const uint8_t* s0 = vol + p.uvt_slice_bytes * tc.k0;
+                const uint8_t* s1 = vol + p.uvt_slice_bytes * tc.k1;
                 for (int bi = tid; bi < nb; bi += nthr) {
                     uint32_t t0[16], t1[16];
-                    bc7_decode(__ldg(s0 + bi), [&](int i, uint32_t v) { t0[i] = v; });
-                    bc7_decode(__ldg(s1 + bi), [&](int i, uint32_t v) { t1[i] = v; });
+                    block4_decode(p.fmt_uvt, s0, bi, [&](int i, uint32_t v) { t0[i] = v; });
+                    block4_decode(p.fmt_uvt, s1, bi, [&](int i, uint32_t v) { t1[i] = v; });
                     const int bx = bi % nbx, by = bi / nbx;
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -393,6 +394,11 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                         v10 = (float)__ldg(m + (tc.r0 * p.U + x1) * 2 + q);
                         v01 = (float)__ldg(m + (tc.r1 * p.U + x0) * 2 + q);
                         v11 = (float)__ldg(m + (tc.r1 * p.U + x1) * 2 + q);
+                    } else if (p.fmt_line == FMT_BC5) {
+                        v00 = (float)((bc5_texel_at(m, p.U, x0, tc.r0) >> (8 * q)) & 0xffu);
+                        v10 = (float)((bc5_texel_at(m, p.U, x1, tc.r0) >> (8 * q)) & 0xffu);
+                        v01 = (float)((bc5_texel_at(m, p.U, x0, tc.r1) >> (8 * q)) & 0xffu);
+                        v11 = (float)((bc5_texel_at(m, p.U, x1, tc.r1) >> (8 * q)) & 0xffu);
                     } else {
                         const uint16_t* mh = reinterpret_cast<const uint16_t*>(m);
                         v00 = half_bits_to_float(__ldg(mh + (tc.r0 * p.U + x0) * 2 + q));
@@ -401,7 +407,7 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                         v11 = half_bits_to_float(__ldg(mh + (tc.r1 * p.U + x1) * 2 + q));
                     }
                     float v = (1.f - fx) * omr * v00 + fx * omr * v10 + (1.f - fx) * rho * v01 + fx * rho * v11;
-                    c[q] = p.fmt_line == FMT_U8 ? v * (1.0f / 255.0f) : v;
+                    c[q] = p.fmt_line != FMT_F16 ? v * (1.0f / 255.0f) : v;   // U8, BC5: q/255 (R8)
                 }
                 if (e < C) {
                     sUt[i] = pack_f16x2(c[0], c[1]);

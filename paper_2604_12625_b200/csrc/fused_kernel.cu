@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         }
         // F_uv texel (row, blk*128 + tid) as two f16x2 holding the integers q (R8)
         auto uv_texel = [&](int row, int jr, int blk, uint32_t& lo, uint32_t& hi) {
-            if constexpr (FMT_UV == FMT_BC7) {
+            if constexpr (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) {
                 u8x4_to_h2(sUv[jr * C + blk * kThreads + tid], lo, hi);
             } else if constexpr (FMT_UV == FMT_BC7_TEX) {
                 // hardware BC7 decode returns q/255 (UNORM); x255 lands within 2^-16
@@ -244,16 +244,19 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const int nbr = crows >> 2;
             const int br = br_all < nbr ? br_all : br_all % nbr;
             const int gbc = 32 * blk + 8 * warp + bc;       // block column in the tile
-            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(uvmap) + ((jc >> 2) + br) * (C >> 2) + gbc);
+            const size_t bidx = (size_t)((jc >> 2) + br) * (C >> 2) + gbc;
             uint32_t* dst = sUv + (4 * br) * C + 4 * gbc;
             const bool store = br_all < nbr;
             uint32_t rowv[4];
-            __syncwarp();   // previous chunk fully gathered by this warp
-            bc7_decode(raw, [&](int i, uint32_t v) {
+            auto sink = [&](int i, uint32_t v) {
                 rowv[i & 3] = v;
                 if ((i & 3) == 3 && store)
                     *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
-            });
+            };
+            __syncwarp();   // previous chunk fully gathered by this warp
+            if constexpr (FMT_UV == FMT_BC1) bc1_decode(__ldg(reinterpret_cast<const uint2*>(uvmap) + bidx), false, sink);
+            else if constexpr (FMT_UV == FMT_BC3) bc3_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
+            else bc7_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
             __syncwarp();
         };
 
@@ -277,8 +280,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const int nnew = bhi - n0 + 1;
             __syncwarp();   // this warp's gathers of the previous chunk are done
             if (nnew > 0) {
-                if (p.fmt_uvt == FMT_BC7) {
-                    // one BC7 block per lane (both slices' blocks: 2 * nnew * wxb <= 48
+                if (fmt_block4(p.fmt_uvt)) {
+                    // one BC7 / BC1 / BC3 block per lane (both slices' blocks: 2 * nnew * wxb <= 48
                     // decodes), raw RGBA8 into this warp's part of the F_uv chunk
                     // buffer (free between chunks: 16 rows x 128 B), then all lanes
                     // blend texels into the ring
@@ -291,9 +294,9 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                             const int pos = g0 + (q >> 1), sl = q & 1;
                             const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
                             const int gbx = wbx0 + qx < nbm ? wbx0 + qx : nbm - 1;
-                            const uint4* src = reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0));
+                            const uint8_t* src = vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0);
                             uint32_t t[16];
-                            bc7_decode(__ldg(src + br * nbm + gbx), [&](int i, uint32_t v) { t[i] = v; });
+                            block4_decode(p.fmt_uvt, src, (size_t)br * nbm + gbx, [&](int i, uint32_t v) { t[i] = v; });
                             if (lane < 2 * ng) {
                                 // scratch slot q: 64 B at row q >> 1, byte (q & 1) * 64
                                 uint4* d = reinterpret_cast<uint4*>(scratch + (size_t)(q >> 1) * C * 4 + (q & 1) * 64);
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         const int chunk_items = crows * BPR;
         for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
         if constexpr (WIN) stage_window(j_begin + c0 / BPR, crows);   // uses the F_uv chunk buffer as scratch
-        if (FMT_UV == FMT_BC7) decode_chunk(j_begin + c0 / BPR, crows);
+        if (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) decode_chunk(j_begin + c0 / BPR, crows);
         for (int it = c0; it < c0 + chunk_items; it += S) {
             PROF_T0();
             if constexpr (BPR == 1 && S == 2) {
@@ -706,6 +709,8 @@ static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t 
     if (p.fmt_uv == FMT_BC7_TEX) return launch_fused_t<H, FMT_BC7_TEX, CT>(p, num_sms, s);
     if (p.fmt_uv == FMT_BC7) return launch_fused_t<H, FMT_BC7, CT>(p, num_sms, s);
     if (p.fmt_uv == FMT_U8) return launch_fused_t<H, FMT_U8, CT>(p, num_sms, s);
+    if (p.fmt_uv == FMT_BC1) return launch_fused_t<H, FMT_BC1, CT>(p, num_sms, s);
+    if (p.fmt_uv == FMT_BC3) return launch_fused_t<H, FMT_BC3, CT>(p, num_sms, s);
     return launch_fused_t<H, FMT_F16, CT>(p, num_sms, s);
 }
 

@@ -90,13 +90,16 @@ struct DeviceGuard {
 };
 
 size_t map2d_bytes(uint32_t fmt, uint32_t rx, uint32_t ry, uint32_t nc) {
-    if (fmt == NDGI_FMT_BC7) return (size_t)(rx / 4) * (ry / 4) * 16;
+    if (fmt == NDGI_FMT_BC7 || fmt == NDGI_FMT_BC3 || fmt == NDGI_FMT_BC5) return (size_t)(rx / 4) * (ry / 4) * 16;
+    if (fmt == NDGI_FMT_BC1) return (size_t)(rx / 4) * (ry / 4) * 8;
     return (size_t)rx * ry * nc * (fmt == NDGI_FMT_U8 ? 1 : 2);
 }
 
 size_t mlp_elems(uint32_t h) { return (size_t)16 * h + h + (size_t)h * h + h + 3 * (size_t)h + 3; }
 
-bool fmt_ok(uint32_t f) { return f <= NDGI_FMT_F16; }
+// 4-channel maps: BC7, U8, F16, BC1, BC3; 2-channel line maps: U8, F16, BC5
+bool fmt_ok(uint32_t f) { return f <= NDGI_FMT_BC3; }
+bool fmt_block(uint32_t f) { return f == NDGI_FMT_BC7 || f == NDGI_FMT_BC1 || f == NDGI_FMT_BC3 || f == NDGI_FMT_BC5; }
 
 ndgi_status validate(const ndgi_layout* L, int* fast) {
     if (!L) return fail(NDGI_ERR_ARG, "layout is NULL");
@@ -109,9 +112,12 @@ ndgi_status validate(const ndgi_layout* L, int* fast) {
     if (L->uv_res == 0 || L->uvt_res == 0 || L->uvt_depth == 0 || L->line_res == 0 || L->line_t == 0)
         return fail(NDGI_ERR_ARG, "zero resolution");
     if (!fmt_ok(L->fmt_uv) || !fmt_ok(L->fmt_uvt)) return fail(NDGI_ERR_ARG, "bad feature format");
-    if (L->fmt_line != NDGI_FMT_U8 && L->fmt_line != NDGI_FMT_F16) return fail(NDGI_ERR_ARG, "fmt_line must be U8 or F16");
-    if (L->fmt_uv == NDGI_FMT_BC7 && L->uv_res % 4) return fail(NDGI_ERR_ARG, "BC7 F_uv resolution must be a multiple of 4");
-    if (L->fmt_uvt == NDGI_FMT_BC7 && L->uvt_res % 4) return fail(NDGI_ERR_ARG, "BC7 F_uvt resolution must be a multiple of 4");
+    if (L->fmt_line != NDGI_FMT_U8 && L->fmt_line != NDGI_FMT_F16 && L->fmt_line != NDGI_FMT_BC5)
+        return fail(NDGI_ERR_ARG, "fmt_line must be U8, F16 or BC5");
+    if (fmt_block(L->fmt_uv) && L->uv_res % 4) return fail(NDGI_ERR_ARG, "block-compressed F_uv resolution must be a multiple of 4");
+    if (fmt_block(L->fmt_uvt) && L->uvt_res % 4) return fail(NDGI_ERR_ARG, "block-compressed F_uvt resolution must be a multiple of 4");
+    if (L->fmt_line == NDGI_FMT_BC5 && (L->line_res % 4 || L->line_t % 4))
+        return fail(NDGI_ERR_ARG, "BC5 line maps need line_res and line_t multiples of 4");
     if (L->hidden < 1 || L->hidden > 256) return fail(NDGI_ERR_ARG, "hidden must be in [1, 256]");
     if (L->gelu > NDGI_GELU_TANH) return fail(NDGI_ERR_ARG, "bad gelu");
     if (L->border_mode > NDGI_BORDER_EVAL_CLAMP) return fail(NDGI_ERR_ARG, "bad border_mode");
@@ -246,9 +252,9 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
             if (v && strcmp(v, "pipe") == 0) return 3;
             return 0;
         }();
-        const bool deflt = p.H != 16 || variant == 0;
+        const bool deflt = p.H != 16 || variant == 0 || p.fmt_uv > ndgi::FMT_F16;   // variants: BC7 / U8 / F16 F_uv
         choose_strips(p, ctx->num_sms, deflt ? 4 : 16);
-        if (p.H != 16 || variant == 0) e = ndgi::launch_fused(p, ctx->num_sms, s);
+        if (deflt) e = ndgi::launch_fused(p, ctx->num_sms, s);
         else if (variant == 1) e = ndgi::launch_fused_ws(p, ctx->num_sms, s);
         else if (variant == 2) e = ndgi::launch_fused_hmma(p, ctx->num_sms, s);
         else e = ndgi::launch_fused_pipe(p, ctx->num_sms, s);

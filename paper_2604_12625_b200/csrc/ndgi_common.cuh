@@ -7,9 +7,9 @@
 
 namespace ndgi {
 
-enum : int { FMT_BC7 = 0, FMT_U8 = 1, FMT_F16 = 2 };
+enum : int { FMT_BC7 = 0, FMT_U8 = 1, FMT_F16 = 2, FMT_BC1 = 3, FMT_BC3 = 4, FMT_BC5 = 5 };
 // kernel-internal: BC7 F_uv fetched through the texture unit (NDGI_MODE_FAST_TEXUNIT)
-constexpr int FMT_BC7_TEX = 3;
+constexpr int FMT_BC7_TEX = 16;
 constexpr int kMaxTexAtlases = 64;
 enum : int { OUT_RGBA8 = 0, OUT_RGBA16F = 1, OUT_RGBA32F = 2 };
 enum : int { GELU_ERF = 0, GELU_TANH = 1 };

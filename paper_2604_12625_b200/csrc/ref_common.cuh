@@ -1,9 +1,11 @@
 // ref_common.cuh -- scalar fp32 sampling helpers shared by the reference
 // decode kernel (ref_kernel.cu) and the fine-tuning kernels (train_kernel.cu):
-// texel fetch from a stored map (BC7 decoded per tap, R8 dequantisation),
+// texel fetch from a stored map (BC7 / BC1 / BC3 / BC5 decoded per tap, R8
+// dequantisation),
 // texel-centre bilinear with clamp (R1), accurate GELU (R7).
 #pragma once
 #include "bc7_device.cuh"
+#include "bcn_device.cuh"
 #include "ndgi_common.cuh"
 
 namespace ndgi {
@@ -15,9 +17,20 @@ struct Map2D {
 
 // all channels of texel (a, b), dequantised (R8)
 __device__ __forceinline__ void fetch_texel(const Map2D& m, int a, int b, float* out) {
-    if (m.fmt == FMT_BC7) {
-        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(m.base) + (b >> 2) * (m.rx >> 2) + (a >> 2));
-        const uint32_t v = bc7_texel(raw, 4 * (b & 3) + (a & 3));
+    if (m.fmt == FMT_BC7 || m.fmt == FMT_BC1 || m.fmt == FMT_BC3 || m.fmt == FMT_BC5) {
+        const size_t bi = (size_t)(b >> 2) * (m.rx >> 2) + (a >> 2);
+        const int i = 4 * (b & 3) + (a & 3);
+        uint32_t v;
+        if (m.fmt == FMT_BC1) {
+            v = bc1_texel(__ldg(reinterpret_cast<const uint2*>(m.base) + bi), i, false);
+        } else {
+            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(m.base) + bi);
+            if (m.fmt == FMT_BC7) v = bc7_texel(raw, i);
+            else if (m.fmt == FMT_BC3)
+                v = (bc1_texel(make_uint2(raw.z, raw.w), i, true) & 0x00ffffffu) |
+                    bc4_texel(make_uint2(raw.x, raw.y), i) << 24;
+            else v = bc4_texel(make_uint2(raw.x, raw.y), i) | bc4_texel(make_uint2(raw.z, raw.w), i) << 8;   // BC5
+        }
         for (int c = 0; c < m.nc; ++c) out[c] = (float)((v >> (8 * c)) & 0xffu) / 255.0f;
     } else if (m.fmt == FMT_U8) {
         const uint8_t* p = m.base + ((size_t)b * m.rx + a) * m.nc;

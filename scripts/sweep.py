@@ -1,4 +1,5 @@
-"""Config 5 sweep: decoder width x feature format on config 2's
+"""Config 5 sweep: decoder width x feature format (BC7, and
+BC3 / BC1 with BC5 line maps (R29), u8, f16) on config 2's
 atlas (1,024 tiles), decode_full at 24 times per call, RGBA8.  For every cell:
 written Gtexel/s, kernel ms, the ALU roofline fraction (2h GELU activations per
 texel against the measured GELU rate), the HBM fraction of the algorithmic bytes,
@@ -35,7 +36,7 @@ TS = [i / 24 for i in range(24)]
 out = {"gelu_rate_act_per_s": r_gelu, "cells": []}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for prof in ("L", "M", "H", "M64"):
-    for fmt in ("bc7", "u8", "f16"):
+    for fmt in ("bc7", "bc3", "bc1", "u8", "f16"):
         lay, seed = S.config(f"c5:{prof}:{fmt}")
         th = S.make_theta(lay, seed)
         ctx = ndgi.ndgi_load(lay, ndgi.upload_theta(th), 0)
@@ -72,10 +73,13 @@ for prof in ("L", "M", "H", "M64"):
         alg_bytes = 24 * (1024 * (theta_t / lay["uvt_depth"] * 0 + 0) + per_t * 4)
         # Theta bytes read at one t: F_uv + 2 slices + 2x2 line rows + MLP
         def b2(f, rx, ry, nc):
-            return (rx // 4) * (ry // 4) * 16 if f == "bc7" else rx * ry * nc * (1 if f == "u8" else 2)
-        lb = 1 if lay["fmt_line"] == "u8" else 2
+            if f in ("bc7", "bc3", "bc1"):
+                return (rx // 4) * (ry // 4) * (8 if f == "bc1" else 16)
+            return rx * ry * nc * (1 if f == "u8" else 2)
+        # one line-map row: U texels x 2 channels, or (BC5) its whole 4-row block row
+        row_b = {"u8": 2 * lay["line_res"], "f16": 4 * lay["line_res"], "bc5": 4 * lay["line_res"]}[lay["fmt_line"]]
         read_t = (b2(lay["fmt_uv"], 128, 128, 4) + 2 * b2(lay["fmt_uvt"], lay["uvt_res"], lay["uvt_res"], 4)
-                  + 2 * 2 * lay["line_res"] * 2 * lb + 2 * (16 * h + h + h * h + h + 3 * h + 3))
+                  + 2 * 2 * row_b + 2 * (16 * h + h + h * h + h + 3 * h + 3))
         alg_bytes = 24 * 1024 * (read_t + 128 * 128 * 4)
         cell = {"profile": prof, "fmt": fmt, "hidden": h, "gtexel_s": texels / (kms * 1e-3) / 1e9, "ms_per_24t": kms,
                 "alu_frac": texels * 2 * h / (kms * 1e-3) / r_gelu,

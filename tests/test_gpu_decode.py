@@ -152,6 +152,11 @@ FAST_CASES = {
     "H-u8": (S.layout(1, 2, 1, "H", fmt_uv="u8", fmt_uvt="u8"), "smooth"),
     "H-f16": (S.layout(1, 2, 1, "H", fmt_uv="f16", fmt_uvt="f16", fmt_line="f16"), "smooth"),
     "C256": (S.layout(1, 1, 1, "M", core=256, uv_res=256), "smooth"),
+    # R29: the other DXTC formats (config 5's BC-format axis)
+    "bc3-bc5": (S.layout(1, 2, 1, "M", uvt_depth=4, line_t=8, fmt_uv="bc3", fmt_uvt="bc3", fmt_line="bc5"), "smooth"),
+    "bc1-bc5-mixed": (S.layout(1, 2, 1, "M", uvt_depth=4, line_t=8, fmt_uv="bc1", fmt_uvt="bc1", fmt_line="bc5"),
+                      "mixed"),
+    "H-bc3": (S.layout(1, 1, 2, "H", fmt_uv="bc3", fmt_uvt="bc3", fmt_line="bc5"), "mixed"),   # windowed F_uvt
 }
 
 
@@ -220,6 +225,50 @@ def test_cross_format_u8_equals_bc7():
         a = gpu_full(_load(lay, th), 0.45, "rgba32f", mode)
         b = gpu_full(_load(lay8, th8), 0.45, "rgba32f", mode)
         np.testing.assert_array_equal(a, b)
+
+
+def _bcn_image(fmt, blocks, w, h):
+    """Oracle decode of a [h/4][w/4] block map into [h][w][channels] u8."""
+    nch = 2 if fmt == "bc5" else 4
+    bsz = 8 if fmt == "bc1" else 16
+    b = np.ascontiguousarray(blocks).reshape(h // 4, w // 4, bsz)
+    out = np.zeros((h, w, nch), np.uint8)
+    for by in range(h // 4):
+        for bx in range(w // 4):
+            out[4 * by:4 * by + 4, 4 * bx:4 * bx + 4] = oracle.bcn_decode_block(fmt, b[by, bx].tobytes()).reshape(4, 4, nch)
+    return out
+
+
+@pytest.mark.parametrize("fmt", ["bc1", "bc3"])
+def test_cross_format_u8_equals_bcn(fmt):
+    # the device BC1 / BC3 / BC5 decoders are bit-exact: decoding the same
+    # blocks with the oracle into u8 maps gives identical outputs in both modes
+    lay = S.layout(1, 2, 1, "M", uvt_depth=3, line_t=8, fmt_uv=fmt, fmt_uvt=fmt, fmt_line="bc5")
+    th = S.make_theta(lay, 77, "mixed")
+    lay8 = dict(lay, fmt_uv="u8", fmt_uvt="u8", fmt_line="u8")
+    th8 = dict(th)
+    R, R3, U, T = lay["uv_res"], lay["uvt_res"], lay["line_res"], lay["line_t"]
+    th8["uv"] = np.stack([_bcn_image(fmt, th["uv"][k], R, R) for k in range(2)])
+    th8["uvt"] = np.stack([[_bcn_image(fmt, th["uvt"][k, d], R3, R3) for d in range(3)] for k in range(2)])
+    th8["ut"] = np.stack([_bcn_image("bc5", th["ut"][k], U, T) for k in range(2)])
+    th8["vt"] = np.stack([_bcn_image("bc5", th["vt"][k], U, T) for k in range(2)])
+    for mode in ("fast", "ref_fp32"):
+        a = gpu_full(_load(lay, th), [0.45, 0.8], "rgba32f", mode)
+        b = gpu_full(_load(lay8, th8), [0.45, 0.8], "rgba32f", mode)
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(gpu_tiles(_load(lay, th), [1, 0], 0.2, "rgba8"),
+                                  gpu_tiles(_load(lay8, th8), [1, 0], 0.2, "rgba8"))
+
+
+@pytest.mark.parametrize("fmt", ["bc1", "bc3"])
+def test_ref_fp32_bcn(fmt):
+    lay = S.layout(1, 2, 1, "M", uvt_depth=4, line_t=8, fmt_uv=fmt, fmt_uvt=fmt, fmt_line="bc5")
+    th = S.make_theta(lay, 5, "smooth")
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    for t in (0.3, 0.9):
+        mx, _ = _err(gpu_full(ctx, t, "rgba32f", "ref_fp32")[0], M.decode_full(t, NTHR))
+        assert mx <= REF_MAX, (fmt, t, mx)
 
 
 @pytest.mark.parametrize("payload", ["smooth", "mixed"])
