@@ -60,6 +60,9 @@ def lib():
             "oracle_bc7_decode_block": (I, [P, P]),
             "oracle_bc7_decode_image": (None, [P, I, I, P]),
             "oracle_bc1_decode_block": (None, [P, P, I]),
+            "oracle_ptq_u8": (C.c_uint8, [C.c_float]),
+            "oracle_float_to_half": (C.c_uint16, [C.c_float]),
+            "oracle_train_full_export": (None, [P, P, P, P, P, P, P]),
             "oracle_bc4_decode_block": (None, [P, P]),
             "oracle_bc3_decode_block": (None, [P, P]),
             "oracle_bc5_decode_block": (None, [P, P]),
@@ -129,6 +132,14 @@ def bcn_decode_block(fmt: str, block) -> np.ndarray:
     else:
         getattr(lib(), f"oracle_{fmt}_decode_block")(_ptr(b), _ptr(out))
     return out.reshape(16, nch)
+
+
+def ptq_u8(x: float) -> int:
+    return int(lib().oracle_ptq_u8(float(x)))
+
+
+def float_to_half(x: float) -> int:
+    return int(lib().oracle_float_to_half(float(x)))
 
 
 def bc7_weight(bits: int, index: int) -> int:
@@ -224,6 +235,20 @@ class Model:
                                             _ptr(np.ascontiguousarray(target, np.float64)),
                                             _ptr(np.ascontiguousarray(noise, np.float64)), len(uvt), _ptr(g))
         return loss, g
+
+    def train_full_export(self, theta: np.ndarray) -> dict:
+        """R30: fp32 parameters [num_tiles][P] -> a deployable Theta (BC7 F_uv,
+        BC7 F_uvt, u8 line maps, f16 MLP) in ndgi_load's dense layouts."""
+        L = self.lay
+        theta = np.ascontiguousarray(theta, np.float32)
+        n, R, R3, D, U, T = L["num_tiles"], L["uv_res"], L["uvt_res"], L["uvt_depth"], L["line_res"], L["line_t"]
+        h = L["hidden"]
+        out = {"uv": np.zeros((n, R // 4, R // 4, 16), np.uint8),
+               "uvt": np.zeros((n, D, R3 // 4, R3 // 4, 16), np.uint8),
+               "ut": np.zeros((n, T, U, 2), np.uint8), "vt": np.zeros((n, T, U, 2), np.uint8),
+               "mlp": np.zeros((n, 16 * h + h + h * h + h + 3 * h + 3), np.uint16)}
+        lib().oracle_train_full_export(C.byref(self.L), _ptr(theta), *(_ptr(out[k]) for k in ("uv", "uvt", "ut", "vt", "mlp")))
+        return out
 
     def train_full_project(self, theta: np.ndarray) -> None:
         assert theta.dtype == np.float64 and theta.flags["C_CONTIGUOUS"]

@@ -1219,3 +1219,86 @@ void oracle_train_full_project(const oracle_layout *L, double *theta)
     const full_offsets o = full_layout(L);
     for (size_t i = o.uv; i < o.total; ++i) theta[i] = fmin(fmax(theta[i], 0.0), 1.0);
 }
+
+/* ------------------------------------------------------------------ */
+/* Export of fully trained tiles to a deployable Theta (SURVEY.md 8(f) */
+/* NEXT 3 "u8 PTQ plus a BC7 encoder", "BC compression on the    */
+/* final generated feature maps"; reading R30).                 */
+/* Per tile, from its fp32 parameter vector (R28 layout):              */
+/*  * F_uv and every F_uvt slice: each block's 16 texels by Eq. 7 in   */
+/*    fp32, x = (1 - w) e1 + w e2 (every operation rounded to fp32, no */
+/*    fused multiply-add: the trainer's precision, so the integer      */
+/*    decision below is taken in it), post-training quantisation       */
+/*    q = RN-even(clamp(x, 0, 1) * 255), then BC7 mode 6 (R26);        */
+/*  * F_ut, F_vt: q = RN-even(clamp(v, 0, 1) * 255), u8 [T][U][2];     */
+/*  * the MLP: fp32 -> f16, RN-even.                                   */
+/* Outputs in ndgi_load's dense per-tile layouts (BC7, BC7, U8, f16).  */
+/* ------------------------------------------------------------------ */
+uint8_t oracle_ptq_u8(float x)
+{
+    x = x < 0.0f ? 0.0f : (x > 1.0f ? 1.0f : x);
+    float s = x * 255.0f;
+    return (uint8_t)rintf(s);
+}
+
+/* IEEE binary16 of a float, round to nearest even */
+uint16_t oracle_float_to_half(float f)
+{
+    uint32_t x;
+    memcpy(&x, &f, 4);
+    uint32_t sign = (x >> 16) & 0x8000u, ax = x & 0x7fffffffu;
+    if (ax >= 0x7f800000u) return (uint16_t)(sign | 0x7c00u | (ax > 0x7f800000u ? 0x200u : 0u));
+    if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);            /* >= 65520: inf */
+    if (ax < 0x38800000u) {                                                /* < 2^-14: subnormal */
+        double r = nearbyint((double)fabsf(f) * 16777216.0);               /* units of 2^-24 */
+        return (uint16_t)(sign | (uint32_t)r);
+    }
+    uint32_t h = ((((ax >> 23) - 127u + 15u)) << 10) | ((ax & 0x7fffffu) >> 13);
+    uint32_t rem = ax & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) h++;
+    return (uint16_t)(sign | h);
+}
+
+static void bc_map_image(const float *blocks, int R, uint8_t *rgba)
+{
+    int nb = R / 4;
+    for (int by = 0; by < nb; ++by)
+        for (int bx = 0; bx < nb; ++bx) {
+            const float *blk = blocks + ((size_t)by * nb + bx) * 24;
+            for (int p = 0; p < 16; ++p) {
+                float w = blk[8 + p];
+                for (int c = 0; c < 4; ++c) {
+                    float a = 1.0f - w;
+                    float t1 = a * blk[c];
+                    float t2 = w * blk[4 + c];
+                    float x = t1 + t2;                                      /* Eq. 7 */
+                    rgba[((size_t)(4 * by + p / 4) * R + 4 * bx + p % 4) * 4 + c] = oracle_ptq_u8(x);
+                }
+            }
+        }
+}
+
+void oracle_train_full_export(const oracle_layout *L, const float *theta, uint8_t *uv, uint8_t *uvt, uint8_t *ut,
+                              uint8_t *vt, uint16_t *mlp)
+{
+    const full_offsets o = full_layout(L);
+    const int R = L->uv_res, R3 = L->uvt_res, D = L->uvt_depth;
+    const size_t uvb = (size_t)(R / 4) * (R / 4) * 16, uvtb = (size_t)(R3 / 4) * (R3 / 4) * 16;
+    const size_t nl = (size_t)L->line_t * L->line_res * 2, pm = oracle_mlp_params(L->hidden);
+    uint8_t *img = (uint8_t *)malloc((size_t)(R > R3 ? R : R3) * (R > R3 ? R : R3) * 4);
+    for (int k = 0; k < L->num_tiles; ++k) {
+        const float *th = theta + (size_t)k * o.total;
+        bc_map_image(th + o.uv, R, img);
+        oracle_bc7_encode_image_mode6(img, R, R, uv + k * uvb);
+        for (int d = 0; d < D; ++d) {
+            bc_map_image(th + o.uvt + (size_t)d * (R3 / 4) * (R3 / 4) * 24, R3, img);
+            oracle_bc7_encode_image_mode6(img, R3, R3, uvt + ((size_t)k * D + d) * uvtb);
+        }
+        for (size_t i = 0; i < nl; ++i) {
+            ut[k * nl + i] = oracle_ptq_u8(th[o.ut + i]);
+            vt[k * nl + i] = oracle_ptq_u8(th[o.vt + i]);
+        }
+        for (size_t i = 0; i < pm; ++i) mlp[k * pm + i] = oracle_float_to_half(th[i]);
+    }
+    free(img);
+}
