@@ -585,6 +585,12 @@ def finetune_leg(ndgi, torch, args):
     e1.record(stream)
     e1.synchronize()
     sf = e0.elapsed_time(e1) / reps * 1e-3
+    tf.export_full(stream)                                     # R30 export, warm
+    e0.record(stream)
+    tf.export_full(stream)
+    e1.record(stream)
+    e1.synchronize()
+    sx = e0.elapsed_time(e1) * 1e-3
     tf.close()
     ctx.close()
     return {"workload": "1024 tiles x 4096 samples (c2, BC7 features), forward + backward + Adam, h = 16",
@@ -592,7 +598,10 @@ def finetune_leg(ndgi, torch, args):
             "mlp_tflops": flops / s_ / 1e12, "fp32_peak_tflops": fma_peak, "frac": flops / s_ / 1e12 / fma_peak,
             "full": {"workload": f"same batch, full step (R28): {P} fp32 parameters per tile "
                                  "(MLP + BC-simulated maps + line grids), Eq. 5 noise, Adam + [0,1] projection",
-                     "ms_per_step": sf * 1e3, "msample_s": n / sf / 1e6}}
+                     "ms_per_step": sf * 1e3, "msample_s": n / sf / 1e6,
+                     "export_ms": sx * 1e3,
+                     "export": "R30: Eq. 7 texels -> u8 PTQ -> BC7 mode 6 (F_uv, F_uvt), line grids -> u8, "
+                               "MLP -> f16, all 1,024 tiles"}}
 
 
 def main():

@@ -371,6 +371,23 @@ NDGI_API ndgi_status ndgi_train_full_step(ndgi_train* tr, const uint32_t* tile_i
                                           const float* targets, const float* noise, uint32_t S, float lr, float* loss,
                                           void* stream);
 
+/*
+ * Export of a full trainer's tiles to a deployable Theta (SURVEY.md §8(f)
+ * NEXT 3 "u8 PTQ plus a BC7 encoder"; "BC compression on the final
+ * generated feature maps"; reading R30).  Per tile: every BC-simulated
+ * block's 16 texels by Eq. 7 in fp32 (each operation rounded, no FMA),
+ * post-training quantisation q = RN-even(clamp(x, 0, 1) * 255), BC7 mode 6
+ * (as ndgi_bc7_encode_mode6) for F_uv and each F_uvt slice; line grids by
+ * the same PTQ to u8; the MLP to f16 (RN-even).  All outputs DEVICE, in
+ * ndgi_load's dense per-tile layouts for fmt_uv = fmt_uvt = NDGI_FMT_BC7,
+ * fmt_line = NDGI_FMT_U8: uv [num_tiles][R_uv/4][R_uv/4][16] B,
+ * uvt [num_tiles][D][R3/4][R3/4][16] B, ut / vt [num_tiles][T][U][2] B,
+ * mlp [num_tiles][P_mlp] f16.  Needs a full trainer (NDGI_ERR_ARG otherwise);
+ * stream-ordered; uses stream-ordered scratch of 4 B per map texel.
+ */
+NDGI_API ndgi_status ndgi_train_full_export(ndgi_train* tr, void* uv, void* uvt, void* ut, void* vt, uint16_t* mlp,
+                                            void* stream);
+
 /* the last step's gradients (mean-loss gradient of each batch tile, before
  * Adam) -> DEVICE float[n][P]; n <= that step's batch (RANGE otherwise) */
 NDGI_API ndgi_status ndgi_train_last_grad(ndgi_train* tr, float* out, uint32_t n, void* stream);

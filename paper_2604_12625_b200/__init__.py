@@ -87,6 +87,7 @@ _SIGS = {
     "ndgi_train_free": (_I, [_P]),
     "ndgi_train_full_params": (C.c_size_t, [C.POINTER(ndgi_layout)]),
     "ndgi_train_full_create": (_I, [_P, _P, C.POINTER(C.c_void_p)]),
+    "ndgi_train_full_export": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "ndgi_train_full_step": (_I, [_P, _P, _U32, _P, _P, _P, _U32, _F, _P, _P]),
     "ndgi_sample_lighting": (_I, [_P, _P, C.c_int32, _P, _U32, _P, _P, _U32, _F, C.POINTER(ndgi_hdr), _P, _P]),
 }
@@ -404,6 +405,24 @@ class Trainer:
     def export_f16(self, mlp, stream=None) -> None:
         _check(_lib.ndgi_train_export_f16(self.handle, C.c_void_p(mlp.data_ptr()), _stream_ptr(stream)),
                "ndgi_train_export_f16")
+
+    def export_full(self, stream=None) -> dict:
+        """R30 (full trainer): the deployable Theta as CUDA tensors for ndgi_load
+        with fmt_uv = fmt_uvt = "bc7", fmt_line = "u8"."""
+        import torch
+        L = self.ctx.lay
+        n, R, R3, D, U, T = L["num_tiles"], L["uv_res"], L["uvt_res"], L["uvt_depth"], L["line_res"], L["line_t"]
+        h = L["hidden"]
+        dev = torch.device("cuda", torch.cuda.current_device())
+        out = {"uv": torch.empty((n, R // 4, R // 4, 16), dtype=torch.uint8, device=dev),
+               "uvt": torch.empty((n, D, R3 // 4, R3 // 4, 16), dtype=torch.uint8, device=dev),
+               "ut": torch.empty((n, T, U, 2), dtype=torch.uint8, device=dev),
+               "vt": torch.empty((n, T, U, 2), dtype=torch.uint8, device=dev),
+               "mlp": torch.empty((n, 16 * h + h + h * h + h + 3 * h + 3), dtype=torch.int16, device=dev)}
+        _check(_lib.ndgi_train_full_export(self.handle, *(C.c_void_p(out[k].data_ptr()) for k in
+                                                          ("uv", "uvt", "ut", "vt", "mlp")), _stream_ptr(stream)),
+               "ndgi_train_full_export")
+        return out
 
     def close(self) -> None:
         lib = _lib

@@ -24,6 +24,12 @@ int fused_ctas_per_sm(int H);
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s);
 cudaError_t launch_train_grad(const TrainArgs& a, int H, cudaStream_t s);
+cudaError_t launch_convert_f32_f16_2d(const float* in, size_t in_stride, uint16_t* out, size_t out_stride, size_t rows,
+                                      size_t cols, cudaStream_t s);
+cudaError_t launch_full_ptq(const float* theta, size_t P, size_t off_uv, size_t off_uvt, size_t off_ut, size_t off_vt,
+                            int num_tiles, int R, int R3, int D, int nline, uint32_t* uv_img, uint32_t* uvt_img,
+                            uint8_t* ut, uint8_t* vt, int num_sms, cudaStream_t s);
+cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s);
 cudaError_t launch_adam(float* theta, float* m, float* v, int* steps, const float* grad, const uint32_t* tile_ids,
                         int n, size_t P, int num_tiles, float lr, float b1, float b2, float eps, size_t proj,
                         cudaStream_t s);
@@ -761,11 +767,37 @@ ndgi_status ndgi_train_export_f16(ndgi_train* t, uint16_t* mlp, void* stream) {
     if (!t->full) {
         e = ndgi::launch_convert_f32_f16(t->theta, mlp, (size_t)t->ctx->L.num_tiles * pm, static_cast<cudaStream_t>(stream));
     } else {
-        for (uint32_t k = 0; k < t->ctx->L.num_tiles && e == cudaSuccess; ++k)   // the MLP part of each tile
-            e = ndgi::launch_convert_f32_f16(t->theta + (size_t)k * t->P, mlp + (size_t)k * pm, pm,
-                                             static_cast<cudaStream_t>(stream));
+        e = ndgi::launch_convert_f32_f16_2d(t->theta, t->P, mlp, pm, t->ctx->L.num_tiles, pm,   // the MLP part
+                                            static_cast<cudaStream_t>(stream));
     }
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "train export");
+}
+
+ndgi_status ndgi_train_full_export(ndgi_train* t, void* uv, void* uvt, void* ut, void* vt, uint16_t* mlp,
+                                   void* stream) {
+    if (!t || !uv || !uvt || !ut || !vt || !mlp) return fail(NDGI_ERR_ARG, "NULL argument");
+    if (!t->full) return fail(NDGI_ERR_ARG, "export needs a full trainer");
+    ndgi_ctx* ctx = t->ctx;
+    const ndgi_layout& L = ctx->L;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t n_uv = (size_t)L.num_tiles * L.uv_res * L.uv_res * 4,
+                 n_uvt = (size_t)L.num_tiles * L.uvt_depth * L.uvt_res * L.uvt_res * 4;
+    uint8_t* img = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&img), n_uv + n_uvt, s);
+    if (e != cudaSuccess) return cuda_fail(e, "export scratch");
+    e = ndgi::launch_full_ptq(t->theta, t->P, t->off_uv, t->off_uvt, t->off_ut, t->off_vt, (int)L.num_tiles,
+                              (int)L.uv_res, (int)L.uvt_res, (int)L.uvt_depth, (int)(L.line_t * L.line_res * 2),
+                              reinterpret_cast<uint32_t*>(img), reinterpret_cast<uint32_t*>(img + n_uv),
+                              static_cast<uint8_t*>(ut), static_cast<uint8_t*>(vt), ctx->num_sms, s);
+    if (e == cudaSuccess)   // the tile-major image stack encodes straight into [tile][by][bx] blocks
+        e = ndgi::launch_bc7_encode_mode6(img, (int)L.uv_res, (int)(L.num_tiles * L.uv_res), uv, ctx->num_sms, s);
+    if (e == cudaSuccess)
+        e = ndgi::launch_bc7_encode_mode6(img + n_uv, (int)L.uvt_res, (int)(L.num_tiles * L.uvt_depth * L.uvt_res), uvt,
+                                          ctx->num_sms, s);
+    cudaFreeAsync(img, s);
+    if (e != cudaSuccess) return cuda_fail(e, "export");
+    return ndgi_train_export_f16(t, mlp, stream);
 }
 
 ndgi_status ndgi_train_free(ndgi_train* t) {

@@ -443,6 +443,53 @@ __global__ void ndgi_bc_grad_kernel(const TrainArgs a) {
     }
 }
 
+// R30 export: Eq. 7 texels of every BC-simulated block in fp32 (each
+// operation rounded, no FMA -- the oracle's order), PTQ q = RN-even(clamp *
+// 255) into RGBA8 images (tile-major rows, so one BC7 encode over the whole
+// stack yields ndgi_load's per-tile block layout); line grids to u8.
+__device__ __forceinline__ uint32_t ptq_u8(float x) {
+    return (uint32_t)__float2int_rn(__fmul_rn(fminf(fmaxf(x, 0.0f), 1.0f), 255.0f));
+}
+
+__global__ void ndgi_full_ptq_kernel(const float* __restrict__ theta, size_t P, size_t off_uv, size_t off_uvt,
+                                     size_t off_ut, size_t off_vt, int num_tiles, int R, int R3, int D, int nline,
+                                     uint32_t* __restrict__ uv_img, uint32_t* __restrict__ uvt_img,
+                                     uint8_t* __restrict__ ut, uint8_t* __restrict__ vt) {
+    const size_t n_uv = (size_t)R * R, n_uvt = (size_t)D * R3 * R3;
+    const size_t per = n_uv + n_uvt + 2 * (size_t)nline, total = per * num_tiles;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t k = i / per, j = i % per;
+        const float* th = theta + k * P;
+        if (j >= n_uv + n_uvt) {
+            const size_t l = j - n_uv - n_uvt;
+            if (l < (size_t)nline) ut[k * nline + l] = (uint8_t)ptq_u8(th[off_ut + l]);
+            else vt[k * nline + (l - nline)] = (uint8_t)ptq_u8(th[off_vt + (l - nline)]);
+            continue;
+        }
+        const bool is_uv = j < n_uv;
+        const size_t jj = is_uv ? j : j - n_uv;
+        const int res = is_uv ? R : R3;
+        const size_t slice = jj / ((size_t)res * res), r = jj % ((size_t)res * res);
+        const int y = (int)(r / res), x = (int)(r % res);
+        const float* blk = th + (is_uv ? off_uv : off_uvt + slice * (size_t)(res / 4) * (res / 4) * 24) +
+                           ((size_t)(y >> 2) * (res >> 2) + (x >> 2)) * 24;
+        const float w = blk[8 + 4 * (y & 3) + (x & 3)], a = __fsub_rn(1.0f, w);
+        uint32_t q = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) q |= ptq_u8(__fadd_rn(__fmul_rn(a, blk[c]), __fmul_rn(w, blk[4 + c]))) << (8 * c);
+        if (is_uv) uv_img[k * n_uv + r] = q;
+        else uvt_img[(k * D + slice) * (size_t)R3 * R3 + r] = q;
+    }
+}
+
+cudaError_t launch_full_ptq(const float* theta, size_t P, size_t off_uv, size_t off_uvt, size_t off_ut, size_t off_vt,
+                            int num_tiles, int R, int R3, int D, int nline, uint32_t* uv_img, uint32_t* uvt_img,
+                            uint8_t* ut, uint8_t* vt, int num_sms, cudaStream_t s) {
+    ndgi_full_ptq_kernel<<<num_sms * 8, 256, 0, s>>>(theta, P, off_uv, off_uvt, off_ut, off_vt, num_tiles, R, R3, D,
+                                                     nline, uv_img, uvt_img, ut, vt);
+    return cudaGetLastError();
+}
+
 __global__ void ndgi_step_count_kernel(int* steps, const uint32_t* tile_ids, int n, int num_tiles) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
@@ -453,6 +500,17 @@ __global__ void ndgi_step_count_kernel(int* steps, const uint32_t* tile_ids, int
 __global__ void ndgi_f16_to_f32_kernel(const uint16_t* in, float* out, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         out[i] = half_bits_to_float(in[i]);
+}
+// rows x cols, row strides in elements (the MLP part of full parameter vectors)
+__global__ void ndgi_f32_to_f16_2d_kernel(const float* in, size_t in_stride, uint16_t* out, size_t out_stride,
+                                          size_t rows, size_t cols) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < rows * cols; i += (size_t)gridDim.x * blockDim.x)
+        out[(i / cols) * out_stride + i % cols] = __half_as_ushort(__float2half_rn(in[(i / cols) * in_stride + i % cols]));
+}
+cudaError_t launch_convert_f32_f16_2d(const float* in, size_t in_stride, uint16_t* out, size_t out_stride, size_t rows,
+                                      size_t cols, cudaStream_t s) {
+    ndgi_f32_to_f16_2d_kernel<<<1024, 256, 0, s>>>(in, in_stride, out, out_stride, rows, cols);
+    return cudaGetLastError();
 }
 __global__ void ndgi_f32_to_f16_kernel(const float* in, uint16_t* out, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)

@@ -115,3 +115,34 @@ def test_full_trainer_rejects_wrong_step_kind():
     with pytest.raises(ndgi.NdgiError):
         tr.step(torch.tensor([0], dtype=torch.int32, device="cuda"), torch.from_numpy(smp).cuda(),
                 torch.from_numpy(tgt).cuda(), lr=1e-3, noise=None)
+
+
+def test_full_export_bit_exact_and_decodable():
+    # R30: Eq. 7 texels -> u8 PTQ -> BC7 mode 6, line grids -> u8, MLP -> f16,
+    # bit-identical to the oracle's export of the same fp32 parameters; the
+    # exported Theta loads and decodes (REF_FP32 mode: this small core) within 1e-5 of the oracle
+    lay, ctx, M, P, pm, init = _setup()
+    tr = ndgi.Trainer(ctx, full_init=torch.from_numpy(init).cuda())
+    tiles = [0, 2, 3]
+    smp, tgt = S.train_batch(tiles, 512, 4)
+    noise = np.random.default_rng(2).uniform(-0.5, 0.5, (3, 512, 12)).astype(np.float32)
+    for _ in range(3):
+        tr.step(torch.tensor(tiles, dtype=torch.int32, device="cuda"), torch.from_numpy(smp).cuda(),
+                torch.from_numpy(tgt).cuda(), lr=1e-2, noise=torch.from_numpy(noise).cuda())
+    w = torch.zeros((lay["num_tiles"], P), device="cuda")
+    tr.weights(w)
+    out = tr.export_full()
+    torch.cuda.synchronize()
+    exp = M.train_full_export(w.cpu().numpy())
+    for key in ("uv", "uvt", "ut", "vt"):
+        np.testing.assert_array_equal(out[key].cpu().numpy(), exp[key], err_msg=key)
+    np.testing.assert_array_equal(out["mlp"].cpu().numpy().view(np.uint16), exp["mlp"])
+    lay2 = dict(lay, fmt_uv="bc7", fmt_uvt="bc7", fmt_line="u8")
+    ctx2 = ndgi.ndgi_load(lay2, out, 0)
+    C = lay["core"]
+    y = torch.zeros((1, lay["tiles_y"] * C, lay["tiles_x"] * C, 4), device="cuda")
+    ndgi.ndgi_decode_full(ctx2, 0.4, y, "rgba32f", "ref_fp32")
+    torch.cuda.synchronize()
+    ref = oracle.Model(lay2, exp).decode_full(0.4)
+    d = np.abs(y.cpu().numpy()[..., :3] - ref[0])
+    assert d.max() <= 1e-5
