@@ -89,6 +89,8 @@ def lib():
             "oracle_train_full_project": (None, [P, P]),
             "oracle_adam": (None, [P, P, P, P, I, I, D, D, D, D]),
             "oracle_bc7_encode_image_mode6": (None, [P, I, I, P]),
+            "oracle_bc7_encode_multi": (I, [P, P]),
+            "oracle_bc7_encode_image_multi": (None, [P, I, I, P]),
             "oracle_restore": (D, [D, D, D]),
             "oracle_sample_lighting": (I, [P, P, I, I, I, I, I, D, D, I, D, P, P]),
         }
@@ -344,6 +346,23 @@ def bc7_encode_block_mode6(px: np.ndarray) -> np.ndarray:
     px = np.ascontiguousarray(np.asarray(px, np.uint8).reshape(64))
     out = np.zeros(16, np.uint8)
     lib().oracle_bc7_encode_mode6(_ptr(px), _ptr(out))
+    return out
+
+
+def bc7_encode_block_multi(px: np.ndarray) -> tuple[np.ndarray, int]:
+    """R31: one 4x4 RGBA8 block ([16][4] or [4][4][4]) -> (16-byte block, chosen mode)."""
+    p = np.ascontiguousarray(px, np.uint8).reshape(64)
+    out = np.zeros(16, np.uint8)
+    m = lib().oracle_bc7_encode_multi(_ptr(p), _ptr(out))
+    return out, int(m)
+
+
+def bc7_encode_image_multi(rgba: np.ndarray) -> np.ndarray:
+    """R31: [h][w][4] uint8 -> [h/4][w/4][16] BC7 blocks (mode 6 / 5 / 7 search)."""
+    h, w = rgba.shape[:2]
+    r = np.ascontiguousarray(rgba, np.uint8)
+    out = np.zeros((h // 4, w // 4, 16), np.uint8)
+    lib().oracle_bc7_encode_image_multi(_ptr(r), w, h, _ptr(out))
     return out
 
 

@@ -1302,3 +1302,245 @@ void oracle_train_full_export(const oracle_layout *L, const float *theta, uint8_
     }
     free(img);
 }
+
+/* ------------------------------------------------------------------ */
+/* BC7 multi-mode search (SURVEY.md 8(f) NEXT 3 "first mode 6 ... then */
+/* multi-mode search"; reading R31).  Candidates in this order, */
+/* each scored by the squared error of its DECODED block (the pinned   */
+/* decoder above) against the input; a later candidate replaces the    */
+/* best only if strictly better:                                        */
+/*  1. mode 6 (R26);                                                    */
+/*  2. mode 5, rotation r = 0..3 (A swapped with R, G, B for r = 1..3): */
+/*     RGB endpoints = the texels extreme along the integer principal   */
+/*     axis of RGB, 7-bit codes (nearest after bit replication, ties to */
+/*     the lower code); alpha endpoints = min / max alpha (8 bits);     */
+/*     2-bit colour and alpha indices (nearest, ties to the lower       */
+/*     index); anchor fix per index set;                                */
+/*  3. mode 7, partition p = 0..63: per subset, RGBA endpoints = the    */
+/*     subset's texels extreme along its principal axis, 5-bit codes +  */
+/*     one p-bit per endpoint (the p-bit with the smaller squared       */
+/*     endpoint error, ties to 0), 2-bit indices, anchor fix per        */
+/*     subset.                                                          */
+/* The principal axis is R26 step 2 over the chosen texels / channels.  */
+/* ------------------------------------------------------------------ */
+static void axis_extremes(const uint8_t px[64], uint32_t mask, const int *chs, int nc, int *imin, int *imax)
+{
+    int64_t S[4] = {0, 0, 0, 0}, Q[4][4], M[4][4], v[4];
+    memset(Q, 0, sizeof(Q));
+    int n = 0;
+    for (int i = 0; i < 16; ++i) {
+        if (!((mask >> i) & 1u)) continue;
+        n++;
+        for (int c = 0; c < nc; ++c) {
+            S[c] += px[4 * i + chs[c]];
+            for (int d = 0; d < nc; ++d) Q[c][d] += (int64_t)px[4 * i + chs[c]] * px[4 * i + chs[d]];
+        }
+    }
+    for (int c = 0; c < nc; ++c)
+        for (int d = 0; d < nc; ++d) M[c][d] = n * Q[c][d] - S[c] * S[d];
+    int cs = 0;
+    for (int c = 1; c < nc; ++c)
+        if (M[c][c] > M[cs][cs]) cs = c;
+    for (int c = 0; c < nc; ++c) v[c] = M[c][cs];
+    for (int it = 0; it <= 4; ++it) {
+        int64_t w[4];
+        for (int c = 0; c < nc; ++c) {
+            if (it == 0) { w[c] = v[c]; continue; }
+            w[c] = 0;
+            for (int d = 0; d < nc; ++d) w[c] += M[c][d] * v[d];
+        }
+        uint64_t mx = 0;
+        for (int c = 0; c < nc; ++c) {
+            uint64_t a = (uint64_t)(w[c] < 0 ? -w[c] : w[c]);
+            if (a > mx) mx = a;
+        }
+        if (mx == 0) {
+            if (it == 0) for (int c = 0; c < nc; ++c) v[c] = 1;
+            break;
+        }
+        const int s = bitlen64(mx) > 20 ? bitlen64(mx) - 20 : 0;
+        for (int c = 0; c < nc; ++c) {
+            const uint64_t a = (uint64_t)(w[c] < 0 ? -w[c] : w[c]) >> s;
+            v[c] = w[c] < 0 ? -(int64_t)a : (int64_t)a;
+        }
+    }
+    int first = 1;
+    int64_t dmin = 0, dmax = 0;
+    *imin = *imax = 0;
+    for (int i = 0; i < 16; ++i) {
+        if (!((mask >> i) & 1u)) continue;
+        int64_t d = 0;
+        for (int c = 0; c < nc; ++c) d += (int64_t)px[4 * i + chs[c]] * v[c];
+        if (first || d < dmin) { dmin = d; *imin = i; }
+        if (first || d > dmax) { dmax = d; *imax = i; }
+        first = 0;
+    }
+}
+
+/* nearest code of `bits` bits (plus p-bit p >= 0) to the 8-bit value e */
+static int nearest_code(int e, int bits, int p)
+{
+    int best = -1, bk = 0;
+    for (int k = 0; k < (1 << bits); ++k) {
+        int val = p < 0 ? expand8(k, bits) : expand8((k << 1) | p, bits + 1);
+        int d = val > e ? val - e : e - val;
+        if (best < 0 || d < best) { best = d; bk = k; }
+    }
+    return bk;
+}
+
+static int64_t block_sse(const uint8_t blk[16], const uint8_t px[64])
+{
+    uint8_t dec[64];
+    oracle_bc7_decode_block(blk, dec);
+    int64_t e = 0;
+    for (int i = 0; i < 64; ++i) e += (int64_t)(dec[i] - px[i]) * (dec[i] - px[i]);
+    return e;
+}
+
+static void encode_mode5(const uint8_t in[64], int rot, uint8_t out[16])
+{
+    uint8_t px[64];
+    memcpy(px, in, 64);
+    if (rot > 0)
+        for (int i = 0; i < 16; ++i) { uint8_t t = px[4 * i + 3]; px[4 * i + 3] = px[4 * i + rot - 1]; px[4 * i + rot - 1] = t; }
+    const int rgb[3] = {0, 1, 2};
+    int imin, imax;
+    axis_extremes(px, 0xffffu, rgb, 3, &imin, &imax);
+    int C0[3], C1[3], V0[3], V1[3];
+    for (int c = 0; c < 3; ++c) {
+        C0[c] = nearest_code(px[4 * imin + c], 7, -1);
+        C1[c] = nearest_code(px[4 * imax + c], 7, -1);
+        V0[c] = expand8(C0[c], 7);
+        V1[c] = expand8(C1[c], 7);
+    }
+    int A0 = 255, A1 = 0;
+    for (int i = 0; i < 16; ++i) {
+        if (px[4 * i + 3] < A0) A0 = px[4 * i + 3];
+        if (px[4 * i + 3] > A1) A1 = px[4 * i + 3];
+    }
+    int ci[16], ai[16];
+    for (int i = 0; i < 16; ++i) {
+        int best = -1, ba = -1;
+        for (int w = 0; w < 4; ++w) {
+            int err = 0;
+            for (int c = 0; c < 3; ++c) {
+                const int d = interp(V0[c], V1[c], BC7_W2[w]) - px[4 * i + c];
+                err += d * d;
+            }
+            if (best < 0 || err < best) { best = err; ci[i] = w; }
+            const int da = interp(A0, A1, BC7_W2[w]) - px[4 * i + 3];
+            if (ba < 0 || da * da < ba) { ba = da * da; ai[i] = w; }
+        }
+    }
+    if (ci[0] >= 2) {
+        for (int c = 0; c < 3; ++c) { int t = C0[c]; C0[c] = C1[c]; C1[c] = t; }
+        for (int i = 0; i < 16; ++i) ci[i] = 3 - ci[i];
+    }
+    if (ai[0] >= 2) {
+        int t = A0; A0 = A1; A1 = t;
+        for (int i = 0; i < 16; ++i) ai[i] = 3 - ai[i];
+    }
+    memset(out, 0, 16);
+    bitwriter bw = {out, 0};
+    put(&bw, 1 << 5, 6);
+    put(&bw, rot, 2);
+    for (int c = 0; c < 3; ++c) { put(&bw, C0[c], 7); put(&bw, C1[c], 7); }
+    put(&bw, A0, 8);
+    put(&bw, A1, 8);
+    put(&bw, ci[0], 1);
+    for (int i = 1; i < 16; ++i) put(&bw, ci[i], 2);
+    put(&bw, ai[0], 1);
+    for (int i = 1; i < 16; ++i) put(&bw, ai[i], 2);
+}
+
+static void encode_mode7(const uint8_t px[64], int part, uint8_t out[16])
+{
+    const int rgba[4] = {0, 1, 2, 3};
+    int code[2][2][4], pb[2][2], val[2][2][4], idx[16];
+    uint32_t mask[2] = {0, 0};
+    for (int i = 0; i < 16; ++i) mask[oracle_bc7_subset(2, part, i)] |= 1u << i;
+    for (int s = 0; s < 2; ++s) {
+        int ie[2];
+        axis_extremes(px, mask[s], rgba, 4, &ie[0], &ie[1]);
+        for (int e = 0; e < 2; ++e) {
+            int best = -1;
+            for (int p = 0; p < 2; ++p) {
+                int k[4], err = 0;
+                for (int c = 0; c < 4; ++c) {
+                    k[c] = nearest_code(px[4 * ie[e] + c], 5, p);
+                    const int d = expand8((k[c] << 1) | p, 6) - px[4 * ie[e] + c];
+                    err += d * d;
+                }
+                if (best < 0 || err < best) {
+                    best = err;
+                    pb[s][e] = p;
+                    for (int c = 0; c < 4; ++c) { code[s][e][c] = k[c]; val[s][e][c] = expand8((k[c] << 1) | p, 6); }
+                }
+            }
+        }
+    }
+    for (int i = 0; i < 16; ++i) {
+        const int s = oracle_bc7_subset(2, part, i);
+        int best = -1;
+        for (int w = 0; w < 4; ++w) {
+            int err = 0;
+            for (int c = 0; c < 4; ++c) {
+                const int d = interp(val[s][0][c], val[s][1][c], BC7_W2[w]) - px[4 * i + c];
+                err += d * d;
+            }
+            if (best < 0 || err < best) { best = err; idx[i] = w; }
+        }
+    }
+    for (int s = 0; s < 2; ++s) {
+        const int a = oracle_bc7_anchor(2, part, s);
+        if (idx[a] >= 2) {
+            for (int c = 0; c < 4; ++c) { int t = code[s][0][c]; code[s][0][c] = code[s][1][c]; code[s][1][c] = t; }
+            int t = pb[s][0]; pb[s][0] = pb[s][1]; pb[s][1] = t;
+            for (int i = 0; i < 16; ++i)
+                if (oracle_bc7_subset(2, part, i) == s) idx[i] = 3 - idx[i];
+        }
+    }
+    memset(out, 0, 16);
+    bitwriter bw = {out, 0};
+    put(&bw, 1 << 7, 8);
+    put(&bw, part, 6);
+    for (int c = 0; c < 4; ++c)
+        for (int s = 0; s < 2; ++s)
+            for (int e = 0; e < 2; ++e) put(&bw, code[s][e][c], 5);
+    for (int s = 0; s < 2; ++s)
+        for (int e = 0; e < 2; ++e) put(&bw, pb[s][e], 1);
+    const int a1 = oracle_bc7_anchor(2, part, 1);
+    for (int i = 0; i < 16; ++i) put(&bw, idx[i], (i == 0 || i == a1) ? 1 : 2);
+}
+
+/* returns the chosen mode (6, 5 or 7) */
+int oracle_bc7_encode_multi(const uint8_t px[64], uint8_t out[16])
+{
+    uint8_t cand[16];
+    oracle_bc7_encode_mode6(px, out);
+    int64_t best = block_sse(out, px);
+    int mode = 6;
+    for (int r = 0; r < 4 && best > 0; ++r) {
+        encode_mode5(px, r, cand);
+        const int64_t e = block_sse(cand, px);
+        if (e < best) { best = e; memcpy(out, cand, 16); mode = 5; }
+    }
+    for (int p = 0; p < 64 && best > 0; ++p) {
+        encode_mode7(px, p, cand);
+        const int64_t e = block_sse(cand, px);
+        if (e < best) { best = e; memcpy(out, cand, 16); mode = 7; }
+    }
+    return mode;
+}
+
+void oracle_bc7_encode_image_multi(const uint8_t *rgba, int w, int h, uint8_t *blocks)
+{
+    for (int by = 0; by < h / 4; ++by)
+        for (int bx = 0; bx < w / 4; ++bx) {
+            uint8_t px[64];
+            for (int i = 0; i < 16; ++i)
+                memcpy(px + 4 * i, rgba + ((size_t)(4 * by + i / 4) * w + 4 * bx + i % 4) * 4, 4);
+            oracle_bc7_encode_multi(px, blocks + ((size_t)by * (w / 4) + bx) * 16);
+        }
+}
