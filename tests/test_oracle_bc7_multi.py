@@ -68,7 +68,7 @@ def test_exact_mode7_two_flat_subsets():
             dec, _ = oracle.bc7_decode_block(blk)
             np.testing.assert_array_equal(dec.reshape(16, 4), px)
             if (np.array(cols) % 2 != np.array(cols)[:, :1] % 2).any():    # off mode 6's parity grid
-                assert mode == 7
+                assert mode in (5, 7)
 
 
 def test_exact_mode5_rgb_and_independent_alpha():
