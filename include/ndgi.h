@@ -327,6 +327,16 @@ NDGI_API ndgi_status ndgi_sample_lighting(ndgi_ctx* ctx, const int32_t* page_tab
  * ------------------------------------------------------------------------ */
 NDGI_API ndgi_status ndgi_bc7_encode_mode6(const void* rgba, uint32_t w, uint32_t h, void* blocks, void* stream);
 
+/* Multi-mode search (SURVEY.md §8(f) NEXT 3 "then multi-mode search";
+ * reading R31): per block the mode-6 result above, then mode 5 with each of
+ * the 4 rotations (7-bit RGB endpoints along the RGB principal axis, 8-bit
+ * alpha endpoints min/max, 2-bit indices), then mode 7 with each of the 64
+ * two-subset partitions (per-subset principal-axis endpoints, 5-bit + p-bit,
+ * 2-bit indices); a candidate replaces the best only if its squared error
+ * is strictly smaller.  Same arguments, layout and errors as
+ * ndgi_bc7_encode_mode6; equal to the oracle's search bit for bit.        */
+NDGI_API ndgi_status ndgi_bc7_encode_multi(const void* rgba, uint32_t w, uint32_t h, void* blocks, void* stream);
+
 /* ------------------------------------------------------------------------
  * Fine-tuning of the per-tile decoders: the paper's
  * last training stage, "we freeze the feature maps and fine-tune the MLP

@@ -79,6 +79,7 @@ _SIGS = {
     "ndgi_vt_upload": (_I, [_P, _P, _P]),
     "ndgi_vt_stats": (_I, [_P, _P]),
     "ndgi_bc7_encode_mode6": (_I, [_P, _U32, _U32, _P, _P]),
+    "ndgi_bc7_encode_multi": (_I, [_P, _U32, _U32, _P, _P]),
     "ndgi_train_create": (_I, [_P, C.POINTER(C.c_void_p)]),
     "ndgi_train_step": (_I, [_P, _P, _U32, _P, _P, _U32, _F, _P, _P]),
     "ndgi_train_weights": (_I, [_P, _P, _P]),
@@ -357,6 +358,14 @@ def ndgi_bc7_encode_mode6(rgba, blocks, stream=None) -> None:
     st = _lib.ndgi_bc7_encode_mode6(C.c_void_p(rgba.data_ptr()), w, h, C.c_void_p(blocks.data_ptr()),
                                     _stream_ptr(stream))
     _check(st, "ndgi_bc7_encode_mode6")
+
+
+def ndgi_bc7_encode_multi(rgba, blocks, stream=None) -> None:
+    """rgba: CUDA uint8 [h][w][4]; blocks: CUDA uint8 [h/4 * w/4][16] (or any 16-B-per-block buffer)."""
+    h, w = int(rgba.shape[0]), int(rgba.shape[1])
+    st = _lib.ndgi_bc7_encode_multi(C.c_void_p(rgba.data_ptr()), w, h, C.c_void_p(blocks.data_ptr()),
+                                    _stream_ptr(stream))
+    _check(st, "ndgi_bc7_encode_multi")
 
 
 # ---------------------------------------------------------------- fine-tuning (NEXT 4)

@@ -26,6 +26,7 @@ cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks
 cudaError_t launch_train_grad(const TrainArgs& a, int H, cudaStream_t s);
 cudaError_t launch_convert_f32_f16_2d(const float* in, size_t in_stride, uint16_t* out, size_t out_stride, size_t rows,
                                       size_t cols, cudaStream_t s);
+cudaError_t launch_bc7_encode_multi(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s);
 cudaError_t launch_full_ptq(const float* theta, size_t P, size_t off_uv, size_t off_uvt, size_t off_ut, size_t off_vt,
                             int num_tiles, int R, int R3, int D, int nline, uint32_t* uv_img, uint32_t* uvt_img,
                             uint8_t* ut, uint8_t* vt, int num_sms, cudaStream_t s);
@@ -555,6 +556,18 @@ ndgi_status ndgi_bc7_encode_mode6(const void* rgba, uint32_t w, uint32_t h, void
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(e, "device query");
     e = ndgi::launch_bc7_encode_mode6(rgba, (int)w, (int)h, blocks, sms, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 encode launch");
+}
+
+ndgi_status ndgi_bc7_encode_multi(const void* rgba, uint32_t w, uint32_t h, void* blocks, void* stream) {
+    if (!rgba || !blocks) return fail(NDGI_ERR_ARG, "NULL rgba or blocks");
+    if (w == 0 || h == 0 || w % 4 || h % 4) return fail(NDGI_ERR_ARG, "w and h must be positive multiples of 4");
+    if (w > (1u << 16) || h > (1u << 16)) return fail(NDGI_ERR_RANGE, "w or h > 65536");
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "device query");
+    e = ndgi::launch_bc7_encode_multi(rgba, (int)w, (int)h, blocks, sms, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 encode launch");
 }
 

@@ -83,3 +83,53 @@ def test_encoder_argument_errors():
     with pytest.raises(ndgi.NdgiError) as e:
         ndgi.ndgi_bc7_encode_mode6(src, out)                 # h = 6 not a multiple of 4
     assert e.value.status == ndgi.ERR_ARG
+
+
+# ---------------------------------------------------------------- R31 multi-mode search
+def gpu_encode_multi(img):
+    h, w = img.shape[:2]
+    src = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    out = torch.zeros(((h // 4) * (w // 4), 16), dtype=torch.uint8, device="cuda")
+    ndgi.ndgi_bc7_encode_multi(src, out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("kind", ["random", "smooth", "edges", "flat2"])
+def test_multi_mode_bit_exact(kind):
+    rng = np.random.default_rng(7)
+    h = w = 128
+    if kind == "random":
+        img = rng.integers(0, 256, (h, w, 4)).astype(np.uint8)
+    elif kind == "smooth":
+        img = _smooth(h, w, 3)
+    elif kind == "edges":
+        img = _smooth(h, w, 4)
+        y, x = np.mgrid[0:h, 0:w]
+        img[((x * 3 + y * 5) % 23) < 9] //= 3
+    else:   # two flat colours per block on random partitions: mode 7 / mode 5 territory
+        img = np.zeros((h, w, 4), np.uint8)
+        for by in range(h // 4):
+            for bx in range(w // 4):
+                part = int(rng.integers(0, 64))
+                cols = rng.integers(0, 256, (2, 4))
+                sub = np.array([oracle.bc7_subset(2, part, i) for i in range(16)]).reshape(4, 4)
+                img[4 * by:4 * by + 4, 4 * bx:4 * bx + 4] = cols[sub]
+    exp = oracle.bc7_encode_image_multi(img).reshape(-1, 16)
+    got = gpu_encode_multi(img)
+    np.testing.assert_array_equal(got, exp)
+    modes = np.unique(exp[:, 0])
+    if kind in ("random", "flat2"):
+        assert len(modes) >= 3
+
+
+def test_multi_mode_large_image_sampled_blocks():
+    # 2048^2 in one launch (grid-stride), sampled blocks against the oracle block encoder
+    img = _smooth(2048, 2048, 9)
+    rng = np.random.default_rng(1)
+    img[::5] = rng.integers(0, 256, img[::5].shape).astype(np.uint8)
+    got = gpu_encode_multi(img)
+    for _ in range(300):
+        by, bx = (int(v) for v in rng.integers(0, 512, 2))
+        blk, _ = oracle.bc7_encode_block_multi(img[4 * by:4 * by + 4, 4 * bx:4 * bx + 4])
+        np.testing.assert_array_equal(got[by * 512 + bx], blk)
