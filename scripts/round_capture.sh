@@ -12,4 +12,14 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ndgi_fused -s 3 -c 1 \
    -o gpurun_out/${TAG}_fused $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
+
+# summaries on the box (the full report can exceed gpurun's 64 MiB copy-back)
+if [ -f gpurun_out/${TAG}_fused.ncu-rep ]; then
+  python scripts/ncu_summary.py gpurun_out/${TAG}_fused.ncu-rep gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_fused.txt 2>&1
+  python scripts/ncu_hot.py gpurun_out/${TAG}_fused.ncu-rep 40 > gpurun_out/${TAG}_fused_hot_sass.txt 2>&1
+  ncu -i gpurun_out/${TAG}_fused.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_src.csv 2>/dev/null
+  python scripts/ncu_regions.py gpurun_out/${TAG}_src.csv > gpurun_out/${TAG}_fused_regions.txt 2>&1
+  rm -f gpurun_out/${TAG}_src.csv
+  find gpurun_out -name '*.ncu-rep' -size +40M -delete
+fi
 echo done
