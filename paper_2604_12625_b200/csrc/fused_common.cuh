@@ -103,6 +103,12 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
 }
 
 // ---- GELU epilogue of one layer: D (fp32) -> f16x2 GELU~ -> A23 ---------------
+// NDGI_POLY_PAIRS of every 8 f16x2 GELU pairs run on the FMA pipe
+// (gelu_poly_f16x2) instead of MUFU.TANH: the MUFU queue (mio_throttle) is the
+// hot loop's main stall; 1 of 8 measured best
+#ifndef NDGI_POLY_PAIRS
+#define NDGI_POLY_PAIRS 1
+#endif
 template <int H>
 __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) {
 #pragma unroll
@@ -111,8 +117,10 @@ __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) 
         ptx::tmem_ld_x16(d_addr + c0, d);
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1])));
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t x = pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
+            g[q] = q < 8 - NDGI_POLY_PAIRS ? gelu_scaled_f16x2(x) : gelu_poly_f16x2(x);
+        }
         ptx::tmem_st_x8(a_addr + c0 / 2, g);
     }
 }
@@ -122,6 +130,7 @@ __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) 
 #ifndef NDGI_F16ACC
 #define NDGI_F16ACC 1
 #endif
+
 
 // h = 16, S items with f16 accumulators (layers 1, 2): tcgen05.ld .pack::16b
 // delivers the 16 pre-activations as 8 f16x2 words -- no fp32 -> f16 packing
@@ -135,7 +144,7 @@ __device__ __forceinline__ void gelu_epilogue_h16_f16acc(uint32_t d0, uint32_t a
     for (int s = 0; s < S; ++s) {
         uint32_t g[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) g[q] = gelu_scaled_f16x2(x[s][q]);
+        for (int q = 0; q < 8; ++q) g[q] = q < 8 - NDGI_POLY_PAIRS ? gelu_scaled_f16x2(x[s][q]) : gelu_poly_f16x2(x[s][q]);
         ptx::tmem_st_x8(a0 + s * stride, g);
     }
 }

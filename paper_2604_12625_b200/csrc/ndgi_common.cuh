@@ -167,6 +167,24 @@ __device__ __forceinline__ uint32_t gelu_scaled_f16x2(uint32_t h) {
     return g;
 }
 
+// GELU~ on the FMA pipe (experiment, NDGI_POLY_PAIRS): g = h + (h hc) Q(hc^2),
+// hc = clamp(h, +-2.5), h Q(h^2) a degree-11 odd least-squares fit of
+// tanh(h (1 + c h^2)) on [0, 2.5] -- no MUFU, ~10 HFMA2-pipe instructions
+__device__ __forceinline__ uint32_t gelu_poly_f16x2(uint32_t h) {
+    uint32_t hc, s, q, hh, g;
+    asm("min.f16x2 %0, %1, %2;" : "=r"(hc) : "r"(h), "r"(0x41004100u));
+    asm("max.f16x2 %0, %1, %2;" : "=r"(hc) : "r"(hc), "r"(0xC100C100u));
+    asm("mul.rn.f16x2 %0, %1, %1;" : "=r"(s) : "r"(hc));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(q) : "r"(s), "r"(0x82428242u), "r"(0x12EB12EBu));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(s), "r"(0xA0A7A0A7u));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(s), "r"(0x2B7B2B7Bu));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(s), "r"(0xB429B429u));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(q) : "r"(q), "r"(s), "r"(0x3BFF3BFFu));
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(hh) : "r"(h), "r"(hc));
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(g) : "r"(hh), "r"(q), "r"(h));
+    return g;
+}
+
 __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

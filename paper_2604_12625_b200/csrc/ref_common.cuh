@@ -15,29 +15,31 @@ struct Map2D {
     int fmt, rx, ry, nc;
 };
 
+// packed texel of the other block formats (BC1 / BC3 / BC5), out of line so
+// the taps that inline fetch_texel do not each carry these decoders
+static __device__ __noinline__ uint32_t bcn_texel(const uint8_t* base, int fmt, size_t bi, int i) {
+    if (fmt == FMT_BC1) return bc1_texel(__ldg(reinterpret_cast<const uint2*>(base) + bi), i, false);
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(base) + bi);
+    if (fmt == FMT_BC3)
+        return (bc1_texel(make_uint2(raw.z, raw.w), i, true) & 0x00ffffffu) | bc4_texel(make_uint2(raw.x, raw.y), i) << 24;
+    return bc4_texel(make_uint2(raw.x, raw.y), i) | bc4_texel(make_uint2(raw.z, raw.w), i) << 8;   // BC5
+}
+
 // all channels of texel (a, b), dequantised (R8)
 __device__ __forceinline__ void fetch_texel(const Map2D& m, int a, int b, float* out) {
-    if (m.fmt == FMT_BC7 || m.fmt == FMT_BC1 || m.fmt == FMT_BC3 || m.fmt == FMT_BC5) {
-        const size_t bi = (size_t)(b >> 2) * (m.rx >> 2) + (a >> 2);
-        const int i = 4 * (b & 3) + (a & 3);
-        uint32_t v;
-        if (m.fmt == FMT_BC1) {
-            v = bc1_texel(__ldg(reinterpret_cast<const uint2*>(m.base) + bi), i, false);
-        } else {
-            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(m.base) + bi);
-            if (m.fmt == FMT_BC7) v = bc7_texel(raw, i);
-            else if (m.fmt == FMT_BC3)
-                v = (bc1_texel(make_uint2(raw.z, raw.w), i, true) & 0x00ffffffu) |
-                    bc4_texel(make_uint2(raw.x, raw.y), i) << 24;
-            else v = bc4_texel(make_uint2(raw.x, raw.y), i) | bc4_texel(make_uint2(raw.z, raw.w), i) << 8;   // BC5
-        }
+    if (m.fmt == FMT_BC7) {
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(m.base) + (b >> 2) * (m.rx >> 2) + (a >> 2));
+        const uint32_t v = bc7_texel(raw, 4 * (b & 3) + (a & 3));
         for (int c = 0; c < m.nc; ++c) out[c] = (float)((v >> (8 * c)) & 0xffu) / 255.0f;
     } else if (m.fmt == FMT_U8) {
         const uint8_t* p = m.base + ((size_t)b * m.rx + a) * m.nc;
         for (int c = 0; c < m.nc; ++c) out[c] = (float)p[c] / 255.0f;
-    } else {
+    } else if (m.fmt == FMT_F16) {
         const uint16_t* p = reinterpret_cast<const uint16_t*>(m.base) + ((size_t)b * m.rx + a) * m.nc;
         for (int c = 0; c < m.nc; ++c) out[c] = half_bits_to_float(p[c]);
+    } else {   // BC1 / BC3 / BC5
+        const uint32_t v = bcn_texel(m.base, m.fmt, (size_t)(b >> 2) * (m.rx >> 2) + (a >> 2), 4 * (b & 3) + (a & 3));
+        for (int c = 0; c < m.nc; ++c) out[c] = (float)((v >> (8 * c)) & 0xffu) / 255.0f;
     }
 }
 
