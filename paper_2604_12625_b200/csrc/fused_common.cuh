@@ -105,9 +105,12 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
 // ---- GELU epilogue of one layer: D (fp32) -> f16x2 GELU~ -> A23 ---------------
 // NDGI_POLY_PAIRS of every 8 f16x2 GELU pairs run on the FMA pipe
 // (gelu_poly_f16x2) instead of MUFU.TANH: the MUFU queue (mio_throttle) is the
-// hot loop's main stall; 1 of 8 measured best
+// hot loop's main stall; 2 + 1 of the step's 16 measured best
 #ifndef NDGI_POLY_PAIRS
 #define NDGI_POLY_PAIRS 1
+#endif
+#ifndef NDGI_POLY_PAIRS_ITEM0   // the first item of a step: 2 of 8 (measured)
+#define NDGI_POLY_PAIRS_ITEM0 2
 #endif
 template <int H>
 __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) {
@@ -144,7 +147,9 @@ __device__ __forceinline__ void gelu_epilogue_h16_f16acc(uint32_t d0, uint32_t a
     for (int s = 0; s < S; ++s) {
         uint32_t g[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) g[q] = q < 8 - NDGI_POLY_PAIRS ? gelu_scaled_f16x2(x[s][q]) : gelu_poly_f16x2(x[s][q]);
+        for (int q = 0; q < 8; ++q)
+            g[q] = q < 8 - (s == 0 ? NDGI_POLY_PAIRS_ITEM0 : NDGI_POLY_PAIRS) ? gelu_scaled_f16x2(x[s][q])
+                                                                            : gelu_poly_f16x2(x[s][q]);
         ptx::tmem_st_x8(a0 + s * stride, g);
     }
 }
