@@ -75,6 +75,15 @@ __device__ __forceinline__ uint32_t sel8(const uint32_t p[8], uint32_t q) {
     return (q & 4u) ? hi : lo;
 }
 
+// the 8 BC4 palette bytes packed into two words: entry q = byte q of {hi:lo},
+// so a lookup is one PRMT (byte_perm selects by a 3-bit index)
+__device__ __forceinline__ void bc4_palette_packed(uint32_t lo, uint32_t& plo, uint32_t& phi) {
+    uint32_t p[8];
+    bc4_palette(lo, p);
+    plo = p[0] | p[1] << 8 | p[2] << 16 | p[3] << 24;
+    phi = p[4] | p[5] << 8 | p[6] << 16 | p[7] << 24;
+}
+
 __device__ __forceinline__ uint32_t bc4_index(uint2 w, int i) {
     const uint64_t v = (uint64_t)w.y << 32 | w.x;
     return (uint32_t)(v >> (16 + 3 * i)) & 7u;
@@ -91,13 +100,16 @@ __device__ __forceinline__ void bc1_decode(uint2 w, bool always4, Sink&& sink) {
 
 template <class Sink>
 __device__ __forceinline__ void bc3_decode(uint4 raw, Sink&& sink) {
-    uint32_t pal[4], apal[8];
+    uint32_t pal[4], alo, ahi;
     bc1_palette(raw.z, true, pal);
-    bc4_palette(raw.x, apal);
+    bc4_palette_packed(raw.x, alo, ahi);
     const uint2 aw = make_uint2(raw.x, raw.y);
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-        sink(i, (sel4(pal, (raw.w >> (2 * i)) & 3u) & 0x00ffffffu) | sel8(apal, bc4_index(aw, i)) << 24);
+    for (int i = 0; i < 16; ++i) {
+        // colour bytes 0..2, then palette byte q of {ahi:alo} as byte 3
+        const uint32_t a = __byte_perm(alo, ahi, bc4_index(aw, i));
+        sink(i, __byte_perm(sel4(pal, (raw.w >> (2 * i)) & 3u), a, 0x4210u));
+    }
 }
 
 // single texels (reference / training paths)
