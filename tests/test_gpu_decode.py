@@ -400,6 +400,35 @@ def test_c2_fullsize_sampled():
             assert mx <= FAST_MAX and mean <= FAST_MEAN
 
 
+@pytest.mark.parametrize("name", ["c5:M:bc3", "c5:M:bc1", "c5:H:bc3", "c5:M64:bc7"])
+def test_c5_fullsize_sampled(name):
+    """Config 5 cells at full size (c2's 1,024-tile atlas), four times per call
+    (RGBA8 and RGBA32F): sampled texels against the oracle one by one; RGBA8 =
+    the oracle's quantiser of the kernel's own fp32 output."""
+    lay, seed = S.config(name)
+    th = S.make_theta(lay, seed)
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    ts = [i / 24 for i in (0, 7, 13, 23)]
+    y32 = gpu_full(ctx, ts, "rgba32f")
+    q8 = gpu_full(ctx, ts, "rgba8")
+    rng = np.random.default_rng(3)
+    C = 128
+    errs = []
+    for _ in range(150):
+        ti = int(rng.integers(0, len(ts)))
+        k = int(rng.integers(0, 1024))
+        i, j = (int(v) for v in rng.integers(0, C, 2))
+        tx, ty = k % 32, k // 32
+        exp = M.texel(k, i + 4, j + 4, ts[ti])
+        got = y32[ti, 0, ty * C + j, tx * C + i]
+        errs.append(np.abs(got[:3] - exp))
+        np.testing.assert_array_equal(q8[ti, 0, ty * C + j, tx * C + i],
+                                      oracle.quantize_rgba8(np.ascontiguousarray(got[None]))[0])
+    errs = np.array(errs)
+    assert errs.max() <= FAST_MAX and errs.mean() <= FAST_MEAN, (name, errs.max(), errs.mean())
+
+
 def test_c2_bench_launch_all_texels_of_one_time():
     """The exact launch bench.py times (config 2, decode_full_batch over the 24
     times, RGBA8, the FULL8 kernel): every texel of one time against the
