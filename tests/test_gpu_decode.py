@@ -467,3 +467,52 @@ def test_host_buffer_path():
     host = torch.zeros((3, 1, 256, 256, 4), dtype=torch.uint8).pin_memory()
     ndgi.ndgi_decode_full_host(ctx, ts, host, "rgba8")
     np.testing.assert_array_equal(host.numpy(), gpu_full(ctx, ts, "rgba8"))
+
+
+def _tile_oracle(seed, k, t):
+    """Oracle decode of global tile k alone (payloads depend only on (seed, k))."""
+    lay1 = S.layout(1, 1, 1, "M")
+    return oracle.Model(lay1, S.make_theta(lay1, seed, tiles=[k])).decode_tiles([0], t, NTHR)[0, 4:132, 4:132]
+
+
+def test_c4_full_scene_one_gpu_sampled():
+    """Config 4's whole 16,384-tile scene (4 x 8192^2 atlases, the maximum size)
+    in one decode_full call, RGBA8 and RGBA32F: sampled texels of the GPU output
+    against the oracle evaluated per global tile id."""
+    lay, seed = S.config("c4")
+    th = S.make_theta(lay, seed)
+    ctx = _load(lay, th)
+    t = 11 / 24
+    y = gpu_full(ctx, t, "rgba32f")[0]              # [4][8192][8192][4]
+    q = gpu_full(ctx, t, "rgba8")[0]
+    C = 128
+    rng = np.random.default_rng(11)
+    for k in [0, 16383, *rng.integers(1, 16383, 4).tolist()]:
+        a, r = divmod(int(k), 64 * 64)
+        ty, tx = divmod(r, 64)
+        exp = _tile_oracle(seed, int(k), t)
+        got = y[a, ty * C:(ty + 1) * C, tx * C:(tx + 1) * C]
+        mx, mean = _err(got, exp)
+        assert mx <= FAST_MAX and mean <= FAST_MEAN, (k, mx, mean)
+        np.testing.assert_array_equal(q[a, ty * C:(ty + 1) * C, tx * C:(tx + 1) * C],
+                                      oracle.quantize_rgba8(np.ascontiguousarray(got)))
+
+
+@pytest.mark.parametrize("rank", [0, 5])
+def test_c4_shard_of_eight_matches_global_tiles(rank):
+    """bench.py --workload c4 at N = 8: rank r holds tiles k % 8 == r in a
+    compact 64 x 32 atlas; each local tile l must equal the oracle's decode of
+    global tile shard_tiles(...)[l] (no hot-path communication needed)."""
+    from paper_2604_12625_b200 import parallel as par
+    _, seed = S.config("c4")
+    gids = par.shard_tiles(16384, 8, rank)
+    lay = S.layout(1, 64, len(gids) // 64, "M")
+    ctx = _load(lay, S.make_theta(lay, seed, tiles=gids))
+    t = 19 / 24
+    y = gpu_full(ctx, t, "rgba32f")[0, 0]
+    C = 128
+    rng = np.random.default_rng(rank)
+    for l in [0, len(gids) - 1, *rng.integers(1, len(gids) - 1, 3).tolist()]:
+        ty, tx = divmod(int(l), 64)
+        mx, mean = _err(y[ty * C:(ty + 1) * C, tx * C:(tx + 1) * C], _tile_oracle(seed, int(gids[l]), t))
+        assert mx <= FAST_MAX and mean <= FAST_MEAN, (rank, l, mx, mean)
