@@ -419,11 +419,25 @@ NDGI_API ndgi_status ndgi_debug_bc7_decode(const void* blocks, uint32_t w, uint3
  * independent hardware decoder for the cross-check.  Synchronous. */
 NDGI_API ndgi_status ndgi_debug_bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
 
-/* GELU-rate microbenchmark for the ALU roofline: runs the fused kernel's
- * GELU formulation (f16x2, tanh.approx) on `iters` x (grid*256*8) pairs and
- * returns the elapsed device milliseconds and activations evaluated.
- * Synchronous. */
-NDGI_API ndgi_status ndgi_debug_gelu_rate(uint32_t iters, float* ms, double* activations);
+/* GELU-rate microbenchmark for the ALU roofline (SURVEY.md §8(d) T_alu):
+ * the fused kernel's own f16x2 GELU epilogue functions on 148 x 2048 threads,
+ * 16 independent chains of GELU pairs per thread, `mufu_pairs` of every 16
+ * pairs through MUFU.TANH (tanh.approx.f16x2) and the rest through the
+ * FMA-pipe polynomial; pack_f32 != 0 first packs each pair from two fp32
+ * values (cvt.rn.f16x2.f32) as the fp32-accumulator epilogue does.  Returns
+ * the elapsed device milliseconds and activations evaluated (2 per pair).
+ * Errors: ARG, RANGE (mufu_pairs > 16), CUDA.  Synchronous. */
+NDGI_API ndgi_status ndgi_debug_gelu_rate(uint32_t iters, uint32_t mufu_pairs, int pack_f32, float* ms,
+                                          double* activations);
+
+/* The GELU formulation compiled into the fused kernel for hidden width h (16
+ * or 64): MUFU pairs of every 16 GELU pairs (the rest on the FMA pipe) and
+ * whether the hidden layers accumulate in fp32 (1) or f16 (0). */
+NDGI_API ndgi_status ndgi_debug_gelu_split(uint32_t hidden, uint32_t* mufu_pairs_of_16, int* fp32_acc);
+
+/* Launch-latency floor of the VT path: one empty kernel launched on `stream`
+ * through the C ABI (bench.py times it beside ndgi_decode_tiles). */
+NDGI_API ndgi_status ndgi_debug_null_launch(void* stream);
 
 /* tcgen05 round-trip microbenchmark (st A, barrier, MMA M128N16K16, commit,
  * mbarrier wait, ld D) on one CTA: SM cycles per iteration.  Synchronous. */
@@ -433,14 +447,6 @@ NDGI_API ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_i
  * host_out[128][24] receives columns 0..15 of every lane, then the same columns
  * read with .pack::16b (8 words).  Synchronous. */
 NDGI_API ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out);
-
-/* Cycle accounting of the fused kernel (only in builds with -DNDGI_PROFILE=1;
- * NDGI_ERR_UNSUPPORTED otherwise): sums over warps of SM cycles spent in
- * [barrier (incl. tcgen05.wait::st), MMA issue + mbarrier wait, GELU epilogues,
- * gather, output, unit prologue, total, steps, step loops, warp-0 MMA issue,
- * max resident CTAs per SM, sum of resident CTAs at CTA start] (12 words).
- * reset != 0 zeroes the counters. */
-NDGI_API ndgi_status ndgi_debug_fused_profile(uint64_t* out12, int reset);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,9 @@ Recipe (DESIGN.md "Input recipe"):
   order hashed (both BC1 colour modes, both BC4 palettes), indices hashed;
   "mixed" = all bits random;
 * MLP: PyTorch nn.Linear default init U(+-1/sqrt(fan_in)) for W and b,
-  b3 += 0.5, rounded to f16 (R11).
+  b3 += 0.5, rounded to f16 (R11); mlp="stress" scales the layers (see
+  MLP_SCALES) so the hidden pre-activations reach |z| ~ 10 and the outputs
+  leave [0, 1] on both sides.
 """
 from __future__ import annotations
 
@@ -287,21 +289,29 @@ def _dense_map(seed, stream, tiles, rx, ry, nch, nslices, fmt):
     return out
 
 
-def _mlp(seed, tiles, h):
+# "stress" MLP (GPU parity outside the seeded regime): W1, b1 x 6, W2, b2 x 2.5,
+# W3, b3 x 0.4 and b3 shifted by 0.5 + 0.4 U(-1, 1) per tile and channel, so
+# that hidden pre-activations reach |z| ~ 9-11 and ~10 % of the outputs fall
+# below 0 and ~12 % above 1 (the RGBA8 clamp of R12 on both sides)
+MLP_SCALES = {"default": (1.0, 1.0, 1.0, 0.0), "stress": (6.0, 2.5, 0.4, 0.4)}
+
+
+def _mlp(seed, tiles, h, kind="default"):
     keys = _tile_keys(seed, 5, tiles)
     n = 16 * h + h + h * h + h + 3 * h + 3
-    u = _unif(_hash(keys, n)) * 2.0 - 1.0                   # U(-1, 1)
-    sizes = [(16 * h, 16), (h, 16), (h * h, h), (h, h), (3 * h, h), (3, h)]  # (count, fan_in)
+    u = _unif(_hash(keys, n + 3)) * 2.0 - 1.0               # U(-1, 1)
+    s1, s2, s3, sb = MLP_SCALES[kind]
+    sizes = [(16 * h, 16, s1), (h, 16, s1), (h * h, h, s2), (h, h, s2), (3 * h, h, s3), (3, h, s3)]  # (count, fan_in, scale)
     parts, o = [], 0
-    for cnt, fan in sizes:
-        parts.append(u[:, o:o + cnt] / np.sqrt(fan))
+    for cnt, fan, sc in sizes:
+        parts.append(u[:, o:o + cnt] / np.sqrt(fan) * sc)
         o += cnt
     w = np.concatenate(parts, axis=1)
-    w[:, -3:] += 0.5
+    w[:, -3:] += 0.5 + sb * u[:, n:n + 3]
     return w.astype(np.float16).view(np.uint16)
 
 
-def make_theta(lay: dict, seed: int, payload: str = "smooth", tiles=None) -> dict:
+def make_theta(lay: dict, seed: int, payload: str = "smooth", tiles=None, mlp: str = "default") -> dict:
     """Theta arrays for tile ids `tiles` (default all) in the layout's formats.
 
     Returns numpy arrays: uv, uvt, ut, vt (uint8 or float16) and mlp (uint16
@@ -329,7 +339,7 @@ def make_theta(lay: dict, seed: int, payload: str = "smooth", tiles=None) -> dic
     else:
         th["ut"] = _dense_map(seed, 3, tiles, U, T, 2, 1, lay["fmt_line"]).reshape(len(tiles), T, U, 2)
         th["vt"] = _dense_map(seed, 4, tiles, U, T, 2, 1, lay["fmt_line"]).reshape(len(tiles), T, U, 2)
-    th["mlp"] = _mlp(seed, tiles, lay["hidden"])
+    th["mlp"] = _mlp(seed, tiles, lay["hidden"], mlp)
     return th
 
 

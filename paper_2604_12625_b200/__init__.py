@@ -67,10 +67,11 @@ _SIGS = {
     "ndgi_validate_layout": (_I, [C.POINTER(ndgi_layout), C.POINTER(_I)]),
     "ndgi_debug_bc7_decode": (_I, [_P, _U32, _U32, _P, _P]),
     "ndgi_debug_bc7_decode_hw": (_I, [_P, _U32, _U32, _P]),
-    "ndgi_debug_gelu_rate": (_I, [_U32, C.POINTER(_F), C.POINTER(C.c_double)]),
+    "ndgi_debug_gelu_rate": (_I, [_U32, _U32, _I, C.POINTER(_F), C.POINTER(C.c_double)]),
+    "ndgi_debug_gelu_split": (_I, [_U32, C.POINTER(_U32), C.POINTER(_I)]),
     "ndgi_debug_mma_latency": (_I, [_U32, C.POINTER(C.c_double)]),
+    "ndgi_debug_null_launch": (_I, [_P]),
     "ndgi_debug_tmem_f16_probe": (_I, [_P]),
-    "ndgi_debug_fused_profile": (_I, [_P, _I]),
     "ndgi_vt_create": (_I, [_U32, _U32, _U32, C.POINTER(C.c_void_p)]),
     "ndgi_vt_free": (_I, [_P]),
     "ndgi_vt_request": (_I, [_P, _P, _U32, _F, _P, _P, C.POINTER(_U32), C.POINTER(_F), C.POINTER(C.c_int32)]),
@@ -237,11 +238,26 @@ def ndgi_debug_bc7_decode_hw(blocks, w: int, h: int, rgba) -> None:
            "ndgi_debug_bc7_decode_hw")
 
 
-def ndgi_debug_gelu_rate(iters: int = 4096) -> tuple[float, float]:
-    """-> (milliseconds, activations) of the f16x2 GELU microbenchmark."""
+def ndgi_debug_gelu_rate(iters: int = 4096, mufu_pairs: int = 16, pack_f32: bool = False) -> tuple[float, float]:
+    """-> (milliseconds, activations) of the GELU microbenchmark: `mufu_pairs`
+    of every 16 f16x2 pairs through MUFU, the rest on the FMA pipe; pack_f32
+    adds the fp32 -> f16x2 packing of the fp32-accumulator epilogue."""
     ms, acts = C.c_float(0), C.c_double(0)
-    _check(_lib.ndgi_debug_gelu_rate(iters, C.byref(ms), C.byref(acts)), "ndgi_debug_gelu_rate")
+    _check(_lib.ndgi_debug_gelu_rate(iters, mufu_pairs, int(pack_f32), C.byref(ms), C.byref(acts)),
+           "ndgi_debug_gelu_rate")
     return float(ms.value), float(acts.value)
+
+
+def ndgi_debug_gelu_split(hidden: int) -> tuple[int, bool]:
+    """-> (MUFU pairs of every 16, fp32 accumulators?) compiled into the fused kernel."""
+    m, f = C.c_uint32(0), C.c_int(0)
+    _check(_lib.ndgi_debug_gelu_split(hidden, C.byref(m), C.byref(f)), "ndgi_debug_gelu_split")
+    return int(m.value), bool(f.value)
+
+
+def ndgi_debug_null_launch(stream=None) -> None:
+    """An empty kernel through the C ABI (the VT launch-latency floor)."""
+    _check(_lib.ndgi_debug_null_launch(_stream_ptr(stream)), "ndgi_debug_null_launch")
 
 
 def ndgi_debug_mma_latency(iters: int = 1000) -> float:

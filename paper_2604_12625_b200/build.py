@@ -48,8 +48,18 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None, de
     os.makedirs(objdir, exist_ok=True)
     extra = (["-Xptxas", "-v"] if verbose else []) + [f"-D{d}" for d in defines]
 
+    hdr_t = max(os.path.getmtime(d) for d in _deps() if not d.endswith(".cu"))
+    stamp = os.path.join(objdir, "flags.txt")
+    flags_key = " ".join(FLAGS + extra)
+    same_flags = os.path.exists(stamp) and open(stamp).read() == flags_key
+
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        # incremental: an object newer than its source and every header, built
+        # with the same flags, is reused
+        if (same_flags and os.path.exists(obj) and
+                os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t)):
+            return obj
         cmd = [NVCC, *FLAGS, *extra, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -60,6 +70,12 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None, de
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
+    with open(stamp, "w") as f:
+        f.write(flags_key)
+    # objects of deleted sources must not be linked
+    for o in glob.glob(os.path.join(objdir, "*.o")):
+        if o not in objs:
+            os.remove(o)
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC", *objs, "-o", lib]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -234,23 +234,40 @@ __device__ __forceinline__ void bc7_decode_generic(uint4 raw, Sink&& sink) {
 // Mode-6 decoder (valid only when (byte0 & 0x7f) == 0x40).
 // Layout: mode(7) R0 R1 G0 G1 B0 B1 A0 A1 (7 each) P0 P1 idx0(3) idx1..15(4)
 // ---------------------------------------------------------------------------
+//
+// Per texel the interpolation ((64 - w) e0 + w e1 + 32) >> 6 runs on two
+// channels at once in 16-bit lanes, rewritten as w (e1 - e0) + (64 e0 + 32):
+// with D = rb1 - rb0 taken as a plain 32-bit difference of the packed words
+// (R + 2^16 B), w D + E = L + 2^16 H exactly, where L and H are the two lanes'
+// non-negative sums (< 2^14), so the lanes separate without borrows -- one
+// IMAD per channel pair.  The 4-bit weights round(64 i / 15) are
+// 4 i + ((i + 2) >> 2) (exact for i = 0..15), evaluated for four texels at
+// once on bytes.
 template <class Sink>
 __device__ __forceinline__ void bc7_decode_mode6(uint4 raw, Sink&& sink) {
     const uint64_t lo = (uint64_t)raw.x | ((uint64_t)raw.y << 32);
-    const uint64_t hi = (uint64_t)raw.z | ((uint64_t)raw.w << 32);
-    const uint32_t p0 = (uint32_t)(lo >> 63), p1 = (uint32_t)hi & 1u;
+    const uint32_t p0 = raw.y >> 31, p1 = raw.z & 1u;
     auto f = [&](int k) { return (uint32_t)(lo >> (7 + 7 * k)) & 0x7fu; };
     const uint32_t rb0 = ((f(0) << 1) | p0) | (((f(4) << 1) | p0) << 16);
     const uint32_t rb1 = ((f(1) << 1) | p1) | (((f(5) << 1) | p1) << 16);
     const uint32_t ga0 = ((f(2) << 1) | p0) | (((f(6) << 1) | p0) << 16);
     const uint32_t ga1 = ((f(3) << 1) | p1) | (((f(7) << 1) | p1) << 16);
-    WTab wt;
-    wt.set(4u);
+    const uint32_t drb = rb1 - rb0, dga = ga1 - ga0;
+    const uint32_t erb = (rb0 << 6) + 0x00200020u, ega = (ga0 << 6) + 0x00200020u;
+    // texel i's index: bits 64 + 4i (i >= 1); texel 0: 3 bits at 65 (anchor)
+    const uint32_t iw0 = (raw.z & ~0xfu) | ((raw.z >> 1) & 7u), iw1 = raw.w;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const uint32_t idx = i == 0 ? (uint32_t)(hi >> 1) & 7u : (uint32_t)(hi >> (4 * i)) & 15u;
-        const uint32_t w = wt.w(idx);
-        sink(i, lerp2(rb0, rb1, w) | (lerp2(ga0, ga1, w) << 8));
+    for (int g = 0; g < 4; ++g) {
+        // indices of texels 4g .. 4g+3 -> bytes, then their weights
+        const uint32_t nib = (g < 2 ? iw0 : iw1) >> (16 * (g & 1));
+        const uint32_t ib = __byte_perm(nib & 0x0f0fu, (nib >> 4) & 0x0f0fu, 0x5140u);
+        const uint32_t wb = (ib << 2) + (((ib + 0x02020202u) >> 2) & 0x3f3f3f3fu);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t w = (wb >> (8 * k)) & 0xffu;
+            const uint32_t vrb = w * drb + erb, vga = w * dga + ega;
+            sink(4 * g + k, ((vrb >> 6) & 0x00ff00ffu) | ((vga << 2) & 0xff00ff00u));
+        }
     }
 }
 

@@ -1,9 +1,12 @@
 // debug.cu -- test hooks of libndgi.so (not the product path):
 //  * BC7 map decode with the fused kernel's device decoder (bit-exact check);
 //  * the same map through the B200 texture unit (independent hardware decoder);
-//  * a GELU-rate microbenchmark of the fused kernel's f16x2 GELU, which is the
+//  * a GELU-rate microbenchmark of the fused kernel's f16x2 GELU epilogue in
+//    any MUFU / FMA-pipe split, whose rate at the kernel's own split is the
 //    measured denominator of the ALU roofline (T_alu).
 #include <cuda_runtime.h>
+
+#include <utility>
 
 #include "bc7_device.cuh"
 #include "ndgi_common.cuh"
@@ -68,44 +71,79 @@ cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* r
     return e;
 }
 
-// 8 independent f16x2 GELU chains per thread
-__global__ void __launch_bounds__(256) gelu_rate_kernel(uint32_t iters, uint32_t* sink) {
-    uint32_t v[8];
+// GELU-rate microbenchmark (the T_alu denominator): 16
+// independent chains of f16x2 GELU pairs per thread, the first M of every 16
+// pairs through MUFU (gelu_scaled_f16x2), the other 16 - M on the FMA pipe
+// (gelu_poly_f16x2) -- the fused kernel's own epilogue functions and split.
+// PACK: each pair is first packed from two fp32 values (cvt.rn.f16x2.f32), as
+// the fp32-accumulator epilogue does; the chain runs through the previous
+// result's bits reinterpreted as fp32 (no extra instruction).
+template <int M, bool PACK>
+__global__ void __launch_bounds__(256) gelu_mix_kernel(uint32_t iters, uint32_t* sink) {
+    uint32_t v[16];
+    float hi[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = pack_f16x2(0.25f + 0.01f * (threadIdx.x & 7) + 0.1f * q, -0.5f - 0.02f * q);
+    for (int q = 0; q < 16; ++q) {
+        v[q] = pack_f16x2(0.25f + 0.01f * (threadIdx.x & 7) + 0.1f * q, -0.5f - 0.02f * q);
+        hi[q] = -1.5f + 0.2f * q;
+    }
     for (uint32_t it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = gelu_scaled_f16x2(v[q]);
+        for (int q = 0; q < 16; ++q) {
+            const uint32_t h = PACK ? pack_f16x2(__uint_as_float(v[q]), hi[q]) : v[q];
+            v[q] = q < M ? gelu_scaled_f16x2(h) : gelu_poly_f16x2(h);
+        }
     }
     uint32_t acc = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc ^= v[q];
+    for (int q = 0; q < 16; ++q) acc ^= v[q];
     if (acc == 0x12345678u) sink[0] = acc;  // keep the chains alive
 }
 
-cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts) {
+template <int M>
+static void launch_gelu_mix(bool pack, int grid, uint32_t iters, uint32_t* sink) {
+    if (pack) gelu_mix_kernel<M, true><<<grid, 256>>>(iters, sink);
+    else gelu_mix_kernel<M, false><<<grid, 256>>>(iters, sink);
+}
+
+template <int... Ms>
+static void dispatch_gelu_mix(int m, bool pack, int grid, uint32_t iters, uint32_t* sink,
+                              std::integer_sequence<int, Ms...>) {
+    ((m == Ms ? launch_gelu_mix<Ms>(pack, grid, iters, sink) : void()), ...);
+}
+
+cudaError_t gelu_rate(uint32_t iters, uint32_t mufu_pairs, int pack, float* ms, double* acts) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint32_t* sink = nullptr;
     cudaError_t e = cudaMalloc(&sink, 4);
     if (e != cudaSuccess) return e;
-    const int grid = sms * 8;
-    gelu_rate_kernel<<<grid, 256>>>(16, sink);  // warm-up
+    const int grid = sms * 8;   // 2048 threads per SM
+    const auto seq = std::make_integer_sequence<int, 17>{};
+    dispatch_gelu_mix((int)mufu_pairs, pack != 0, grid, 16, sink, seq);   // warm-up
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    gelu_rate_kernel<<<grid, 256>>>(iters, sink);
+    dispatch_gelu_mix((int)mufu_pairs, pack != 0, grid, iters, sink, seq);
     cudaEventRecord(b);
     e = cudaEventSynchronize(b);
     if (e == cudaSuccess) e = cudaGetLastError();
     cudaEventElapsedTime(ms, a, b);
-    *acts = (double)grid * 256.0 * 8.0 * 2.0 * (double)iters;
+    *acts = (double)grid * 256.0 * 16.0 * 2.0 * (double)iters;
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(sink);
     return e;
+}
+
+// the VT latency floor: an empty kernel launched through the same C-ABI path
+__global__ void null_kernel() {}
+
+cudaError_t null_launch(cudaStream_t s) {
+    null_kernel<<<1, 32, 0, s>>>();
+    return cudaGetLastError();
 }
 
 }  // namespace ndgi

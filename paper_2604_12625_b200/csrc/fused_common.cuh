@@ -1,5 +1,5 @@
-// fused_common.cuh -- pieces shared by the two fused tile-decode kernels
-// (fused_kernel.cu: CTA-synchronous, fused_ws_kernel.cu: warp-specialised):
+// fused_common.cuh -- pieces of the fused tile-decode kernel (fused_kernel.cu)
+// and the reference/training kernels that share the prologue:
 // TMEM/smem layouts, the GELU epilogue, the per-unit parameter prologue.
 #pragma once
 #include <cuda_runtime.h>
@@ -28,11 +28,19 @@ constexpr int kChunkTexels = 2048;             // F_uv texels decoded per chunk 
 template <int H>
 struct FusedCfg {
     static constexpr int K2 = H + 16;                    // layer 2/3 K incl. bias chunk
-    // per slot: A23 = layer-2/3 A operand (K2/2 columns); layer 1's A (K = 16,
-    // 8 columns) aliases its first 8 columns -- dead once layer 1 completes,
-    // and the bias chunk (columns H/2 .. H/2+7) is never overwritten.
-    static constexpr uint32_t TM_A1 = 0;
+    // TMEM columns of one slot (32-bit columns, two f16 per column for A):
+    //   [0, H/2)          GELU outputs = A of layers 2 and 3 (K = 0 .. H-1)
+    //   [H/2, H/2 + 8)    the "feature chunk", K = H .. H+15 of layers 2/3 and
+    //                     the whole A of layer 1 (K = 16), in the order
+    //                     [1, 0 | V_ut | V_vt | 0, 0 | V_uvt (2 cols) | F_uv (2 cols)]
+    //                     -- B2/B3 are zero past K = H (the bias row), so the
+    //                     features ride along in layers 2/3 at no cost, and the
+    //                     constant columns are written once per work unit
+    //   [TM_D, TM_D + H)  fp32 accumulators
     static constexpr uint32_t TM_A23 = 0;
+    static constexpr uint32_t TM_A1 = H / 2;
+    static constexpr uint32_t TM_UVT = TM_A1 + 4;        // V_uvt, F_uv: per item
+    static constexpr uint32_t TM_VT = TM_A1 + 2;         // V_vt: per row
     static constexpr uint32_t TM_D = H == 16 ? 16 : 64;  // H columns (fp32 accumulators)
     static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
     static constexpr int SLOTS = H == 16 ? NDGI_SLOTS16 : 1;   // 128-texel items per MMA step (one TMEM slot each)
@@ -42,9 +50,16 @@ struct FusedCfg {
     static constexpr int B1_BYTES = H * 16 * 2;
     static constexpr int B2_BYTES = H * K2 * 2;
     static constexpr int B3_BYTES = 16 * K2 * 2;
-    static_assert(TM_A23 + K2 / 2 <= TM_D, "TMEM layout");
+    static_assert(TM_A1 + 8 <= TM_D, "TMEM layout");
     static_assert(TM_D + H <= SLOT_COLS, "TMEM layout");
 };
+
+// layer-1 K position of Eq. 4 input j (R6: x = [V_uvt 0..3 | V_uv 4..7 | V_ut
+// 8..9 | V_vt 10..11 | gamma 12..15]) in the TMEM feature chunk above; the
+// bias (with gamma(t) folded) sits at K = 0, K = 1, 6, 7 hold zeros
+__host__ __device__ constexpr int a1_k_of_input(int j) {
+    return j < 4 ? 8 + j : (j < 8 ? 12 + (j - 4) : (j < 10 ? 2 + (j - 8) : 4 + (j - 10)));
+}
 
 // element (n, k) of a K-major no-swizzle operand with Kt columns:
 // [n/8][k/8][n%8][k%8] halves -> LBO = 128 B, SBO = Kt/8 * 128 B
@@ -129,11 +144,12 @@ __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) 
 }
 
 // h = 16, S items: all accumulators loaded before one wait, 8*S independent
-// GELU pairs in flight
+// GELU pairs in flight.  Layers 1-2 accumulate in fp32 (north_star: "fp16 in,
+// fp32 accumulate"); NDGI_F16ACC=1 is an opt-in build with f16 accumulators
+// read back packed (tcgen05.ld .pack::16b), kept only as a measured variant.
 #ifndef NDGI_F16ACC
-#define NDGI_F16ACC 1
+#define NDGI_F16ACC 0
 #endif
-
 
 // h = 16, S items with f16 accumulators (layers 1, 2): tcgen05.ld .pack::16b
 // delivers the 16 pre-activations as 8 f16x2 words -- no fp32 -> f16 packing
@@ -154,6 +170,8 @@ __device__ __forceinline__ void gelu_epilogue_h16_f16acc(uint32_t d0, uint32_t a
     }
 }
 
+// h = 16, S items with fp32 accumulators: one cvt.rn.f16x2.f32 per pair, then
+// the same GELU split as above
 template <int S>
 __device__ __forceinline__ void gelu_epilogue_h16(uint32_t d0, uint32_t a0, uint32_t stride) {
     uint32_t x[S][16];
@@ -164,8 +182,11 @@ __device__ __forceinline__ void gelu_epilogue_h16(uint32_t d0, uint32_t a0, uint
     for (int s = 0; s < S; ++s) {
         uint32_t g[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(x[s][2 * q]), __uint_as_float(x[s][2 * q + 1])));
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t h = pack_f16x2(__uint_as_float(x[s][2 * q]), __uint_as_float(x[s][2 * q + 1]));
+            g[q] = q < 8 - (s == 0 ? NDGI_POLY_PAIRS_ITEM0 : NDGI_POLY_PAIRS) ? gelu_scaled_f16x2(h)
+                                                                            : gelu_poly_f16x2(h);
+        }
         ptx::tmem_st_x8(a0 + s * stride, g);
     }
 }
@@ -232,10 +253,9 @@ __global__ void prep_weights_kernel(const uint16_t* __restrict__ mlp, size_t til
         __half* B3 = reinterpret_cast<__half*>(o + Cfg::B1_BYTES + Cfg::B2_BYTES);
         float* G = reinterpret_cast<float*>(o + WPack<H>::B_BYTES);
         for (int e = threadIdx.x; e < H * 16; e += blockDim.x) {
-            const int n = e >> 4, kk = e & 15;
-            float v = 0.f;
-            if (kk < 12) v = half_bits_to_float(W1[n * 16 + kk]) * ((kk >= 4 && kk < 8) ? s_uv : a);
-            B1[bofs(n, kk, 16)] = __float2half_rn(v);
+            const int n = e >> 4, j = e & 15;   // Eq. 4 input j; gamma (j >= 12) and b1 go to K = 0 per call
+            if (j < 12) B1[bofs(n, a1_k_of_input(j), 16)] = __float2half_rn(half_bits_to_float(W1[n * 16 + j]) * ((j >= 4 && j < 8) ? s_uv : a));
+            else B1[bofs(n, j == 12 ? 0 : (j == 13 ? 1 : j - 8), 16)] = __float2half_rn(0.f);   // K = 0, 1, 6, 7
         }
         for (int e = threadIdx.x; e < H * Cfg::K2; e += blockDim.x) {
             const int n = e / Cfg::K2, kk = e % Cfg::K2;
@@ -261,7 +281,7 @@ __global__ void prep_weights_kernel(const uint16_t* __restrict__ mlp, size_t til
 }
 
 // the prepacked B operands of tile k -> smem (L.b1, L.b2, L.b3 are contiguous),
-// patching layer-1's bias column with a (b1 + W1_gamma gamma(t)) (R6) on the way
+// patching layer-1's bias column (K = 0) with a (b1 + W1_gamma gamma(t)) (R6) on the way
 template <int H>
 __device__ __forceinline__ void copy_prepacked_weights(const KParams& p, const TConst& tc, int k, uint8_t* smem,
                                                        const FusedSmem& L, int tid, int nthr) {
@@ -272,78 +292,36 @@ __device__ __forceinline__ void copy_prepacked_weights(const KParams& p, const T
     uint4* dst = reinterpret_cast<uint4*>(smem + L.b1);
     for (int c = tid; c < (int)(WPack<H>::B_BYTES / 16); c += nthr) {
         uint4 v = __ldg(src + c);
-        if (c < Cfg::B1_BYTES / 16 && ((c >> 3) & 1)) {
-            // this chunk is k = 8..15 of B1 row n: element k = 12 is v.z's low half
+        if (c < Cfg::B1_BYTES / 16 && !((c >> 3) & 1)) {
+            // this chunk is k = 0..7 of B1 row n: element k = 0 is v.x's low half
             const int n = (c >> 4) * 8 + (c & 7);
             float acc = __ldg(G + n * 5);
 #pragma unroll
             for (int g = 0; g < 4; ++g) acc = fmaf(__ldg(G + n * 5 + 1 + g), tc.gamma[g], acc);
             const uint32_t hb = (uint32_t)__half_as_ushort(__float2half_rn(kGeluA * acc));
-            v.z = (v.z & 0xffff0000u) | hb;
+            v.x = (v.x & 0xffff0000u) | hb;
         }
         dst[c] = v;
     }
 }
 
-// a2 (+a5): one unit's parameters -> shared memory: the tile's MLP as tcgen05
-// B operands (with the folds of DESIGN.md §6.1), the tau-blended F_uvt slice,
-// V_ut per column and the per-row gather table (F_uvt y taps, V_vt).
+// a2: one unit's feature parameters -> shared memory: the tau-blended F_uvt
+// slice, V_ut per column and the per-row gather table (F_uvt y taps, V_vt)
+// (the MLP's B operands come prepacked: copy_prepacked_weights).
 // Executed by threads tid = 0 .. nthr-1 of the CTA.
 // win_pitch == 0: the whole tau-blended F_uvt slice goes to smem (row offsets
 // y * R3 * 8); > 0: the kernel stages per-warp ring windows of win_rows (a
 // power of two) F_uvt rows itself and the row table holds ring-row offsets
-template <int H, int FMT_UV, int C, bool TC_WEIGHTS = true>
+template <int H, int FMT_UV, int C>
 __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc, int k, uint8_t* smem,
                                               const FusedSmem& L, int tid, int nthr, uint32_t win_pitch = 0,
                                               int win_rows = 0) {
-    using Cfg = FusedCfg<H>;
     const int R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);
-    __half* sB1 = reinterpret_cast<__half*>(smem + L.b1);
-    __half* sB2 = reinterpret_cast<__half*>(smem + L.b2);
-    __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
     uint2* sUvt = reinterpret_cast<uint2*>(smem + L.uvt);
     uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
     uint4* sRow = reinterpret_cast<uint4*>(smem + L.rowtab);
         {
-            const uint16_t* w = p.mlp + p.mlp_tile_elems * k;
-            const uint16_t *W1 = w, *b1 = W1 + 16 * H, *W2 = b1 + H, *b2 = W2 + H * H, *W3 = b2 + H, *b3 = W3 + 3 * H;
-            const float a = kGeluA;
-            const float s_uv = FMT_UV == FMT_F16 ? a : a / 255.0f;   // F_uv enters in q units (R8)
-            if constexpr (TC_WEIGHTS) {
-            // layer 1: [H][16]: k 0..11 = Eq. 4 features, 12 = bias (gamma(t) folded), 13..15 = 0
-            for (int e = tid; e < H * 16; e += nthr) {
-                const int n = e >> 4, kk = e & 15;
-                float v = 0.f;
-                if (kk < 12) {
-                    const float wv = half_bits_to_float(__ldg(W1 + n * 16 + kk));
-                    v = wv * ((kk >= 4 && kk < 8) ? s_uv : a);
-                } else if (kk == 12) {
-                    float acc = half_bits_to_float(__ldg(b1 + n));
-                    for (int g = 0; g < 4; ++g) acc = fmaf(half_bits_to_float(__ldg(W1 + n * 16 + 12 + g)), tc.gamma[g], acc);
-                    v = a * acc;
-                }
-                sB1[bofs(n, kk, 16)] = __float2half_rn(v);
-            }
-            // layer 2: [H][H+16]: 0.5*W2 (absorbs 1/(2a) of GELU~ and a of the next pre-scale), bias a*b2
-            for (int e = tid; e < H * Cfg::K2; e += nthr) {
-                const int n = e / Cfg::K2, kk = e % Cfg::K2;
-                float v = 0.f;
-                if (kk < H) v = 0.5f * half_bits_to_float(__ldg(W2 + n * H + kk));
-                else if (kk == H) v = a * half_bits_to_float(__ldg(b2 + n));
-                sB2[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
-            }
-            // layer 3: [16][H+16]: rows 0..2 = W3/(2a), bias b3 (exact); rows 3..15 = 0
-            for (int e = tid; e < 16 * Cfg::K2; e += nthr) {
-                const int n = e / Cfg::K2, kk = e % Cfg::K2;
-                float v = 0.f;
-                if (n < 3) {
-                    if (kk < H) v = half_bits_to_float(__ldg(W3 + n * H + kk)) * (0.5f / a);
-                    else if (kk == H) v = half_bits_to_float(__ldg(b3 + n));
-                }
-                sB3[bofs(n, kk, Cfg::K2)] = __float2half_rn(v);
-            }
-            }
             // F_uvt slices k0, k1 blended with tau (R4, R17) -> f16x4 [R3][R3], values in [0,1]
             const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
             const float tau = tc.tau, omt = 1.0f - tau;

@@ -1,0 +1,8 @@
+// fused_h16_c128_dense.cu -- instantiations of the fused tile-decode kernel (fused_kernel.cuh),
+// one translation unit per group so the build compiles them in parallel
+#include "fused_kernel.cuh"
+
+namespace ndgi {
+template cudaError_t launch_fused_t<16, FMT_U8, 128>(const KParams& p, int num_sms, cudaStream_t s);
+template cudaError_t launch_fused_t<16, FMT_F16, 128>(const KParams& p, int num_sms, cudaStream_t s);
+}  // namespace ndgi

@@ -1,695 +1,25 @@
-// fused_kernel.cu -- NDGI_MODE_FAST: the fused tile-decode kernel for sm_100a.
-//
-// One persistent kernel does the whole hot path of SURVEY.md §8(a):
-//   a1  work units (query time, request, strip of core rows); call constants
-//       gamma(t), k0/k1/tau, r0/r1/rho come precomputed from the host
-//   a2  per unit: the tile's f16 MLP -> smem B operands, the two BC7 t-slices
-//       of F_uvt, the line maps at t; per 16-row chunk the BC7 F_uv blocks
-//   a3  BC7 decode (bc7_device.cuh), one block per lane, each warp decoding
-//       exactly the blocks its own texels need (no CTA barrier)
-//   a4  V_uvt: tau-blended slice (f16, smem) sampled bilinearly (f16x2 math);
-//       V_uv: the texel itself (R2); V_ut per column / V_vt per row (f16x2)
-//   a5  gamma(t): folded into layer-1's bias column (R6)
-//   a6  the 16-wide Eq. 4 input row of each texel -> TMEM (tcgen05.st)
-//   a7  G_Phi on the 5th-gen tensor cores: per 128-texel block three
-//       tcgen05.mma (kind::f16, M=128) with A in TMEM, B (weights) in smem,
-//       fp32 accumulators in TMEM; biases ride in an extra K chunk (A column
-//       of ones); GELU in the epilogue on packed f16x2 (tanh.approx), its
-//       constants folded into the next layer's weights
-//   a8  RGBA8 (or 16F/32F) page-cache writer: core + mirrored border (R3)
-//
-// CTA = 4 warps; thread t owns TMEM lane t, i.e. texel t of each 128-texel
-// item.  A step carries S items (S TMEM slots: 2 for h = 16, 1 for h = 64)
-// through the three layers together: per layer one CTA barrier, S (x K/16)
-// tcgen05.mma issued by one elected lane, one tcgen05.commit -> mbarrier.
-// Several CTAs per SM (6 for h = 16) hide each other's MMA latency.
+// fused_kernel.cu -- host side of the fused tile-decode kernel: the load-time
+// weight prepack and the dispatch to the per-(h, C) instantiations
+// (fused_h16_c128.cu, fused_h16_c256.cu, fused_h64.cu).
 #include <cuda_runtime.h>
-
-#include <cstdio>
-#include <cstdlib>
-#include <mutex>
-#include <type_traits>
-#include <vector>
 
 #include "fused_common.cuh"
 
 namespace ndgi {
 
-constexpr int kThreads = 128;
-
-#ifndef NDGI_PROFILE
-#define NDGI_PROFILE 0
-#endif
-#if NDGI_PROFILE
-// cycle accounting per warp (lane 0): [0] barrier, [1] mbarrier wait, [2] epilogue,
-// [3] gather, [4] output, [5] unit prologue, [6] total, [7] steps
-__device__ unsigned long long g_ndgi_prof[12];
-__device__ int g_ndgi_res[256];   // resident CTAs per SM (profiling builds only)
-#define PROF_T0() (_pt = clock64())
-#define PROF_ADD(k) do { long long _n = clock64(); if (lane == 0) prof[k] += _n - _pt; _pt = _n; } while (0)
-#else
-#define PROF_T0() do {} while (0)
-#define PROF_ADD(k) do {} while (0)
-#endif
-#ifndef NDGI_ONEWAIT
-#define NDGI_ONEWAIT 0
-#endif
-#ifndef NDGI_WAIT_GUARD
-#define NDGI_WAIT_GUARD 0   // 1: bounded mbarrier polls (trap after 2^28), for debugging
-#endif
-#ifndef NDGI_JOINT_EPI
-#define NDGI_JOINT_EPI 1
-#endif
-
-// FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
-// no format switch, row pointers instead of 64-bit index arithmetic
-// WIN: F_uvt staged per chunk in per-warp windows instead of the whole slice
-// (large R3: the H profile's 32 KB slice would halve residency)
-// OUTK: 0 any format / addressing, 1 (FULL8) decode_full RGBA8, 2 (TILES8)
-// decode_tiles RGBA8 (core + mirrored border with 32-bit offsets from the slot)
-template <int H, int FMT_UV, int CT, int OUTK, bool WIN>
-__global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_kernel(const __grid_constant__ KParams p) {
-    constexpr bool FULL8 = OUTK == 1, TILES8 = OUTK == 2;
-    using Cfg = FusedCfg<H>;
-    constexpr int S = Cfg::SLOTS;
-    constexpr int C = CT;                       // core texels per tile side (128 or 256)
-    constexpr int BPR = CT / kThreads;          // 128-texel MMA blocks per row
-    constexpr int chunk_rows = kChunkTexels / CT;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const FusedSmem L = fused_smem_layout<H>(C, p.R3);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t bars = ptx::smem_addr(smem + L.bars);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
-    __half* sB1 = reinterpret_cast<__half*>(smem + L.b1);
-    __half* sB2 = reinterpret_cast<__half*>(smem + L.b2);
-    __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
-    uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
-    uint4* sRow = reinterpret_cast<uint4*>(smem + L.rowtab);
-
-    // ---- one-time setup: counters, mbarriers, TMEM allocation -------------------
-    if (tid < 8) reinterpret_cast<uint32_t*>(smem + L.cnt)[tid] = 0u;
-    if (tid == 0) {
-        ptx::mbar_init(bars, 1);
-        ptx::fence_mbar_init();
-    }
-    if (warp == 0) ptx::tmem_alloc<Cfg::TM_COLS>(ptx::smem_addr(tmem_slot));
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    const int B = p.B, P = p.P, R3 = p.R3;
-    const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
-    static_assert(!WIN || CT == 128, "windowed F_uvt is built for C = 128");
-    const UvtWindow win = uvt_window(R3, C, chunk_rows);
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
-    const uint32_t tm_lane = tmem + lane_base;
-
-    {   // constant part of the layer-2/3 A operand of every slot: bias chunk [1, 0, ..., 0]
-        uint32_t c[8] = {0x00003C00u, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int s = 0; s < S; ++s) ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23 + H / 2, c);
-        ptx::tmem_wait_st();
-    }
-
-    uint32_t dph = 0u;   // d_ready phase
-#if NDGI_PROFILE
-    unsigned long long prof[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    if (tid == 0) {
-        const int now = atomicAdd(&g_ndgi_res[smid & 255], 1) + 1;
-        atomicMax(reinterpret_cast<unsigned long long*>(&g_ndgi_prof[10]), (unsigned long long)now);
-        atomicAdd(&g_ndgi_prof[11], (unsigned long long)now);
-    }
-    const long long prof_start = clock64();
-    long long _pt = prof_start;
-#endif
-
-    for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
-        const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
-        const uint32_t rq = unit / (uint32_t)p.strips_per_tile;
-        const int ti = (int)(rq / p.n_req);
-        const uint32_t r = rq % p.n_req;
-        const TConst& tc = p.tc[ti];
-        int k;
-        size_t out_base;   // texel index of core texel (0,0)
-        size_t row_pitch;  // texels between rows
-        if (p.full) {
-            k = (int)r;
-            const int tx = k % p.tiles_x, ty = (k / p.tiles_x) % p.tiles_y, a = k / (p.tiles_x * p.tiles_y);
-            row_pitch = (size_t)p.tiles_x * C;
-            out_base = (size_t)ti * p.out_t_stride + (size_t)a * p.tiles_y * C * row_pitch +
-                       (size_t)ty * C * row_pitch + (size_t)tx * C;
-        } else {
-            const uint32_t id = __ldg(p.tile_ids + r);
-            const uint32_t slot = p.slots ? __ldg(p.slots + r) : r;
-            if (id >= (uint32_t)p.num_tiles || slot >= p.num_slots) {
-                if (strip == 0 && tid == 0) atomicAdd(p.err, 1u);
-                continue;  // uniform across the CTA
-            }
-            k = (int)id;
-            row_pitch = (size_t)P;
-            out_base = ((size_t)slot * P + B) * P + B;
-        }
-        const int nitems = p.strip_rows * BPR;     // 128-texel blocks of this unit (multiple of S)
-        const int j_begin = strip * p.strip_rows;
-
-        // ---- a2: tile parameters -> shared memory -----------------------------------
-        __syncthreads();  // previous unit's MMAs complete and all smem readers done
-        {
-            PROF_T0();
-            copy_prepacked_weights<H>(p, tc, k, smem, L, tid, kThreads);
-            unit_prologue<H, FMT_UV, C, false>(p, tc, k, smem, L, tid, kThreads, WIN ? win.pitch : 0u, win.wyb * 4);
-            PROF_ADD(5);
-        }
-        ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
-        __syncthreads();
-
-        // per-column gather constants (column i = b*128 + tid, written and read by
-        // the same thread): byte offsets of the two F_uvt x taps from the smem
-        // base, the x weight, V_ut
-        uint4* sCol = reinterpret_cast<uint4*>(smem + L.colc);
-#pragma unroll
-        for (int b = 0; b < BPR; ++b) {
-            const int i = b * kThreads + tid;
-            const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
-            const float flx = floorf(sx);
-            const int x0 = clampi((int)flx, 0, R3 - 1), x1 = clampi((int)flx + 1, 0, R3 - 1);
-            if constexpr (WIN) {
-                // this warp's window starts at the block column of its lane 0
-                const int wx0 = __shfl_sync(0xffffffffu, x0, 0) & ~3;
-                const uint32_t wb = L.uvt + (uint32_t)warp * win.bytes;
-                sCol[i] = make_uint4(wb + (uint32_t)(x0 - wx0) * 8u, wb + (uint32_t)(x1 - wx0) * 8u,
-                                     pack_f16x2(sx - flx, sx - flx), sUt[i]);
-            } else {
-                sCol[i] = make_uint4(L.uvt + (uint32_t)x0 * 8u, L.uvt + (uint32_t)x1 * 8u, pack_f16x2(sx - flx, sx - flx),
-                                     sUt[i]);
-            }
-        }
-        // WIN: window block column of this warp (lane 0's first x tap)
-        const int wbx0 = WIN ? (__shfl_sync(0xffffffffu, clampi((int)floorf(fmaf((float)tid + 0.5f, sc3, -0.5f)), 0, R3 - 1), 0) >> 2) : 0;
-        const uint8_t* const wbase = smem;   // F_uvt taps: row offsets are ring rows (WIN) or slice rows
-        (void)wbx0;
-        const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
-        // decoded F_uv chunk, row-major [chunk_rows][C] RGBA8 (each warp decodes
-        // the blocks of its own 32 columns)
-        uint32_t* sUv = reinterpret_cast<uint32_t*>(smem + L.uvc);
-        // FMT_BC7_TEX: this tile's F_uv in its atlas's BC7 texture (texel centres)
-        cudaTextureObject_t uvtex = 0;
-        float tex_x0 = 0.f, tex_y0 = 0.f;
-        if constexpr (FMT_UV == FMT_BC7_TEX) {
-            const int ttx = k % p.tiles_x, tty = (k / p.tiles_x) % p.tiles_y, ta = k / (p.tiles_x * p.tiles_y);
-            uvtex = p.uvtex[ta];
-            tex_x0 = (float)(ttx * C) + 0.5f + (float)tid;
-            tex_y0 = (float)(tty * C) + 0.5f;
-        }
-        // F_uv texel (row, blk*128 + tid) as two f16x2 holding the integers q (R8)
-        auto uv_texel = [&](int row, int jr, int blk, uint32_t& lo, uint32_t& hi) {
-            if constexpr (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) {
-                u8x4_to_h2(sUv[jr * C + blk * kThreads + tid], lo, hi);
-            } else if constexpr (FMT_UV == FMT_BC7_TEX) {
-                // hardware BC7 decode returns q/255 (UNORM); x255 lands within 2^-16
-                // of q, which the f16 rounding makes exact
-                const float4 v = tex2D<float4>(uvtex, tex_x0 + (float)(blk * kThreads), tex_y0 + (float)row);
-                lo = pack_f16x2(v.x * 255.f, v.y * 255.f);
-                hi = pack_f16x2(v.z * 255.f, v.w * 255.f);
-            } else if constexpr (FMT_UV == FMT_U8) {
-                u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + blk * kThreads + tid), lo, hi);
-            } else {
-                const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)row * C + blk * kThreads + tid);
-                lo = hv.x;
-                hi = hv.y;
-            }
-        };
-        // MMA descriptors of this unit's weights
-        // layers 1, 2: f16 accumulators for h = 16 (the GELU input is f16 anyway);
-        // layer 3 (the output y): fp32
-        const uint32_t idesc1 = (H == 16 && NDGI_F16ACC) ? ptx::idesc_f16_f16(128, H) : ptx::idesc_f16_f32(128, H);
-        const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
-        constexpr uint32_t sbo2 = (uint32_t)(Cfg::K2 / 8) * 128u;
-        const uint64_t bd1 = ptx::smem_desc_kmajor(ptx::smem_addr(sB1), 128u, 256u);
-        const uint64_t bd2 = ptx::smem_desc_kmajor(ptx::smem_addr(sB2), 128u, sbo2);
-        const uint64_t bd3 = ptx::smem_desc_kmajor(ptx::smem_addr(sB3), 128u, sbo2);
-        const int out_fmt = p.out_fmt;
-        const bool tiles_border = !p.full && B > 0;
-
-        // a3: this warp's BC7 blocks of the chunk of `crows` core rows (4..16)
-        // starting at row jc: one block per lane; for short chunks (small VT
-        // batches) the spare lanes decode a duplicate and do not store, so the
-        // warp-uniform decoder paths stay converged
-        auto decode_chunk = [&](int jc, int crows) {
-            constexpr int bpw = 8 * BPR;                    // blocks per block-row for this warp
-            const int br_all = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
-            const int nbr = crows >> 2;
-            const int br = br_all < nbr ? br_all : br_all % nbr;
-            const int gbc = 32 * blk + 8 * warp + bc;       // block column in the tile
-            const size_t bidx = (size_t)((jc >> 2) + br) * (C >> 2) + gbc;
-            uint32_t* dst = sUv + (4 * br) * C + 4 * gbc;
-            const bool store = br_all < nbr;
-            uint32_t rowv[4];
-            auto sink = [&](int i, uint32_t v) {
-                rowv[i & 3] = v;
-                if ((i & 3) == 3 && store)
-                    *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
-            };
-            __syncwarp();   // previous chunk fully gathered by this warp
-            if constexpr (FMT_UV == FMT_BC1) bc1_decode(__ldg(reinterpret_cast<const uint2*>(uvmap) + bidx), false, sink);
-            else if constexpr (FMT_UV == FMT_BC3) bc3_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
-            else bc7_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
-            __syncwarp();
-        };
-
-        // WIN: this warp's ring window of the tau-blended F_uvt slice: wyb*4
-        // (a power of two) F_uvt rows x wxb*4 columns, F_uvt row y in ring row
-        // y mod (wyb*4); per chunk only the block rows not yet resident are
-        // decoded (same blend arithmetic as unit_prologue, so bit-identical to
-        // the whole-slice path)
-        int w_lo = 1, w_hi = 0;   // resident block rows [w_lo, w_hi] (empty)
-        auto stage_window = [&](int jc, int nrows) {
-            const int ymin = clampi((int)floorf(fmaf((float)jc + 0.5f, sc3, -0.5f)), 0, R3 - 1);
-            const int ymax = clampi((int)floorf(fmaf((float)(jc + nrows - 1) + 0.5f, sc3, -0.5f)) + 1, 0, R3 - 1);
-            const int blo = ymin >> 2, bhi = ymax >> 2;
-            const int nbm = R3 >> 2, ring = win.wyb;
-            const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
-            const float tau = tc.tau, omt = 1.0f - tau;
-            uint2* wdst = reinterpret_cast<uint2*>(smem + L.uvt + (uint32_t)warp * win.bytes);
-            const int WX = win.wxb * 4;
-            // new block rows: [blo, bhi] minus the resident [w_lo, w_hi] (monotone strips)
-            const int n0 = (w_hi >= w_lo && blo >= w_lo && blo <= w_hi) ? w_hi + 1 : blo;
-            const int nnew = bhi - n0 + 1;
-            __syncwarp();   // this warp's gathers of the previous chunk are done
-            if (nnew > 0) {
-                if (fmt_block4(p.fmt_uvt)) {
-                    // one BC7 / BC1 / BC3 block per lane (both slices' blocks: 2 * nnew * wxb <= 48
-                    // decodes), raw RGBA8 into this warp's part of the F_uv chunk
-                    // buffer (free between chunks: 16 rows x 128 B), then all lanes
-                    // blend texels into the ring
-                    const int nblk = nnew * win.wxb;             // block positions
-                    uint8_t* scratch = reinterpret_cast<uint8_t*>(sUv) + warp * 128;   // row r at + r * C * 4
-                    for (int g0 = 0; g0 < nblk; g0 += 16) {      // 16 positions = 32 blocks per round
-                        const int ng = nblk - g0 < 16 ? nblk - g0 : 16;
-                        {
-                            const int q = lane < 2 * ng ? lane : 0;   // spare lanes: duplicate, no store
-                            const int pos = g0 + (q >> 1), sl = q & 1;
-                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
-                            const int gbx = wbx0 + qx < nbm ? wbx0 + qx : nbm - 1;
-                            const uint8_t* src = vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0);
-                            uint32_t t[16];
-                            block4_decode(p.fmt_uvt, src, (size_t)br * nbm + gbx, [&](int i, uint32_t v) { t[i] = v; });
-                            if (lane < 2 * ng) {
-                                // scratch slot q: 64 B at row q >> 1, byte (q & 1) * 64
-                                uint4* d = reinterpret_cast<uint4*>(scratch + (size_t)(q >> 1) * C * 4 + (q & 1) * 64);
-#pragma unroll
-                                for (int r = 0; r < 4; ++r) d[r] = make_uint4(t[4 * r], t[4 * r + 1], t[4 * r + 2], t[4 * r + 3]);
-                            }
-                        }
-                        __syncwarp();
-                        for (int e = lane; e < ng * 16; e += 32) {
-                            const int pos = g0 + (e >> 4), i = e & 15;
-                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
-                            if (wbx0 + qx >= nbm) continue;
-                            const uint32_t* sp = reinterpret_cast<const uint32_t*>(scratch + (size_t)(e >> 4) * C * 4);
-                            const uint32_t q0v = sp[i], q1v = sp[16 + i];
-                            float c[4];
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = (omt * (float)((q0v >> (8 * qq)) & 0xffu) + tau * (float)((q1v >> (8 * qq)) & 0xffu)) *
-                                        (1.0f / 255.0f);
-                            wdst[((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)] =
-                                make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
-                        }
-                        __syncwarp();
-                    }
-                } else {
-                    const int ntex = nnew * 4 * WX;
-                    for (int e = lane; e < ntex; e += 32) {
-                        const int gy = n0 * 4 + e / WX, gx = wbx0 * 4 + e % WX;
-                        if (gx >= R3) continue;
-                        const int g = gy * R3 + gx;
-                        float c[4];
-                        if (p.fmt_uvt == FMT_U8) {
-                            const uint32_t q0 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k0) + g);
-                            const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + g);
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = (omt * (float)((q0 >> (8 * qq)) & 0xffu) + tau * (float)((q1 >> (8 * qq)) & 0xffu)) *
-                                        (1.0f / 255.0f);
-                        } else {
-                            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * g;
-                            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k1) + 4 * g;
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
-                        }
-                        wdst[((gy & (4 * ring - 1))) * WX + e % WX] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
-                    }
-                }
-            }
-            __syncwarp();
-            w_lo = blo;
-            w_hi = bhi;
-        };
-
-        // one layer for all S items of the step: A written by all 128 threads ->
-        // CTA barrier -> one elected lane of warp 0 issues S x (K/16) MMAs and
-        // commits them to d_ready -> everyone waits for the accumulators
-        auto run_layer = [&](auto layer) {
-            constexpr int l = decltype(layer)::value;
-            PROF_T0();
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncthreads();
-            PROF_ADD(0);
-            if (warp == 0) {
-                ptx::tc_fence_after();
-                if (ptx::elect_one()) {
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
-                        if (l == 0) {
-                            ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A1, bd1, idesc1, 0u);
-                        } else {
-#pragma unroll
-                            for (int st = 0; st < Cfg::K2 / 16; ++st)   // +256 B (= +16 in the desc) per K step
-                                ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A23 + 8u * st,
-                                                (l == 1 ? bd2 : bd3) + 16u * st, l == 1 ? idesc1 : idesc3, st > 0);
-                        }
-                    }
-                    ptx::mma_commit(bars);
-                }
-                __syncwarp();
-#if NDGI_PROFILE
-                if (lane == 0) prof[9] += clock64() - _pt;
-#endif
-            }
-#if NDGI_ONEWAIT
-            // only warp 0 polls the mbarrier; the others sleep in the CTA barrier
-            if (warp == 0) ptx::mbar_wait_fast(bars, dph);
-            __syncthreads();
-#elif NDGI_WAIT_GUARD
-            ptx::mbar_wait_fast(bars, dph);
-#else
-            ptx::mbar_wait_spin(bars, dph);
-#endif
-            PROF_ADD(1);
-            dph ^= 1u;
-            ptx::tc_fence_after();
-        };
-        using L0 = std::integral_constant<int, 0>;
-        using L1 = std::integral_constant<int, 1>;
-        using L2 = std::integral_constant<int, 2>;
-
-        // a4/a6: Eq. 4 input row of block (row, blk) -> A1 of slot s; jr = row
-        // within the decoded F_uv chunk
-        auto gather = [&](int row, int jr, int blk, int s) {
-            const uint4 rt = sRow[row];                  // y0 row byte offset, y1 row byte offset, fy, V_vt
-            const uint4 cc = sCol[blk * kThreads + tid]; // x0, x1 byte offsets (from smem base), fx, V_ut
-            const uint2 t00 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.x);
-            const uint2 t10 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.y);
-            const uint2 t01 = *reinterpret_cast<const uint2*>(wbase + rt.y + cc.x);
-            const uint2 t11 = *reinterpret_cast<const uint2*>(wbase + rt.y + cc.y);
-            uint32_t a1[8];
-            a1[0] = hlerp2(hlerp2(t00.x, t10.x, cc.z), hlerp2(t01.x, t11.x, cc.z), rt.z);
-            a1[1] = hlerp2(hlerp2(t00.y, t10.y, cc.z), hlerp2(t01.y, t11.y, cc.z), rt.z);
-            uv_texel(row, jr, blk, a1[2], a1[3]);
-            a1[4] = cc.w;
-            a1[5] = rt.w;
-            a1[6] = 0x00003C00u;  // k = 12: 1.0 (bias column), k = 13: 0
-            a1[7] = 0u;
-            ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1, a1);
-        };
-
-        // C = 128, two consecutive rows per step: both rows usually sit between
-        // the same two F_uvt rows (R3 <= C/2), so the x-lerped taps of the first
-        // row serve the second (warp-uniform test, exact: same operands)
-        auto gather_rows2 = [&](int row, int jr) {
-            const uint4 rt0 = sRow[row], rt1 = sRow[row + 1];
-            const uint4 cc = sCol[tid];
-            auto xlerp = [&](uint32_t yoff, uint32_t& lo, uint32_t& hi) {
-                const uint2 a = *reinterpret_cast<const uint2*>(wbase + yoff + cc.x);
-                const uint2 b = *reinterpret_cast<const uint2*>(wbase + yoff + cc.y);
-                lo = hlerp2(a.x, b.x, cc.z);
-                hi = hlerp2(a.y, b.y, cc.z);
-            };
-            uint32_t y0lo, y0hi, y1lo, y1hi;
-            xlerp(rt0.x, y0lo, y0hi);
-            xlerp(rt0.y, y1lo, y1hi);
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const uint4 rt = s ? rt1 : rt0;
-                if (s == 1 && (rt1.x != rt0.x || rt1.y != rt0.y)) {
-                    xlerp(rt1.x, y0lo, y0hi);
-                    xlerp(rt1.y, y1lo, y1hi);
-                }
-                uint32_t a1[8];
-                a1[0] = hlerp2(y0lo, y1lo, rt.z);
-                a1[1] = hlerp2(y0hi, y1hi, rt.z);
-                uv_texel(row + s, jr + s, 0, a1[2], a1[3]);
-                a1[4] = cc.w;
-                a1[5] = rt.w;
-                a1[6] = 0x00003C00u;
-                a1[7] = 0u;
-                ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1, a1);
-            }
-        };
-
-        // FULL8: this thread's texel of core row j_begin in the RGBA8 atlas
-        uint32_t* const orow = reinterpret_cast<uint32_t*>(p.out) + out_base + (size_t)j_begin * row_pitch + tid;
-        const uint32_t rp32 = (uint32_t)row_pitch;
-
-        // a8: y of block (row j, blk) in slot s -> page cache
-        auto output = [&](int j, int blk, int s) {
-            const int i = blk * kThreads + tid;
-            uint32_t yv[4];
-            ptx::tmem_ld_x4(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, yv);
-            ptx::tmem_wait_ld();
-            const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
-            if constexpr (FULL8) {
-                orow[(size_t)((uint32_t)(j - j_begin) * rp32) + blk * kThreads] = rgba8_fma(y0f, y1f, y2f);
-                return;
-            }
-            if constexpr (TILES8) {
-                // slot-relative 32-bit offsets; mirrored copies (R3): core i -> -i, 2(C-1)-i
-                const uint32_t v = rgba8_fma(y0f, y1f, y2f);
-                uint32_t* const tb = reinterpret_cast<uint32_t*>(p.out) + out_base;
-                const int P_ = (int)rp32;
-                tb[j * P_ + i] = v;
-                const bool bx = B > 0 && ((i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2));
-                const int xm = i <= B ? -i : 2 * (C - 1) - i;
-                if (bx) tb[j * P_ + xm] = v;
-                if (B > 0 && ((j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2))) {   // CTA-uniform
-                    const int ym = j <= B ? -j : 2 * (C - 1) - j;
-                    tb[ym * P_ + i] = v;
-                    if (bx) tb[ym * P_ + xm] = v;
-                }
-                return;
-            }
-            const size_t o = out_base + (size_t)j * row_pitch + i;
-            if (out_fmt == OUT_RGBA8) {
-                const uint32_t v = rgba8_fma(y0f, y1f, y2f);
-                uint32_t* out = reinterpret_cast<uint32_t*>(p.out);
-                out[o] = v;
-                if (tiles_border) {
-                    const bool bx = (i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2);
-                    const bool by = (j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2);
-                    if (bx || by) {
-                        // mirrored positions (R3): core i -> padded-core offsets -i and 2(C-1)-i
-                        const ptrdiff_t xm = i <= B ? -i : 2 * (C - 1) - i;
-                        const ptrdiff_t ym = j <= B ? -j : 2 * (C - 1) - j;
-                        const ptrdiff_t base = (ptrdiff_t)out_base, rp = (ptrdiff_t)row_pitch;
-                        if (bx) out[base + j * rp + xm] = v;
-                        if (by) out[base + ym * rp + i] = v;
-                        if (bx && by) out[base + ym * rp + xm] = v;
-                    }
-                }
-                return;
-            }
-            store_texel(p.out, o, out_fmt, y0f, y1f, y2f);
-            if (tiles_border) {
-                const bool bx = (i >= 1 && i <= B) || (i >= C - 1 - B && i <= C - 2);
-                const bool by = (j >= 1 && j <= B) || (j >= C - 1 - B && j <= C - 2);
-                if (bx || by) {
-                    const int xm = i <= B ? -i : 2 * (C - 1) - i;
-                    const int ym = j <= B ? -j : 2 * (C - 1) - j;
-                    const ptrdiff_t base = (ptrdiff_t)out_base, rp = (ptrdiff_t)row_pitch;
-                    if (bx) store_texel(p.out, (size_t)(base + (ptrdiff_t)j * rp + xm), out_fmt, y0f, y1f, y2f);
-                    if (by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + i), out_fmt, y0f, y1f, y2f);
-                    if (bx && by) store_texel(p.out, (size_t)(base + (ptrdiff_t)ym * rp + xm), out_fmt, y0f, y1f, y2f);
-                }
-            }
-        };
-
-        auto epilogues = [&]() {
-#if NDGI_JOINT_EPI
-            if constexpr (H == 16) {
-#if NDGI_F16ACC
-                gelu_epilogue_h16_f16acc<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
-#else
-                gelu_epilogue_h16<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
-#endif
-                return;
-            }
-#endif
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-                gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);
-        };
-
-        // S items per step; item n = (row j_begin + n / BPR, block n % BPR)
-#if NDGI_PROFILE
-        const long long loop_t0 = clock64();
-#endif
-        // strips are whole F_uv chunks, or (small batches) 4..8-row strips
-        const int crows = p.strip_rows < chunk_rows ? p.strip_rows : chunk_rows;
-        const int chunk_items = crows * BPR;
-        for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
-        if constexpr (WIN) stage_window(j_begin + c0 / BPR, crows);   // uses the F_uv chunk buffer as scratch
-        if (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) decode_chunk(j_begin + c0 / BPR, crows);
-        for (int it = c0; it < c0 + chunk_items; it += S) {
-            PROF_T0();
-            if constexpr (BPR == 1 && S == 2) {
-                gather_rows2(j_begin + it, it - c0);
-            } else {
-#pragma unroll
-                for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s - c0) / BPR, (it + s) % BPR, s);
-            }
-            PROF_ADD(3);
-            run_layer(L0{});
-            PROF_T0();
-            epilogues();
-            PROF_ADD(2);
-            run_layer(L1{});
-            PROF_T0();
-            epilogues();
-            PROF_ADD(2);
-            run_layer(L2{});
-            PROF_T0();
-#pragma unroll
-            for (int s = 0; s < S; ++s) output(j_begin + (it + s) / BPR, (it + s) % BPR, s);
-            PROF_ADD(4);
-#if NDGI_PROFILE
-            if (lane == 0) prof[7] += 1;
-#endif
-        }
-        }
-#if NDGI_PROFILE
-        if (lane == 0) prof[8] += clock64() - loop_t0;
-#endif
-    }
-
-    // ---- teardown --------------------------------------------------------------------
-#if NDGI_PROFILE
-    prof[6] = clock64() - prof_start;
-    if (tid == 0) atomicSub(&g_ndgi_res[smid & 255], 1);
-    if (lane == 0)
-        for (int q = 0; q < 10; ++q) atomicAdd(&g_ndgi_prof[q], prof[q]);
-#endif
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 0) ptx::tmem_dealloc<Cfg::TM_COLS>(tmem);
-}
-
-// ---- host-side launch helpers ---------------------------------------------------
-// Launch configuration of one kernel instantiation on one device for one smem
-// size: computed once (attribute calls cost microseconds, which a small VT
-// batch would otherwise pay on every call).
-struct LaunchCfg {
-    const void* kern;
-    int dev;
-    uint32_t smem;
-    int occ;
-};
-
-template <typename K>
-static cudaError_t fused_launch_cfg(K kern, uint32_t smem, int tmem_cols, int& occ_out) {
-    static std::mutex mu;
-    static std::vector<LaunchCfg> cache;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    std::lock_guard<std::mutex> lock(mu);
-    // the dynamic-smem limit is per-kernel state: keep it at the largest size
-    // this kernel has been configured for (a smaller later setting would make
-    // a cached larger configuration fail to launch)
-    uint32_t attr = smem;
-    for (const LaunchCfg& c : cache) {
-        if (c.kern != reinterpret_cast<const void*>(kern) || c.dev != dev) continue;
-        if (c.smem == smem) {
-            occ_out = c.occ;
-            return cudaSuccess;
-        }
-        if (c.smem > attr) attr = c.smem;
-    }
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    // Resident CTAs per SM from the kernel's own resource use (the runtime's
-    // occupancy query reports 1 for tcgen05 kernels on driver 580).
-    cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    int smem_sm = 0, regs_sm = 0;
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-    const int regs_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (kThreads / 32);   // per-warp allocation unit 256
-    const int smem_cta = (int)smem + (int)fa.sharedSizeBytes + 1024;   // + per-CTA reserved smem
-    int occ = regs_sm / regs_cta;
-    if (smem_sm / smem_cta < occ) occ = smem_sm / smem_cta;
-    const int tmem_cap = 512 / tmem_cols;
-    if (occ > tmem_cap) occ = tmem_cap;
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    if (getenv("NDGI_VERBOSE"))
-        fprintf(stderr, "[ndgi] fused launch cfg: occ=%d (regs %d, local %zu) smem=%u\n", occ, fa.numRegs,
-                fa.localSizeBytes, smem);
-    cache.push_back(LaunchCfg{reinterpret_cast<const void*>(kern), dev, smem, occ});
-    occ_out = occ;
-    return cudaSuccess;
-}
-
+// per-format instantiations live in fused_h*_*.cu (parallel compilation)
 template <int H, int FMT_UV, int CT>
-static cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
-    const FusedSmem L = fused_smem_layout<H>(CT, p.R3);
-    const bool full8 = p.full && p.out_fmt == OUT_RGBA8;
-    // windowed F_uvt when the whole slice would cost residency (h = 16, C = 128)
-    constexpr bool kWinOk = H == 16 && CT == 128;
-    const bool win = kWinOk && p.R3 > 32;
-    uint32_t smem = L.total;
-    if (win) smem = L.uvt + 4u * uvt_window(p.R3, CT, kChunkTexels / CT).bytes;
-    const bool tiles8 = !p.full && p.out_fmt == OUT_RGBA8;
-    auto pick = [&](auto ok, auto w) {
-        return ndgi_fused_kernel<H, FMT_UV, CT, decltype(ok)::value, decltype(w)::value && kWinOk>;
-    };
-    using K0 = std::integral_constant<int, 0>;
-    using K1 = std::integral_constant<int, 1>;
-    using K2 = std::integral_constant<int, 2>;
-    using T_ = std::true_type;
-    using F_ = std::false_type;
-    auto kern = full8 ? (win ? pick(K1{}, T_{}) : pick(K1{}, F_{}))
-                      : tiles8 ? (win ? pick(K2{}, T_{}) : pick(K2{}, F_{}))
-                               : (win ? pick(K0{}, T_{}) : pick(K0{}, F_{}));
-    int occ = 0;
-    cudaError_t e = fused_launch_cfg(kern, smem, FusedCfg<H>::TM_COLS, occ);
-    if (e != cudaSuccess) return e;
-    const uint32_t cap = (uint32_t)(num_sms * occ);
-    const uint32_t grid = p.units < cap ? p.units : cap;
-    kern<<<grid, kThreads, smem, s>>>(p);
-    return cudaGetLastError();
-}
+cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s);
 
-#if NDGI_PROFILE
-int fused_prof_read(unsigned long long* out8, int reset) {
-    cudaMemcpyFromSymbol(out8, g_ndgi_prof, 12 * sizeof(unsigned long long));
-    if (reset) {
-        unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-        cudaMemcpyToSymbol(g_ndgi_prof, z, sizeof(z));
-    }
-    return 1;
+template <int H, int CT>
+static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t s) {
+    if (p.fmt_uv == FMT_BC7_TEX) return launch_fused_t<H, FMT_BC7_TEX, CT>(p, num_sms, s);
+    if (p.fmt_uv == FMT_BC7) return launch_fused_t<H, FMT_BC7, CT>(p, num_sms, s);
+    if (p.fmt_uv == FMT_U8) return launch_fused_t<H, FMT_U8, CT>(p, num_sms, s);
+    if (p.fmt_uv == FMT_BC1) return launch_fused_t<H, FMT_BC1, CT>(p, num_sms, s);
+    if (p.fmt_uv == FMT_BC3) return launch_fused_t<H, FMT_BC3, CT>(p, num_sms, s);
+    return launch_fused_t<H, FMT_F16, CT>(p, num_sms, s);
 }
-#else
-int fused_prof_read(unsigned long long*, int) { return 0; }
-#endif
 
 size_t wpack_tile_bytes(int H) { return H == 16 ? WPack<16>::BYTES : WPack<64>::BYTES; }
 
@@ -702,17 +32,15 @@ cudaError_t prep_weights(const uint16_t* mlp, size_t tile_elems, int H, int fmt_
     return cudaGetLastError();
 }
 
-int fused_ctas_per_sm(int H) { return H == 16 ? FusedCfg<16>::MIN_CTAS : FusedCfg<64>::MIN_CTAS; }
-
-template <int H, int CT>
-static cudaError_t launch_fused_fmt(const KParams& p, int num_sms, cudaStream_t s) {
-    if (p.fmt_uv == FMT_BC7_TEX) return launch_fused_t<H, FMT_BC7_TEX, CT>(p, num_sms, s);
-    if (p.fmt_uv == FMT_BC7) return launch_fused_t<H, FMT_BC7, CT>(p, num_sms, s);
-    if (p.fmt_uv == FMT_U8) return launch_fused_t<H, FMT_U8, CT>(p, num_sms, s);
-    if (p.fmt_uv == FMT_BC1) return launch_fused_t<H, FMT_BC1, CT>(p, num_sms, s);
-    if (p.fmt_uv == FMT_BC3) return launch_fused_t<H, FMT_BC3, CT>(p, num_sms, s);
-    return launch_fused_t<H, FMT_F16, CT>(p, num_sms, s);
+// the GELU split compiled into the epilogues: MUFU pairs of every 16 (h = 16:
+// a step's two items take NDGI_POLY_PAIRS_ITEM0 + NDGI_POLY_PAIRS polynomial
+// pairs of their 2 x 8; h = 64: NDGI_POLY_PAIRS of every 8)
+int fused_gelu_mufu_pairs(int H) {
+    return H == 16 ? 16 - NDGI_POLY_PAIRS_ITEM0 - NDGI_POLY_PAIRS : 16 - 2 * NDGI_POLY_PAIRS;
 }
+int fused_f16acc() { return NDGI_F16ACC; }
+
+int fused_ctas_per_sm(int H) { return H == 16 ? FusedCfg<16>::MIN_CTAS : FusedCfg<64>::MIN_CTAS; }
 
 cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s) {
     if (p.H == 16) return p.C == 128 ? launch_fused_fmt<16, 128>(p, num_sms, s) : launch_fused_fmt<16, 256>(p, num_sms, s);

@@ -1,0 +1,599 @@
+#pragma once
+// fused_kernel.cuh -- NDGI_MODE_FAST: the fused tile-decode kernel for sm_100a
+// (template; instantiated per (h, C) in fused_h*_c*.cu, dispatched in fused_kernel.cu).
+//
+// One persistent kernel does the whole hot path of SURVEY.md §8(a):
+//   a1  work units (query time, request, strip of core rows); call constants
+//       gamma(t), k0/k1/tau, r0/r1/rho come precomputed from the host
+//   a2  per unit: the tile's f16 MLP -> smem B operands, the two BC7 t-slices
+//       of F_uvt, the line maps at t; per 16-row chunk the BC7 F_uv blocks
+//   a3  BC7 decode (bc7_device.cuh), one block per lane, each warp decoding
+//       exactly the blocks its own texels need (no CTA barrier)
+//   a4  V_uvt: tau-blended slice (f16, smem) sampled bilinearly (f16x2 math);
+//       V_uv: the texel itself (R2); V_ut per column / V_vt per row (f16x2)
+//   a5  gamma(t): folded into layer-1's bias column (R6)
+//   a6  the 16-wide Eq. 4 input row of each texel -> TMEM (tcgen05.st)
+//   a7  G_Phi on the 5th-gen tensor cores: per 128-texel block three
+//       tcgen05.mma (kind::f16, M=128) with A in TMEM, B (weights) in smem,
+//       fp32 accumulators in TMEM; biases ride in an extra K chunk (A column
+//       of ones); GELU in the epilogue on packed f16x2 (tanh.approx), its
+//       constants folded into the next layer's weights
+//   a8  RGBA8 (or 16F/32F) page-cache writer: core + mirrored border (R3)
+//
+// CTA = 4 warps; thread t owns TMEM lane t, i.e. texel t of each 128-texel
+// item.  A step carries S items (S TMEM slots: 2 for h = 16, 1 for h = 64)
+// through the three layers together: per layer one CTA barrier, S (x K/16)
+// tcgen05.mma issued by one elected lane, one tcgen05.commit -> mbarrier.
+// Several CTAs per SM (6 for h = 16) hide each other's MMA latency.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "fused_common.cuh"
+
+namespace ndgi {
+
+constexpr int kThreads = 128;
+
+#ifndef NDGI_JOINT_EPI
+#define NDGI_JOINT_EPI 1
+#endif
+
+// FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
+// no format switch, row pointers instead of 64-bit index arithmetic
+// WIN: F_uvt staged per chunk in per-warp windows instead of the whole slice
+// (large R3: the H profile's 32 KB slice would halve residency)
+// OUTK: 0 any format / addressing, 1 (FULL8) decode_full RGBA8, 2 (TILES8)
+// decode_tiles RGBA8 (core + mirrored border with 32-bit offsets from the slot)
+template <int H, int FMT_UV, int CT, int OUTK, bool WIN>
+__global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_kernel(const __grid_constant__ KParams p) {
+    constexpr bool FULL8 = OUTK == 1, TILES8 = OUTK == 2;
+    using Cfg = FusedCfg<H>;
+    constexpr int S = Cfg::SLOTS;
+    constexpr int C = CT;                       // core texels per tile side (128 or 256)
+    constexpr int BPR = CT / kThreads;          // 128-texel MMA blocks per row
+    constexpr int chunk_rows = kChunkTexels / CT;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const FusedSmem L = fused_smem_layout<H>(C, p.R3);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t bars = ptx::smem_addr(smem + L.bars);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
+    __half* sB1 = reinterpret_cast<__half*>(smem + L.b1);
+    __half* sB2 = reinterpret_cast<__half*>(smem + L.b2);
+    __half* sB3 = reinterpret_cast<__half*>(smem + L.b3);
+    uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
+    uint4* sRow = reinterpret_cast<uint4*>(smem + L.rowtab);
+
+    // ---- one-time setup: counters, mbarriers, TMEM allocation -------------------
+    if (tid < 8) reinterpret_cast<uint32_t*>(smem + L.cnt)[tid] = 0u;
+    if (tid == 0) {
+        ptx::mbar_init(bars, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<Cfg::TM_COLS>(ptx::smem_addr(tmem_slot));
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int B = p.B, P = p.P, R3 = p.R3;
+    const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
+    static_assert(!WIN || CT == 128, "windowed F_uvt is built for C = 128");
+    const UvtWindow win = uvt_window(R3, C, chunk_rows);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
+    const uint32_t tm_lane = tmem + lane_base;
+
+    {   // every slot's feature chunk (FusedCfg): [1, 0 | 0 ...] -- the bias column of
+        // all three layers; the feature columns are written per unit / item
+        uint32_t c[8] = {0x00003C00u, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int s = 0; s < S; ++s) ptx::tmem_st_x8(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1, c);
+        ptx::tmem_wait_st();
+    }
+
+    uint32_t dph = 0u;   // d_ready phase
+
+    for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
+        const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
+        const uint32_t rq = unit / (uint32_t)p.strips_per_tile;
+        const int ti = (int)(rq / p.n_req);
+        const uint32_t r = rq % p.n_req;
+        const TConst& tc = p.tc[ti];
+        int k;
+        size_t out_base;   // texel index of core texel (0,0)
+        size_t row_pitch;  // texels between rows
+        if (p.full) {
+            k = (int)r;
+            const int tx = k % p.tiles_x, ty = (k / p.tiles_x) % p.tiles_y, a = k / (p.tiles_x * p.tiles_y);
+            row_pitch = (size_t)p.tiles_x * C;
+            out_base = (size_t)ti * p.out_t_stride + (size_t)a * p.tiles_y * C * row_pitch +
+                       (size_t)ty * C * row_pitch + (size_t)tx * C;
+        } else {
+            const uint32_t id = __ldg(p.tile_ids + r);
+            const uint32_t slot = p.slots ? __ldg(p.slots + r) : r;
+            if (id >= (uint32_t)p.num_tiles || slot >= p.num_slots) {
+                if (strip == 0 && tid == 0) atomicAdd(p.err, 1u);
+                continue;  // uniform across the CTA
+            }
+            k = (int)id;
+            row_pitch = (size_t)P;
+            out_base = ((size_t)slot * P + B) * P + B;
+        }
+        const int nitems = p.strip_rows * BPR;     // 128-texel blocks of this unit (multiple of S)
+        const int j_begin = strip * p.strip_rows;
+
+        // ---- a2: tile parameters -> shared memory -----------------------------------
+        __syncthreads();  // previous unit's MMAs complete and all smem readers done
+        {
+            copy_prepacked_weights<H>(p, tc, k, smem, L, tid, kThreads);
+            unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads, WIN ? win.pitch : 0u, win.wyb * 4);
+        }
+        ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
+        __syncthreads();
+
+        // per-column gather constants (column i = b*128 + tid, written and read by
+        // the same thread): byte offsets of the two F_uvt x taps from the smem
+        // base, the x weight, V_ut
+        uint4* sCol = reinterpret_cast<uint4*>(smem + L.colc);
+#pragma unroll
+        for (int b = 0; b < BPR; ++b) {
+            const int i = b * kThreads + tid;
+            const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
+            const float flx = floorf(sx);
+            const int x0 = clampi((int)flx, 0, R3 - 1), x1 = clampi((int)flx + 1, 0, R3 - 1);
+            if constexpr (WIN) {
+                // this warp's window starts at the block column of its lane 0
+                const int wx0 = __shfl_sync(0xffffffffu, x0, 0) & ~3;
+                const uint32_t wb = L.uvt + (uint32_t)warp * win.bytes;
+                sCol[i] = make_uint4(wb + (uint32_t)(x0 - wx0) * 8u, wb + (uint32_t)(x1 - wx0) * 8u,
+                                     pack_f16x2(sx - flx, sx - flx), sUt[i]);
+            } else {
+                sCol[i] = make_uint4(L.uvt + (uint32_t)x0 * 8u, L.uvt + (uint32_t)x1 * 8u, pack_f16x2(sx - flx, sx - flx),
+                                     sUt[i]);
+            }
+        }
+        if constexpr (BPR == 1) {   // V_ut of this thread's column: constant over the unit
+#pragma unroll
+            for (int s = 0; s < S; ++s) ptx::tmem_st_x1(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1 + 1, sUt[tid]);
+        }
+        // WIN: window block column of this warp (lane 0's first x tap)
+        const int wbx0 = WIN ? (__shfl_sync(0xffffffffu, clampi((int)floorf(fmaf((float)tid + 0.5f, sc3, -0.5f)), 0, R3 - 1), 0) >> 2) : 0;
+        const uint8_t* const wbase = smem;   // F_uvt taps: row offsets are ring rows (WIN) or slice rows
+        (void)wbx0;
+        const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
+        // decoded F_uv chunk, row-major [chunk_rows][C] RGBA8 (each warp decodes
+        // the blocks of its own 32 columns)
+        uint32_t* sUv = reinterpret_cast<uint32_t*>(smem + L.uvc);
+        // FMT_BC7_TEX: this tile's F_uv in its atlas's BC7 texture (texel centres)
+        cudaTextureObject_t uvtex = 0;
+        float tex_x0 = 0.f, tex_y0 = 0.f;
+        if constexpr (FMT_UV == FMT_BC7_TEX) {
+            const int ttx = k % p.tiles_x, tty = (k / p.tiles_x) % p.tiles_y, ta = k / (p.tiles_x * p.tiles_y);
+            uvtex = p.uvtex[ta];
+            tex_x0 = (float)(ttx * C) + 0.5f + (float)tid;
+            tex_y0 = (float)(tty * C) + 0.5f;
+        }
+        // F_uv texel (row, blk*128 + tid) as two f16x2 holding the integers q (R8)
+        auto uv_texel = [&](int row, int jr, int blk, uint32_t& lo, uint32_t& hi) {
+            if constexpr (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) {
+                u8x4_to_h2(sUv[jr * C + blk * kThreads + tid], lo, hi);
+            } else if constexpr (FMT_UV == FMT_BC7_TEX) {
+                // hardware BC7 decode returns q/255 (UNORM); x255 lands within 2^-16
+                // of q, which the f16 rounding makes exact
+                const float4 v = tex2D<float4>(uvtex, tex_x0 + (float)(blk * kThreads), tex_y0 + (float)row);
+                lo = pack_f16x2(v.x * 255.f, v.y * 255.f);
+                hi = pack_f16x2(v.z * 255.f, v.w * 255.f);
+            } else if constexpr (FMT_UV == FMT_U8) {
+                u8x4_to_h2(__ldg(reinterpret_cast<const uint32_t*>(uvmap) + (size_t)row * C + blk * kThreads + tid), lo, hi);
+            } else {
+                const uint2 hv = __ldg(reinterpret_cast<const uint2*>(uvmap) + (size_t)row * C + blk * kThreads + tid);
+                lo = hv.x;
+                hi = hv.y;
+            }
+        };
+        // MMA descriptors of this unit's weights
+        // layers 1, 2: f16 accumulators for h = 16 (the GELU input is f16 anyway);
+        // layer 3 (the output y): fp32
+        const uint32_t idesc1 = (H == 16 && NDGI_F16ACC) ? ptx::idesc_f16_f16(128, H) : ptx::idesc_f16_f32(128, H);
+        const uint32_t idesc3 = ptx::idesc_f16_f32(128, 16);
+        constexpr uint32_t sbo2 = (uint32_t)(Cfg::K2 / 8) * 128u;
+        const uint64_t bd1 = ptx::smem_desc_kmajor(ptx::smem_addr(sB1), 128u, 256u);
+        const uint64_t bd2 = ptx::smem_desc_kmajor(ptx::smem_addr(sB2), 128u, sbo2);
+        const uint64_t bd3 = ptx::smem_desc_kmajor(ptx::smem_addr(sB3), 128u, sbo2);
+        const int out_fmt = p.out_fmt;
+        const bool tiles_border = !p.full && B > 0;
+
+        // a3: this warp's BC7 blocks of the chunk of `crows` core rows (4..16)
+        // starting at row jc: one block per lane; for short chunks (small VT
+        // batches) the spare lanes decode a duplicate and do not store, so the
+        // warp-uniform decoder paths stay converged
+        auto decode_chunk = [&](int jc, int crows) {
+            constexpr int bpw = 8 * BPR;                    // blocks per block-row for this warp
+            const int br_all = lane / bpw, q = lane % bpw, blk = q >> 3, bc = q & 7;
+            const int nbr = crows >> 2;
+            const int br = br_all < nbr ? br_all : br_all % nbr;
+            const int gbc = 32 * blk + 8 * warp + bc;       // block column in the tile
+            const size_t bidx = (size_t)((jc >> 2) + br) * (C >> 2) + gbc;
+            uint32_t* dst = sUv + (4 * br) * C + 4 * gbc;
+            const bool store = br_all < nbr;
+            uint32_t rowv[4];
+            auto sink = [&](int i, uint32_t v) {
+                rowv[i & 3] = v;
+                if ((i & 3) == 3 && store)
+                    *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
+            };
+            __syncwarp();   // previous chunk fully gathered by this warp
+            if constexpr (FMT_UV == FMT_BC1) bc1_decode(__ldg(reinterpret_cast<const uint2*>(uvmap) + bidx), false, sink);
+            else if constexpr (FMT_UV == FMT_BC3) bc3_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
+            else bc7_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
+            __syncwarp();
+        };
+
+        // WIN: this warp's ring window of the tau-blended F_uvt slice: wyb*4
+        // (a power of two) F_uvt rows x wxb*4 columns, F_uvt row y in ring row
+        // y mod (wyb*4); per chunk only the block rows not yet resident are
+        // decoded (same blend arithmetic as unit_prologue, so bit-identical to
+        // the whole-slice path)
+        int w_lo = 1, w_hi = 0;   // resident block rows [w_lo, w_hi] (empty)
+        auto stage_window = [&](int jc, int nrows) {
+            const int ymin = clampi((int)floorf(fmaf((float)jc + 0.5f, sc3, -0.5f)), 0, R3 - 1);
+            const int ymax = clampi((int)floorf(fmaf((float)(jc + nrows - 1) + 0.5f, sc3, -0.5f)) + 1, 0, R3 - 1);
+            const int blo = ymin >> 2, bhi = ymax >> 2;
+            const int nbm = R3 >> 2, ring = win.wyb;
+            const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
+            const float tau = tc.tau, omt = 1.0f - tau;
+            uint2* wdst = reinterpret_cast<uint2*>(smem + L.uvt + (uint32_t)warp * win.bytes);
+            const int WX = win.wxb * 4;
+            // new block rows: [blo, bhi] minus the resident [w_lo, w_hi] (monotone strips)
+            const int n0 = (w_hi >= w_lo && blo >= w_lo && blo <= w_hi) ? w_hi + 1 : blo;
+            const int nnew = bhi - n0 + 1;
+            __syncwarp();   // this warp's gathers of the previous chunk are done
+            if (nnew > 0) {
+                if (fmt_block4(p.fmt_uvt)) {
+                    // one BC7 / BC1 / BC3 block per lane (both slices' blocks: 2 * nnew * wxb <= 48
+                    // decodes), raw RGBA8 into this warp's part of the F_uv chunk
+                    // buffer (free between chunks: 16 rows x 128 B), then all lanes
+                    // blend texels into the ring
+                    const int nblk = nnew * win.wxb;             // block positions
+                    uint8_t* scratch = reinterpret_cast<uint8_t*>(sUv) + warp * 128;   // row r at + r * C * 4
+                    for (int g0 = 0; g0 < nblk; g0 += 16) {      // 16 positions = 32 blocks per round
+                        const int ng = nblk - g0 < 16 ? nblk - g0 : 16;
+                        {
+                            const int q = lane < 2 * ng ? lane : 0;   // spare lanes: duplicate, no store
+                            const int pos = g0 + (q >> 1), sl = q & 1;
+                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
+                            const int gbx = wbx0 + qx < nbm ? wbx0 + qx : nbm - 1;
+                            const uint8_t* src = vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0);
+                            uint32_t t[16];
+                            block4_decode(p.fmt_uvt, src, (size_t)br * nbm + gbx, [&](int i, uint32_t v) { t[i] = v; });
+                            if (lane < 2 * ng) {
+                                // scratch slot q: 64 B at row q >> 1, byte (q & 1) * 64
+                                uint4* d = reinterpret_cast<uint4*>(scratch + (size_t)(q >> 1) * C * 4 + (q & 1) * 64);
+#pragma unroll
+                                for (int r = 0; r < 4; ++r) d[r] = make_uint4(t[4 * r], t[4 * r + 1], t[4 * r + 2], t[4 * r + 3]);
+                            }
+                        }
+                        __syncwarp();
+                        for (int e = lane; e < ng * 16; e += 32) {
+                            const int pos = g0 + (e >> 4), i = e & 15;
+                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
+                            if (wbx0 + qx >= nbm) continue;
+                            const uint32_t* sp = reinterpret_cast<const uint32_t*>(scratch + (size_t)(e >> 4) * C * 4);
+                            const uint32_t q0v = sp[i], q1v = sp[16 + i];
+                            float c[4];
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[qq] = (omt * (float)((q0v >> (8 * qq)) & 0xffu) + tau * (float)((q1v >> (8 * qq)) & 0xffu)) *
+                                        (1.0f / 255.0f);
+                            wdst[((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)] =
+                                make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+                        }
+                        __syncwarp();
+                    }
+                } else {
+                    const int ntex = nnew * 4 * WX;
+                    for (int e = lane; e < ntex; e += 32) {
+                        const int gy = n0 * 4 + e / WX, gx = wbx0 * 4 + e % WX;
+                        if (gx >= R3 || gy >= R3) continue;
+                        const int g = gy * R3 + gx;
+                        float c[4];
+                        if (p.fmt_uvt == FMT_U8) {
+                            const uint32_t q0 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k0) + g);
+                            const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + g);
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[qq] = (omt * (float)((q0 >> (8 * qq)) & 0xffu) + tau * (float)((q1 >> (8 * qq)) & 0xffu)) *
+                                        (1.0f / 255.0f);
+                        } else {
+                            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * g;
+                            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k1) + 4 * g;
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
+                        }
+                        wdst[((gy & (4 * ring - 1))) * WX + e % WX] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+                    }
+                }
+            }
+            __syncwarp();
+            w_lo = blo;
+            w_hi = bhi;
+        };
+
+        // one layer for all S items of the step: A written by all 128 threads ->
+        // CTA barrier -> one elected lane of warp 0 issues S x (K/16) MMAs and
+        // commits them to d_ready -> everyone waits for the accumulators
+        auto run_layer = [&](auto layer) {
+            constexpr int l = decltype(layer)::value;
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncthreads();
+            if (warp == 0) {
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        const uint32_t slot = tmem + s * Cfg::SLOT_COLS;
+                        if (l == 0) {
+                            ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A1, bd1, idesc1, 0u);
+                        } else {
+#pragma unroll
+                            for (int st = 0; st < Cfg::K2 / 16; ++st)   // +256 B (= +16 in the desc) per K step
+                                ptx::mma_f16_ts(slot + Cfg::TM_D, slot + Cfg::TM_A23 + 8u * st,
+                                                (l == 1 ? bd2 : bd3) + 16u * st, l == 1 ? idesc1 : idesc3, st > 0);
+                        }
+                    }
+                    ptx::mma_commit(bars);
+                }
+                __syncwarp();
+            }
+            ptx::mbar_wait_spin(bars, dph);
+            dph ^= 1u;
+            ptx::tc_fence_after();
+        };
+        using L0 = std::integral_constant<int, 0>;
+        using L1 = std::integral_constant<int, 1>;
+        using L2 = std::integral_constant<int, 2>;
+
+        // a4/a6: the Eq. 4 inputs of block (row, blk) -> the feature chunk of slot
+        // s (FusedCfg: V_uvt, F_uv per item, V_vt per row); jr = row within the
+        // decoded F_uv chunk
+        auto put_features = [&](int s, uint32_t uvt_lo, uint32_t uvt_hi, int row, int jr, int blk, uint32_t vut,
+                                uint32_t vvt) {
+            uint32_t uv_lo, uv_hi;
+            uv_texel(row, jr, blk, uv_lo, uv_hi);
+            const uint32_t base = tm_lane + s * Cfg::SLOT_COLS;
+            ptx::tmem_st_x4(base + Cfg::TM_UVT, uvt_lo, uvt_hi, uv_lo, uv_hi);
+            if constexpr (BPR == 1) ptx::tmem_st_x1(base + Cfg::TM_VT, vvt);
+            else ptx::tmem_st_x2(base + Cfg::TM_A1 + 1, vut, vvt);
+        };
+        auto gather = [&](int row, int jr, int blk, int s) {
+            const uint4 rt = sRow[row];                  // y0 row byte offset, y1 row byte offset, fy, V_vt
+            const uint4 cc = sCol[blk * kThreads + tid]; // x0, x1 byte offsets (from smem base), fx, V_ut
+            const uint2 t00 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.x);
+            const uint2 t10 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.y);
+            const uint2 t01 = *reinterpret_cast<const uint2*>(wbase + rt.y + cc.x);
+            const uint2 t11 = *reinterpret_cast<const uint2*>(wbase + rt.y + cc.y);
+            put_features(s, hlerp2(hlerp2(t00.x, t10.x, cc.z), hlerp2(t01.x, t11.x, cc.z), rt.z),
+                         hlerp2(hlerp2(t00.y, t10.y, cc.z), hlerp2(t01.y, t11.y, cc.z), rt.z), row, jr, blk, cc.w, rt.w);
+        };
+
+        // C = 128, two consecutive rows per step: both rows usually sit between
+        // the same two F_uvt rows (R3 <= C/2), so the x-lerped taps of the first
+        // row serve the second (warp-uniform test, exact: same operands)
+        auto gather_rows2 = [&](int row, int jr) {
+            const uint4 rt0 = sRow[row], rt1 = sRow[row + 1];
+            const uint4 cc = sCol[tid];
+            auto xlerp = [&](uint32_t yoff, uint32_t& lo, uint32_t& hi) {
+                const uint2 a = *reinterpret_cast<const uint2*>(wbase + yoff + cc.x);
+                const uint2 b = *reinterpret_cast<const uint2*>(wbase + yoff + cc.y);
+                lo = hlerp2(a.x, b.x, cc.z);
+                hi = hlerp2(a.y, b.y, cc.z);
+            };
+            uint32_t y0lo, y0hi, y1lo, y1hi;
+            xlerp(rt0.x, y0lo, y0hi);
+            xlerp(rt0.y, y1lo, y1hi);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const uint4 rt = s ? rt1 : rt0;
+                if (s == 1 && (rt1.x != rt0.x || rt1.y != rt0.y)) {
+                    xlerp(rt1.x, y0lo, y0hi);
+                    xlerp(rt1.y, y1lo, y1hi);
+                }
+                put_features(s, hlerp2(y0lo, y1lo, rt.z), hlerp2(y0hi, y1hi, rt.z), row + s, jr + s, 0, cc.w, rt.w);
+            }
+        };
+
+        // FULL8: this thread's texel of core row j_begin in the RGBA8 atlas
+        uint32_t* const orow = reinterpret_cast<uint32_t*>(p.out) + out_base + (size_t)j_begin * row_pitch + tid;
+        const uint32_t rp32 = (uint32_t)row_pitch;
+
+        // a8: y of block (row j, blk) in slot s -> page cache
+        auto output = [&](int j, int blk, int s) {
+            const int i = blk * kThreads + tid;
+            uint32_t yv[4];
+            ptx::tmem_ld_x4(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, yv);
+            ptx::tmem_wait_ld();
+            const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
+            if constexpr (FULL8) {
+                orow[(size_t)((uint32_t)(j - j_begin) * rp32) + blk * kThreads] = rgba8_fma(y0f, y1f, y2f);
+                return;
+            }
+            // decode_tiles: core texel (j, i) and its mirrored border copies
+            // (R3): core i -> padded-core offsets -i (1 <= i <= B) and 2(C-1)-i
+            // (C-1-B <= i <= C-2) -- both when 2B > C-2; rows likewise
+            // (CTA-uniform)
+            auto scatter = [&](auto put) {
+                const bool xl = B > 0 && i >= 1 && i <= B, xr = B > 0 && i >= C - 1 - B && i <= C - 2;
+                const int xm1 = -i, xm2 = 2 * (C - 1) - i;
+                auto row = [&](int y) {
+                    put(y, i);
+                    if (xl) put(y, xm1);
+                    if (xr) put(y, xm2);
+                };
+                row(j);
+                if (B > 0 && j >= 1 && j <= B) row(-j);
+                if (B > 0 && j >= C - 1 - B && j <= C - 2) row(2 * (C - 1) - j);
+            };
+            if constexpr (TILES8) {
+                // slot-relative 32-bit offsets
+                const uint32_t v = rgba8_fma(y0f, y1f, y2f);
+                uint32_t* const tb = reinterpret_cast<uint32_t*>(p.out) + out_base;
+                const int P_ = (int)rp32;
+                scatter([&](int y, int x) { tb[y * P_ + x] = v; });
+                return;
+            }
+            const ptrdiff_t base = (ptrdiff_t)out_base, rp = (ptrdiff_t)row_pitch;
+            if (!tiles_border) {
+                store_texel(p.out, (size_t)(base + (ptrdiff_t)j * rp + i), out_fmt, y0f, y1f, y2f);
+                return;
+            }
+            if (out_fmt == OUT_RGBA8) {
+                const uint32_t v = rgba8_fma(y0f, y1f, y2f);
+                uint32_t* out = reinterpret_cast<uint32_t*>(p.out);
+                scatter([&](int y, int x) { out[base + y * rp + x] = v; });
+                return;
+            }
+            scatter([&](int y, int x) { store_texel(p.out, (size_t)(base + y * rp + x), out_fmt, y0f, y1f, y2f); });
+        };
+
+        auto epilogues = [&]() {
+#if NDGI_JOINT_EPI
+            if constexpr (H == 16) {
+#if NDGI_F16ACC
+                gelu_epilogue_h16_f16acc<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
+#else
+                gelu_epilogue_h16<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
+#endif
+                return;
+            }
+#endif
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);
+        };
+
+        // S items per step; item n = (row j_begin + n / BPR, block n % BPR)
+        // strips are whole F_uv chunks, or (small batches) 4..8-row strips
+        const int crows = p.strip_rows < chunk_rows ? p.strip_rows : chunk_rows;
+        const int chunk_items = crows * BPR;
+        for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
+        if constexpr (WIN) stage_window(j_begin + c0 / BPR, crows);   // uses the F_uv chunk buffer as scratch
+        if (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) decode_chunk(j_begin + c0 / BPR, crows);
+        for (int it = c0; it < c0 + chunk_items; it += S) {
+            if constexpr (BPR == 1 && S == 2) {
+                gather_rows2(j_begin + it, it - c0);
+            } else {
+#pragma unroll
+                for (int s = 0; s < S; ++s) gather(j_begin + (it + s) / BPR, (it + s - c0) / BPR, (it + s) % BPR, s);
+            }
+            run_layer(L0{});
+            epilogues();
+            run_layer(L1{});
+            epilogues();
+            run_layer(L2{});
+#pragma unroll
+            for (int s = 0; s < S; ++s) output(j_begin + (it + s) / BPR, (it + s) % BPR, s);
+        }
+        }
+    }
+
+    // ---- teardown --------------------------------------------------------------------
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<Cfg::TM_COLS>(tmem);
+}
+
+// ---- host-side launch helpers ---------------------------------------------------
+// Launch configuration of one kernel instantiation on one device for one smem
+// size: computed once (attribute calls cost microseconds, which a small VT
+// batch would otherwise pay on every call).
+struct LaunchCfg {
+    const void* kern;
+    int dev;
+    uint32_t smem;
+    int occ;
+};
+
+template <typename K>
+static cudaError_t fused_launch_cfg(K kern, uint32_t smem, int tmem_cols, int& occ_out) {
+    static std::mutex mu;
+    static std::vector<LaunchCfg> cache;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    // the dynamic-smem limit is per-kernel state: keep it at the largest size
+    // this kernel has been configured for (a smaller later setting would make
+    // a cached larger configuration fail to launch)
+    uint32_t attr = smem;
+    for (const LaunchCfg& c : cache) {
+        if (c.kern != reinterpret_cast<const void*>(kern) || c.dev != dev) continue;
+        if (c.smem == smem) {
+            occ_out = c.occ;
+            return cudaSuccess;
+        }
+        if (c.smem > attr) attr = c.smem;
+    }
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attr);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    // Resident CTAs per SM from the kernel's own resource use (the runtime's
+    // occupancy query reports 1 for tcgen05 kernels on driver 580).
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    int smem_sm = 0, regs_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    const int regs_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (kThreads / 32);   // per-warp allocation unit 256
+    const int smem_cta = (int)smem + (int)fa.sharedSizeBytes + 1024;   // + per-CTA reserved smem
+    int occ = regs_sm / regs_cta;
+    if (smem_sm / smem_cta < occ) occ = smem_sm / smem_cta;
+    const int tmem_cap = 512 / tmem_cols;
+    if (occ > tmem_cap) occ = tmem_cap;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (getenv("NDGI_VERBOSE"))
+        fprintf(stderr, "[ndgi] fused launch cfg: occ=%d (regs %d, local %zu) smem=%u\n", occ, fa.numRegs,
+                fa.localSizeBytes, smem);
+    cache.push_back(LaunchCfg{reinterpret_cast<const void*>(kern), dev, smem, occ});
+    occ_out = occ;
+    return cudaSuccess;
+}
+
+template <int H, int FMT_UV, int CT>
+cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
+    const FusedSmem L = fused_smem_layout<H>(CT, p.R3);
+    const bool full8 = p.full && p.out_fmt == OUT_RGBA8;
+    // windowed F_uvt when the whole slice would cost residency (h = 16, C = 128)
+    constexpr bool kWinOk = H == 16 && CT == 128;
+    const bool win = kWinOk && p.R3 > 32;
+    uint32_t smem = L.total;
+    if (win) smem = L.uvt + 4u * uvt_window(p.R3, CT, kChunkTexels / CT).bytes;
+    const bool tiles8 = !p.full && p.out_fmt == OUT_RGBA8;
+    auto pick = [&](auto ok, auto w) {
+        return ndgi_fused_kernel<H, FMT_UV, CT, decltype(ok)::value, decltype(w)::value && kWinOk>;
+    };
+    using K0 = std::integral_constant<int, 0>;
+    using K1 = std::integral_constant<int, 1>;
+    using K2 = std::integral_constant<int, 2>;
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    auto kern = full8 ? (win ? pick(K1{}, T_{}) : pick(K1{}, F_{}))
+                      : tiles8 ? (win ? pick(K2{}, T_{}) : pick(K2{}, F_{}))
+                               : (win ? pick(K0{}, T_{}) : pick(K0{}, F_{}));
+    int occ = 0;
+    cudaError_t e = fused_launch_cfg(kern, smem, FusedCfg<H>::TM_COLS, occ);
+    if (e != cudaSuccess) return e;
+    const uint32_t cap = (uint32_t)(num_sms * occ);
+    const uint32_t grid = p.units < cap ? p.units : cap;
+    kern<<<grid, kThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace ndgi

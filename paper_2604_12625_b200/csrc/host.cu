@@ -17,9 +17,6 @@
 namespace ndgi {
 cudaError_t launch_ref(const KParams& p, cudaStream_t stream);
 cudaError_t launch_fused(const KParams& p, int num_sms, cudaStream_t s);
-cudaError_t launch_fused_ws(const KParams& p, int num_sms, cudaStream_t s);
-cudaError_t launch_fused_hmma(const KParams& p, int num_sms, cudaStream_t s);
-cudaError_t launch_fused_pipe(const KParams& p, int num_sms, cudaStream_t s);
 int fused_ctas_per_sm(int H);
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_bc7_encode_mode6(const void* rgba, int w, int h, void* blocks, int num_sms, cudaStream_t s);
@@ -44,10 +41,12 @@ cudaError_t prep_weights(const uint16_t* mlp, size_t tile_elems, int H, int fmt_
                          cudaStream_t s);
 cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba, cudaStream_t s);
 cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
-cudaError_t gelu_rate(uint32_t iters, float* ms, double* acts);
+cudaError_t gelu_rate(uint32_t iters, uint32_t mufu_pairs, int pack, float* ms, double* acts);
+int fused_gelu_mufu_pairs(int H);
+cudaError_t null_launch(cudaStream_t s);
+int fused_f16acc();
 cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter);
 cudaError_t tmem_f16_probe(uint32_t* host_out);
-int fused_prof_read(unsigned long long* out8, int reset);
 }  // namespace ndgi
 
 struct ndgi_ctx {
@@ -62,7 +61,9 @@ struct ndgi_ctx {
     bool tex_ready;
     cudaArray_t uvarr[ndgi::kMaxTexAtlases];
     unsigned long long uvtex[ndgi::kMaxTexAtlases];
-    // host-buffer path
+    // host-buffer path (ndgi_decode_full_host): staging buffers and streams
+    // shared by every caller of the context, so the whole call holds host_mu
+    std::mutex host_mu;
     cudaStream_t hstream[2];
     cudaEvent_t hevent[2];
     void* stage[2];
@@ -214,11 +215,6 @@ void choose_strips(ndgi::KParams& p, int num_sms, int min_rows) {
         const uint64_t target = 2ull * num_sms * ndgi::fused_ctas_per_sm(p.H);
         while (s < max_strips && req * s < target) s *= 2;
     }
-    static const int forced = [] {   // experiments: NDGI_STRIPS=<power of 2>
-        const char* v = getenv("NDGI_STRIPS");
-        return v ? atoi(v) : 0;
-    }();
-    if (forced > 0) s = forced < max_strips ? forced : max_strips;
     p.strips_per_tile = s;
     p.strip_rows = C / s;
     p.units = (uint32_t)((uint64_t)p.nt * p.n_req * s);
@@ -250,21 +246,8 @@ ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t
         e = ndgi::launch_fused(p, ctx->num_sms, s);
     } else if (mode == NDGI_MODE_FAST) {
         if (!fast) return fail(NDGI_ERR_UNSUPPORTED, "layout not supported by NDGI_MODE_FAST (see ndgi.h)");
-        // NDGI_KERNEL selects the measured h = 16 alternatives (DESIGN.md
-        // §6.1 schedule experiments): ws, hmma, pipe
-        static const int variant = [] {
-            const char* v = getenv("NDGI_KERNEL");
-            if (v && strcmp(v, "ws") == 0) return 1;
-            if (v && strcmp(v, "hmma") == 0) return 2;
-            if (v && strcmp(v, "pipe") == 0) return 3;
-            return 0;
-        }();
-        const bool deflt = p.H != 16 || variant == 0 || p.fmt_uv > ndgi::FMT_F16;   // variants: BC7 / U8 / F16 F_uv
-        choose_strips(p, ctx->num_sms, deflt ? 4 : 16);
-        if (deflt) e = ndgi::launch_fused(p, ctx->num_sms, s);
-        else if (variant == 1) e = ndgi::launch_fused_ws(p, ctx->num_sms, s);
-        else if (variant == 2) e = ndgi::launch_fused_hmma(p, ctx->num_sms, s);
-        else e = ndgi::launch_fused_pipe(p, ctx->num_sms, s);
+        choose_strips(p, ctx->num_sms, 4);
+        e = ndgi::launch_fused(p, ctx->num_sms, s);
     } else {
         e = ndgi::launch_ref(p, s);
     }
@@ -445,6 +428,7 @@ ndgi_status ndgi_decode_full_host(ndgi_ctx* ctx, const float* t, uint32_t n_t, v
         if (st != NDGI_OK) return st;
     }
     DeviceGuard g(ctx->device);
+    std::lock_guard<std::mutex> lock(ctx->host_mu);
     const size_t bytes = ndgi_full_texels(&ctx->L) * ndgi_texel_bytes(fmt);
     cudaError_t e;
     if (ctx->stage_bytes < bytes) {
@@ -584,6 +568,7 @@ struct ndgi_train {
     size_t dtex_stride;
     int* steps;
     uint32_t cap;                  // batch capacity of grad / loss / dtex
+    uint32_t last_n;               // batch of the last step (ndgi_train_last_grad)
 };
 
 namespace {
@@ -723,6 +708,7 @@ ndgi_status train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, cons
     a.off_vt = t->off_vt;
     a.dtex = t->dtex;
     a.dtex_stride = t->dtex_stride;
+    t->last_n = n;
     e = ndgi::launch_train_grad(a, (int)L.hidden, s);
     if (e == cudaSuccess)
         e = ndgi::launch_adam(t->theta, t->m, t->v, t->steps, t->grad, tile_ids, (int)n, t->P, (int)L.num_tiles, lr,
@@ -757,7 +743,7 @@ ndgi_status ndgi_train_full_step(ndgi_train* t, const uint32_t* tile_ids, uint32
 
 ndgi_status ndgi_train_last_grad(ndgi_train* t, float* out, uint32_t n, void* stream) {
     if (!t || !out) return fail(NDGI_ERR_ARG, "NULL argument");
-    if (n == 0 || n > t->cap) return fail(NDGI_ERR_RANGE, "n must be in [1, the last step's batch]");
+    if (n == 0 || n > t->last_n) return fail(NDGI_ERR_RANGE, "n must be in [1, the last step's batch]");
     DeviceGuard g(t->ctx->device);
     const cudaError_t e = cudaMemcpyAsync(out, t->grad, (size_t)n * t->P * 4, cudaMemcpyDeviceToDevice,
                                           static_cast<cudaStream_t>(stream));
@@ -856,10 +842,24 @@ ndgi_status ndgi_debug_bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h,
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "bc7 texture decode");
 }
 
-ndgi_status ndgi_debug_gelu_rate(uint32_t iters, float* ms, double* activations) {
+ndgi_status ndgi_debug_gelu_rate(uint32_t iters, uint32_t mufu_pairs, int pack_f32, float* ms, double* activations) {
     if (!ms || !activations || !iters) return fail(NDGI_ERR_ARG, "bad arguments");
-    cudaError_t e = ndgi::gelu_rate(iters, ms, activations);
+    if (mufu_pairs > 16) return fail(NDGI_ERR_RANGE, "mufu_pairs must be in [0, 16]");
+    cudaError_t e = ndgi::gelu_rate(iters, mufu_pairs, pack_f32, ms, activations);
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "gelu rate");
+}
+
+ndgi_status ndgi_debug_gelu_split(uint32_t hidden, uint32_t* mufu_pairs_of_16, int* fp32_acc) {
+    if (!mufu_pairs_of_16 || !fp32_acc) return fail(NDGI_ERR_ARG, "bad arguments");
+    if (hidden != 16 && hidden != 64) return fail(NDGI_ERR_UNSUPPORTED, "the fused kernel is built for h = 16 / 64");
+    *mufu_pairs_of_16 = (uint32_t)ndgi::fused_gelu_mufu_pairs((int)hidden);
+    *fp32_acc = hidden == 64 ? 1 : !ndgi::fused_f16acc();
+    return NDGI_OK;
+}
+
+ndgi_status ndgi_debug_null_launch(void* stream) {
+    const cudaError_t e = ndgi::null_launch(static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "null launch");
 }
 
 ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_iter) {
@@ -872,13 +872,6 @@ ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out) {
     if (!host_out) return fail(NDGI_ERR_ARG, "bad arguments");
     cudaError_t e = ndgi::tmem_f16_probe(host_out);
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "tmem f16 probe");
-}
-
-ndgi_status ndgi_debug_fused_profile(uint64_t* out8, int reset) {
-    if (!out8) return fail(NDGI_ERR_ARG, "bad arguments");
-    if (!ndgi::fused_prof_read(reinterpret_cast<unsigned long long*>(out8), reset))
-        return fail(NDGI_ERR_UNSUPPORTED, "built without NDGI_PROFILE");
-    return NDGI_OK;
 }
 
 }  // extern "C"
