@@ -622,18 +622,33 @@ def vt_latency(ndgi, torch, args):
         if f >= 16:
             fl.append(e0.elapsed_time(e1) * 1e3)
             fh.append((h1 - h0) * 1e6)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(65)]
+    torch.cuda._sleep(int(2e-3 * 1.9e9))
+    for f in range(64):
+        evs[f].record(stream)
+        ndgi.ndgi_debug_null_launch(stream)
+    evs[-1].record(stream)
+    evs[-1].synchronize()
+    fd = sorted(evs[f].elapsed_time(evs[f + 1]) * 1e3 for f in range(16, 64))
     res["floor"] = {"p50": statistics.median(fl), "host_call_us_p50": statistics.median(fh),
-                    "what": "empty kernel via ndgi_debug_null_launch, events around the Python call"}
+                    "device_p50": fd[len(fd) // 2],
+                    "what": "empty kernel via ndgi_debug_null_launch, events around the Python call (p50) and "
+                            "queued ahead (device_p50)"}
     for n in (8, 32, 128, 512):
         batches = S.vt_batches(lay["num_tiles"], n, 16 + 64, seed)
         cache = torch.empty((n, 136, 136, 4), dtype=torch.uint8, device="cuda")
         ids = [torch.from_numpy(b[0].astype(np.int32)).cuda() for b in batches]
+        # the render loop's buffers: one device id buffer, refilled per frame
+        # (device-to-device, outside the timed call), one bound decoder
+        idbuf = torch.empty(n, dtype=torch.int32, device="cuda")
+        dec = ndgi.TileDecoder(ctx, idbuf, None, n, cache, "rgba8", "fast", stream)
         lat, host = [], []
         for f, (b, t) in enumerate(batches):
+            idbuf.copy_(ids[f])
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             h0 = time.perf_counter()
-            ndgi.ndgi_decode_tiles(ctx, ids[f], None, n, n, t, cache, "rgba8", "fast", stream)
+            dec(n, t)
             h1 = time.perf_counter()
             e1.record(stream)
             e1.synchronize()
@@ -643,8 +658,23 @@ def vt_latency(ndgi, torch, args):
         lat.sort()
         host.sort()
         p50 = lat[len(lat) // 2]
+        # device time per batch with the host running ahead (the renderer's case):
+        # a 2 ms sleep kernel first, so every launch below is queued before the
+        # GPU reaches it; events between consecutive launches
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(batches) + 1)]
+        torch.cuda._sleep(int(2e-3 * 1.9e9))
+        for f, (b, t) in enumerate(batches):
+            evs[f].record(stream)
+            ndgi.ndgi_decode_tiles(ctx, ids[f], None, n, n, t, cache, "rgba8", "fast", stream)
+        evs[-1].record(stream)
+        evs[-1].synchronize()
+        dev = sorted(evs[f].elapsed_time(evs[f + 1]) * 1e3 for f in range(16, len(batches)))
         res[str(n)] = {"p50": p50, "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))],
-                       "gtexel_s": n * 136 * 136 / (p50 * 1e-6) / 1e9, "host_call_us_p50": host[len(host) // 2]}
+                       "gtexel_s": n * 136 * 136 / (p50 * 1e-6) / 1e9, "host_call_us_p50": host[len(host) // 2],
+                       "device_p50": dev[len(dev) // 2], "device_p99": dev[min(len(dev) - 1, int(0.99 * len(dev)))]}
+    res["how"] = ("p50/p99: events around the Python call of ndgi.TileDecoder (ndgi_decode_tiles bound to the "
+                  "render loop's fixed id/cache buffers; host enqueue inside the events); device_p50/p99: per-batch "
+                  "device time with launches queued ahead of the GPU")
     return res
 
 

@@ -191,6 +191,27 @@ def ndgi_decode_tiles(ctx: Context, tile_ids, slots, n: int, num_slots: int, t: 
     _check(st, "ndgi_decode_tiles")
 
 
+class TileDecoder:
+    """ndgi_decode_tiles bound to fixed buffers, as a render loop holds them (the
+    frame's tile ids / slots written into the same device buffers every frame):
+    the pointers, formats and stream are marshalled once, so a call passes only
+    (n, t) -- the per-frame Python cost of the VT path is one ctypes call."""
+
+    def __init__(self, ctx: Context, tile_ids, slots, num_slots: int, out_cache, fmt: str = "rgba8",
+                 mode: str = "fast", stream=None):
+        self._f = _lib.ndgi_decode_tiles
+        self._args = (ctx.handle, C.c_void_p(tile_ids.data_ptr()),
+                      C.c_void_p(slots.data_ptr()) if slots is not None else None)
+        self._tail = (C.c_void_p(out_cache.data_ptr()), OUT[fmt], MODE[mode], _stream_ptr(stream))
+        self._num_slots = int(num_slots)
+        self._keep = (ctx, tile_ids, slots, out_cache)
+
+    def __call__(self, n: int, t: float) -> None:
+        st = self._f(*self._args, n, self._num_slots, t, *self._tail)
+        if st:
+            _check(st, "ndgi_decode_tiles")
+
+
 def ndgi_decode_full(ctx: Context, t: float, out, fmt: str = "rgba8", mode: str = "fast", stream=None) -> None:
     st = _lib.ndgi_decode_full(ctx.handle, float(t), C.c_void_p(out.data_ptr()), OUT[fmt], MODE[mode],
                                _stream_ptr(stream))

@@ -44,7 +44,8 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None, de
     lib = out or LIB
     if not force and out is None and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.basename(lib).replace(".so", ""))
+    # experiment variants keep their objects outside the repo (gpurun snapshot size)
+    objdir = os.path.join(HERE, "build") if out is None else os.path.join("/tmp", "ndgi_" + os.path.basename(lib).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     extra = (["-Xptxas", "-v"] if verbose else []) + [f"-D{d}" for d in defines]
 
