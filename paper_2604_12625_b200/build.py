@@ -85,5 +85,18 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None, de
     return lib
 
 
+CHECKED_LIB = os.path.join(HERE, "libndgi_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The self-checking test build (NDGI_CHECKED: bounds checks that trap;
+    NDGI_JITTER: random per-warp delays at every synchronisation point) used
+    by tests/test_gpu_selfcheck.py in place of compute-sanitizer."""
+    if not force and os.path.exists(CHECKED_LIB) and os.path.getmtime(CHECKED_LIB) >= max(
+            os.path.getmtime(d) for d in _deps()):
+        return CHECKED_LIB
+    return build(out=CHECKED_LIB, defines=["NDGI_CHECKED=1", "NDGI_JITTER=1"])
+
+
 if __name__ == "__main__":
     print(build(verbose="--verbose" in sys.argv, force=True))

@@ -127,12 +127,19 @@ __device__ __forceinline__ uint32_t bc4_texel(uint2 w, int i) {
 
 // one 4-channel block (BC7 / BC1 / BC3) of a map at block index bi; fmt is
 // warp-uniform (bc7_decode votes across the warp)
+static __device__ __noinline__ void bcn_decode16(int fmt, const uint8_t* base, size_t bi, uint32_t* out) {
+    auto sink = [&](int i, uint32_t v) { out[i] = v; };
+    if (fmt == FMT_BC1) bc1_decode(__ldg(reinterpret_cast<const uint2*>(base) + bi), false, sink);
+    else bc3_decode(__ldg(reinterpret_cast<const uint4*>(base) + bi), sink);
+}
+
 template <class Sink>
 __device__ __forceinline__ void block4_decode(int fmt, const uint8_t* base, size_t bi, Sink&& sink) {
-    if (fmt == FMT_BC1) {
-        bc1_decode(__ldg(reinterpret_cast<const uint2*>(base) + bi), false, sink);
-    } else if (fmt == FMT_BC3) {
-        bc3_decode(__ldg(reinterpret_cast<const uint4*>(base) + bi), sink);
+    if (fmt == FMT_BC1 || fmt == FMT_BC3) {   // the other formats' decoders out of line (code size)
+        uint32_t t[16];
+        bcn_decode16(fmt, base, bi, t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sink(i, t[i]);
     } else {
         bc7_decode(__ldg(reinterpret_cast<const uint4*>(base) + bi), sink);
     }

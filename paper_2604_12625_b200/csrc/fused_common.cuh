@@ -343,6 +343,7 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                         for (int q = 0; q < 4; ++q)
                             c[q] = (omt * (float)((t0[i] >> (8 * q)) & 0xffu) + tau * (float)((t1[i] >> (8 * q)) & 0xffu)) *
                                    (1.0f / 255.0f);
+                        NDGI_CHECK((by * 4 + (i >> 2)) * R3 + bx * 4 + (i & 3) < R3 * R3);
                         sUvt[(by * 4 + (i >> 2)) * R3 + bx * 4 + (i & 3)] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
                     }
                 }
@@ -377,6 +378,7 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                 const float sx = fmaf((float)i + 0.5f, scu, -0.5f);
                 const float fl = floorf(sx), fx = sx - fl;
                 const int x0 = clampi((int)fl, 0, p.U - 1), x1 = clampi((int)fl + 1, 0, p.U - 1);
+                NDGI_CHECK(tc.r0 >= 0 && tc.r1 < p.T && tc.k0 >= 0 && tc.k1 < p.D);
                 float c[2];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {

@@ -84,6 +84,12 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
     static_assert(!WIN || CT == 128, "windowed F_uvt is built for C = 128");
     const UvtWindow win = uvt_window(R3, C, chunk_rows);
+#if NDGI_CHECKED
+    uint32_t smem_total;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(smem_total));   // bytes from the smem base
+    // output texels the launch may write: decode_full nt atlas sets, decode_tiles num_slots slots
+    const size_t out_texels = p.full ? (size_t)p.nt * p.out_t_stride : (size_t)p.num_slots * P * P;
+#endif
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
     const uint32_t tm_lane = tmem + lane_base;
 
@@ -127,12 +133,14 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         const int j_begin = strip * p.strip_rows;
 
         // ---- a2: tile parameters -> shared memory -----------------------------------
+        ndgi_jitter(1u);
         __syncthreads();  // previous unit's MMAs complete and all smem readers done
         {
             copy_prepacked_weights<H>(p, tc, k, smem, L, tid, kThreads);
             unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads, WIN ? win.pitch : 0u, win.wyb * 4);
         }
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
+        ndgi_jitter(2u);
         __syncthreads();
 
         // per-column gather constants (column i = b*128 + tid, written and read by
@@ -180,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         // F_uv texel (row, blk*128 + tid) as two f16x2 holding the integers q (R8)
         auto uv_texel = [&](int row, int jr, int blk, uint32_t& lo, uint32_t& hi) {
             if constexpr (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) {
+                NDGI_CHECK(jr >= 0 && jr * C + blk * kThreads + tid < kChunkTexels);
                 u8x4_to_h2(sUv[jr * C + blk * kThreads + tid], lo, hi);
             } else if constexpr (FMT_UV == FMT_BC7_TEX) {
                 // hardware BC7 decode returns q/255 (UNORM); x255 lands within 2^-16
@@ -223,13 +232,18 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             uint32_t rowv[4];
             auto sink = [&](int i, uint32_t v) {
                 rowv[i & 3] = v;
-                if ((i & 3) == 3 && store)
+                if ((i & 3) == 3 && store) {
+                    NDGI_CHECK((size_t)((dst + (i >> 2) * C) - sUv) + 4 <= (size_t)kChunkTexels);
                     *reinterpret_cast<uint4*>(dst + (i >> 2) * C) = make_uint4(rowv[0], rowv[1], rowv[2], rowv[3]);
+                }
             };
+            NDGI_CHECK(bidx < (size_t)(C / 4) * (C / 4));
+            ndgi_jitter(3u);
             __syncwarp();   // previous chunk fully gathered by this warp
             if constexpr (FMT_UV == FMT_BC1) bc1_decode(__ldg(reinterpret_cast<const uint2*>(uvmap) + bidx), false, sink);
             else if constexpr (FMT_UV == FMT_BC3) bc3_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
             else bc7_decode(__ldg(reinterpret_cast<const uint4*>(uvmap) + bidx), sink);
+            ndgi_jitter(6u);
             __syncwarp();
         };
 
@@ -251,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             // new block rows: [blo, bhi] minus the resident [w_lo, w_hi] (monotone strips)
             const int n0 = (w_hi >= w_lo && blo >= w_lo && blo <= w_hi) ? w_hi + 1 : blo;
             const int nnew = bhi - n0 + 1;
+            ndgi_jitter(4u);
             __syncwarp();   // this warp's gathers of the previous chunk are done
             if (nnew > 0) {
                 if (fmt_block4(p.fmt_uvt)) {
@@ -269,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                             const int gbx = wbx0 + qx < nbm ? wbx0 + qx : nbm - 1;
                             const uint8_t* src = vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0);
                             uint32_t t[16];
+                            NDGI_CHECK(br >= 0 && br < nbm && gbx >= 0 && gbx < nbm);
                             block4_decode(p.fmt_uvt, src, (size_t)br * nbm + gbx, [&](int i, uint32_t v) { t[i] = v; });
                             if (lane < 2 * ng) {
                                 // scratch slot q: 64 B at row q >> 1, byte (q & 1) * 64
@@ -277,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                                 for (int r = 0; r < 4; ++r) d[r] = make_uint4(t[4 * r], t[4 * r + 1], t[4 * r + 2], t[4 * r + 3]);
                             }
                         }
+                        ndgi_jitter(7u);
                         __syncwarp();
                         for (int e = lane; e < ng * 16; e += 32) {
                             const int pos = g0 + (e >> 4), i = e & 15;
@@ -289,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                             for (int qq = 0; qq < 4; ++qq)
                                 c[qq] = (omt * (float)((q0v >> (8 * qq)) & 0xffu) + tau * (float)((q1v >> (8 * qq)) & 0xffu)) *
                                         (1.0f / 255.0f);
+                            NDGI_CHECK((uint32_t)(((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)) * 8u < win.bytes);
                             wdst[((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)] =
                                 make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
                         }
@@ -315,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                             for (int qq = 0; qq < 4; ++qq)
                                 c[qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
                         }
+                        NDGI_CHECK((uint32_t)((gy & (4 * ring - 1)) * WX + e % WX) * 8u < win.bytes);
                         wdst[((gy & (4 * ring - 1))) * WX + e % WX] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
                     }
                 }
@@ -374,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         auto gather = [&](int row, int jr, int blk, int s) {
             const uint4 rt = sRow[row];                  // y0 row byte offset, y1 row byte offset, fy, V_vt
             const uint4 cc = sCol[blk * kThreads + tid]; // x0, x1 byte offsets (from smem base), fx, V_ut
+            NDGI_CHECK(row >= 0 && row < C && rt.x + cc.x >= L.uvt && rt.y + cc.y + 8u <= smem_total);
             const uint2 t00 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.x);
             const uint2 t10 = *reinterpret_cast<const uint2*>(wbase + rt.x + cc.y);
             const uint2 t01 = *reinterpret_cast<const uint2*>(wbase + rt.y + cc.x);
@@ -388,7 +408,9 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         auto gather_rows2 = [&](int row, int jr) {
             const uint4 rt0 = sRow[row], rt1 = sRow[row + 1];
             const uint4 cc = sCol[tid];
+            NDGI_CHECK(row >= 0 && row + 1 < C);
             auto xlerp = [&](uint32_t yoff, uint32_t& lo, uint32_t& hi) {
+                NDGI_CHECK(yoff + cc.x >= L.uvt && yoff + cc.y + 8u <= smem_total);
                 const uint2 a = *reinterpret_cast<const uint2*>(wbase + yoff + cc.x);
                 const uint2 b = *reinterpret_cast<const uint2*>(wbase + yoff + cc.y);
                 lo = hlerp2(a.x, b.x, cc.z);
@@ -420,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             ptx::tmem_wait_ld();
             const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
             if constexpr (FULL8) {
+                NDGI_CHECK(out_base + (size_t)j * row_pitch + i < out_texels);
                 orow[(size_t)((uint32_t)(j - j_begin) * rp32) + blk * kThreads] = rgba8_fma(y0f, y1f, y2f);
                 return;
             }
@@ -444,7 +467,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 const uint32_t v = rgba8_fma(y0f, y1f, y2f);
                 uint32_t* const tb = reinterpret_cast<uint32_t*>(p.out) + out_base;
                 const int P_ = (int)rp32;
-                scatter([&](int y, int x) { tb[y * P_ + x] = v; });
+                scatter([&](int y, int x) {
+                    NDGI_CHECK(y + B >= 0 && y + B < P_ && x + B >= 0 && x + B < P_);
+                    tb[y * P_ + x] = v;
+                });
                 return;
             }
             const ptrdiff_t base = (ptrdiff_t)out_base, rp = (ptrdiff_t)row_pitch;
@@ -455,7 +481,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             if (out_fmt == OUT_RGBA8) {
                 const uint32_t v = rgba8_fma(y0f, y1f, y2f);
                 uint32_t* out = reinterpret_cast<uint32_t*>(p.out);
-                scatter([&](int y, int x) { out[base + y * rp + x] = v; });
+                scatter([&](int y, int x) {
+                    NDGI_CHECK(y + B >= 0 && y + B < (int)rp && x + B >= 0 && x + B < (int)rp);
+                    out[base + y * rp + x] = v;
+                });
                 return;
             }
             scatter([&](int y, int x) { store_texel(p.out, (size_t)(base + y * rp + x), out_fmt, y0f, y1f, y2f); });

@@ -104,6 +104,37 @@ struct TrainArgs {
 
 __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
+// ---- self-checking builds (compute-sanitizer is not available on this pool) --
+// NDGI_CHECKED=1: every shared-memory index and every global read / write
+// offset of the fused kernel is checked against its buffer; a violation traps
+// (the launch then fails with cudaErrorLaunchFailure / illegal instruction).
+// NDGI_JITTER=1: pseudo-random per-warp delays (0..~2 us) at every
+// synchronisation point, so a missing barrier or an aliasing race shows up as
+// a nondeterministic output; tests require bit-equality with the product build.
+#ifndef NDGI_CHECKED
+#define NDGI_CHECKED 0
+#endif
+#ifndef NDGI_JITTER
+#define NDGI_JITTER 0
+#endif
+#if NDGI_CHECKED
+#define NDGI_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define NDGI_CHECK(cond) do {} while (0)
+#endif
+__device__ __forceinline__ void ndgi_jitter(uint32_t salt) {
+#if NDGI_JITTER
+    uint32_t h = (uint32_t)clock() * 0x9E3779B1u ^ (salt * 0x85EBCA6Bu) ^ ((threadIdx.x >> 5) * 0xC2B2AE35u) ^
+                 (blockIdx.x * 0x27D4EB2Fu);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if (h & 1u) __nanosleep(h >> 21);   // 0 .. ~2 us
+#else
+    (void)salt;
+#endif
+}
+
 __device__ __forceinline__ float half_bits_to_float(uint16_t h) {
     return __half2float(__ushort_as_half(h));
 }

@@ -2,7 +2,7 @@
 BC3 / BC1 with BC5 line maps (R29), u8, f16) on config 2's
 atlas (1,024 tiles), decode_full at 24 times per call, RGBA8.  For every cell:
 written Gtexel/s, kernel ms, the ALU roofline fraction (2h GELU activations per
-texel against the measured GELU rate), the HBM fraction of the algorithmic bytes,
+texel against the measured rate of the kernel's own GELU epilogue), the HBM fraction of the algorithmic bytes,
 and sampled parity against the C oracle.  Prints one JSON object.
 
     python scripts/sweep.py [--steps K]
@@ -30,10 +30,17 @@ import torch  # noqa: E402
 import paper_2604_12625_b200 as ndgi  # noqa: E402
 
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-ms_g, acts = ndgi.ndgi_debug_gelu_rate(4096)
-r_gelu = acts / (ms_g * 1e-3)
+def gelu_roof(h):
+    """measured rate of the kernel's own GELU epilogue (its MUFU / FMA split, packing)"""
+    m, fp32 = ndgi.ndgi_debug_gelu_split(h)
+    ms_g, acts = ndgi.ndgi_debug_gelu_rate(2048, m, fp32)
+    return acts / (ms_g * 1e-3), m
+
+
+ROOF = {h: gelu_roof(h) for h in (16, 64)}
 TS = [i / 24 for i in range(24)]
-out = {"gelu_rate_act_per_s": r_gelu, "cells": []}
+out = {"gelu_rate_act_per_s": {str(h): r for h, (r, _) in ROOF.items()},
+       "gelu_mufu_pairs_of_16": {str(h): m for h, (_, m) in ROOF.items()}, "cells": []}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for prof in ("L", "M", "H", "M64"):
     for fmt in ("bc7", "bc3", "bc1", "u8", "f16"):
@@ -82,7 +89,7 @@ for prof in ("L", "M", "H", "M64"):
                   + 2 * 2 * row_b + 2 * (16 * h + h + h * h + h + 3 * h + 3))
         alg_bytes = 24 * 1024 * (read_t + 128 * 128 * 4)
         cell = {"profile": prof, "fmt": fmt, "hidden": h, "gtexel_s": texels / (kms * 1e-3) / 1e9, "ms_per_24t": kms,
-                "alu_frac": texels * 2 * h / (kms * 1e-3) / r_gelu,
+                "alu_frac": texels * 2 * h / (kms * 1e-3) / ROOF[h][0],
                 "hbm_frac": alg_bytes / (kms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                 "parity_max_abs": float(errs.max()), "parity_mean_abs": float(errs.mean()),
                 "theta_bytes_per_tile": theta_t}
