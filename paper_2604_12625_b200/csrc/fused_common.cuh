@@ -341,7 +341,7 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                         float c[4];
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
-                            c[q] = (omt * (float)((t0[i] >> (8 * q)) & 0xffu) + tau * (float)((t1[i] >> (8 * q)) & 0xffu)) *
+                            c[q] = (omt * u8f(t0[i], q) + tau * u8f(t1[i], q)) *
                                    (1.0f / 255.0f);
                         NDGI_CHECK((by * 4 + (i >> 2)) * R3 + bx * 4 + (i & 3) < R3 * R3);
                         sUvt[(by * 4 + (i >> 2)) * R3 + bx * 4 + (i & 3)] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
@@ -356,7 +356,7 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                         const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + e);
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
-                            c[q] = (omt * (float)((q0 >> (8 * q)) & 0xffu) + tau * (float)((q1 >> (8 * q)) & 0xffu)) * (1.0f / 255.0f);
+                            c[q] = (omt * u8f(q0, q) + tau * u8f(q1, q)) * (1.0f / 255.0f);
                     } else {
                         const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * e;
                         const uint16_t* h1 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k1) + 4 * e;
@@ -384,15 +384,15 @@ __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc
                 for (int q = 0; q < 2; ++q) {
                     float v00, v10, v01, v11;
                     if (p.fmt_line == FMT_U8) {
-                        v00 = (float)__ldg(m + (tc.r0 * p.U + x0) * 2 + q);
-                        v10 = (float)__ldg(m + (tc.r0 * p.U + x1) * 2 + q);
-                        v01 = (float)__ldg(m + (tc.r1 * p.U + x0) * 2 + q);
-                        v11 = (float)__ldg(m + (tc.r1 * p.U + x1) * 2 + q);
+                        v00 = u8f(__ldg(m + (tc.r0 * p.U + x0) * 2 + q), 0);
+                        v10 = u8f(__ldg(m + (tc.r0 * p.U + x1) * 2 + q), 0);
+                        v01 = u8f(__ldg(m + (tc.r1 * p.U + x0) * 2 + q), 0);
+                        v11 = u8f(__ldg(m + (tc.r1 * p.U + x1) * 2 + q), 0);
                     } else if (p.fmt_line == FMT_BC5) {
-                        v00 = (float)((bc5_texel_at(m, p.U, x0, tc.r0) >> (8 * q)) & 0xffu);
-                        v10 = (float)((bc5_texel_at(m, p.U, x1, tc.r0) >> (8 * q)) & 0xffu);
-                        v01 = (float)((bc5_texel_at(m, p.U, x0, tc.r1) >> (8 * q)) & 0xffu);
-                        v11 = (float)((bc5_texel_at(m, p.U, x1, tc.r1) >> (8 * q)) & 0xffu);
+                        v00 = u8f(bc5_texel_at(m, p.U, x0, tc.r0), q);
+                        v10 = u8f(bc5_texel_at(m, p.U, x1, tc.r0), q);
+                        v01 = u8f(bc5_texel_at(m, p.U, x0, tc.r1), q);
+                        v11 = u8f(bc5_texel_at(m, p.U, x1, tc.r1), q);
                     } else {
                         const uint16_t* mh = reinterpret_cast<const uint16_t*>(m);
                         v00 = half_bits_to_float(__ldg(mh + (tc.r0 * p.U + x0) * 2 + q));

@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                             float c[4];
 #pragma unroll
                             for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = (omt * (float)((q0v >> (8 * qq)) & 0xffu) + tau * (float)((q1v >> (8 * qq)) & 0xffu)) *
+                                c[qq] = (omt * u8f(q0v, qq) + tau * u8f(q1v, qq)) *
                                         (1.0f / 255.0f);
                             NDGI_CHECK((uint32_t)(((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)) * 8u < win.bytes);
                             wdst[((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)] =
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                             const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + g);
 #pragma unroll
                             for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = (omt * (float)((q0 >> (8 * qq)) & 0xffu) + tau * (float)((q1 >> (8 * qq)) & 0xffu)) *
+                                c[qq] = (omt * u8f(q0, qq) + tau * u8f(q1, qq)) *
                                         (1.0f / 255.0f);
                         } else {
                             const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * g;

@@ -139,6 +139,12 @@ __device__ __forceinline__ float half_bits_to_float(uint16_t h) {
     return __half2float(__ushort_as_half(h));
 }
 
+// byte c of `word` as an exact fp32 without I2F (which issues on the XU/MUFU
+// pipe the GELUs saturate): the bits 0x4B0000qq are 2^23 + q, minus 2^23
+__device__ __forceinline__ float u8f(uint32_t word, int c) {
+    return __int_as_float(__byte_perm(word, 0x4B000000u, 0x7540u | (uint32_t)c)) - 8388608.0f;
+}
+
 // mirror a core coordinate, reflect without repeating the edge (R3)
 __device__ __forceinline__ int mirror_core(int i, int C) {
     if (i < 0) i = -i;
