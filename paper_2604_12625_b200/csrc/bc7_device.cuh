@@ -243,32 +243,45 @@ __device__ __forceinline__ void bc7_decode_generic(uint4 raw, Sink&& sink) {
 // IMAD per channel pair.  The 4-bit weights round(64 i / 15) are
 // 4 i + ((i + 2) >> 2) (exact for i = 0..15), evaluated for four texels at
 // once on bytes.
-template <class Sink>
-__device__ __forceinline__ void bc7_decode_mode6(uint4 raw, Sink&& sink) {
-    const uint64_t lo = (uint64_t)raw.x | ((uint64_t)raw.y << 32);
-    const uint32_t p0 = raw.y >> 31, p1 = raw.z & 1u;
-    auto f = [&](int k) { return (uint32_t)(lo >> (7 + 7 * k)) & 0x7fu; };
-    const uint32_t rb0 = ((f(0) << 1) | p0) | (((f(4) << 1) | p0) << 16);
-    const uint32_t rb1 = ((f(1) << 1) | p1) | (((f(5) << 1) | p1) << 16);
-    const uint32_t ga0 = ((f(2) << 1) | p0) | (((f(6) << 1) | p0) << 16);
-    const uint32_t ga1 = ((f(3) << 1) | p1) | (((f(7) << 1) | p1) << 16);
-    const uint32_t drb = rb1 - rb0, dga = ga1 - ga0;
-    const uint32_t erb = (rb0 << 6) + 0x00200020u, ega = (ga0 << 6) + 0x00200020u;
-    // texel i's index: bits 64 + 4i (i >= 1); texel 0: 3 bits at 65 (anchor)
-    const uint32_t iw0 = (raw.z & ~0xfu) | ((raw.z >> 1) & 7u), iw1 = raw.w;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        // indices of texels 4g .. 4g+3 -> bytes, then their weights
+struct Bc7Mode6 {
+    uint32_t drb, dga, erb, ega, iw0, iw1;
+    __device__ __forceinline__ explicit Bc7Mode6(uint4 raw) {
+        const uint64_t lo = (uint64_t)raw.x | ((uint64_t)raw.y << 32);
+        const uint32_t p0 = raw.y >> 31, p1 = raw.z & 1u;
+        auto f = [&](int k) { return (uint32_t)(lo >> (7 + 7 * k)) & 0x7fu; };
+        const uint32_t rb0 = ((f(0) << 1) | p0) | (((f(4) << 1) | p0) << 16);
+        const uint32_t rb1 = ((f(1) << 1) | p1) | (((f(5) << 1) | p1) << 16);
+        const uint32_t ga0 = ((f(2) << 1) | p0) | (((f(6) << 1) | p0) << 16);
+        const uint32_t ga1 = ((f(3) << 1) | p1) | (((f(7) << 1) | p1) << 16);
+        drb = rb1 - rb0;
+        dga = ga1 - ga0;
+        erb = (rb0 << 6) + 0x00200020u;
+        ega = (ga0 << 6) + 0x00200020u;
+        // texel i's index: bits 64 + 4i (i >= 1); texel 0: 3 bits at 65 (anchor)
+        iw0 = (raw.z & ~0xfu) | ((raw.z >> 1) & 7u);
+        iw1 = raw.w;
+    }
+    // texels 4g .. 4g+3 (block row g) as packed RGBA8
+    template <class Sink>
+    __device__ __forceinline__ void row(int g, Sink&& sink) const {
         const uint32_t nib = (g < 2 ? iw0 : iw1) >> (16 * (g & 1));
+        // indices -> bytes, then their weights
         const uint32_t ib = __byte_perm(nib & 0x0f0fu, (nib >> 4) & 0x0f0fu, 0x5140u);
         const uint32_t wb = (ib << 2) + (((ib + 0x02020202u) >> 2) & 0x3f3f3f3fu);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const uint32_t w = (wb >> (8 * k)) & 0xffu;
             const uint32_t vrb = w * drb + erb, vga = w * dga + ega;
-            sink(4 * g + k, ((vrb >> 6) & 0x00ff00ffu) | ((vga << 2) & 0xff00ff00u));
+            sink(k, ((vrb >> 6) & 0x00ff00ffu) | ((vga << 2) & 0xff00ff00u));
         }
     }
+};
+
+template <class Sink>
+__device__ __forceinline__ void bc7_decode_mode6(uint4 raw, Sink&& sink) {
+    const Bc7Mode6 m(raw);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) m.row(g, [&](int k, uint32_t v) { sink(4 * g + k, v); });
 }
 
 __device__ __forceinline__ bool bc7_is_mode6(uint4 raw) { return (raw.x & 0x7fu) == 0x40u; }
@@ -296,6 +309,18 @@ __device__ __forceinline__ void bc7_decode(uint4 raw, Sink&& sink) {
         bc7_decode_generic16(raw, t);
 #pragma unroll
         for (int i = 0; i < 16; ++i) sink(i, t[i]);
+    }
+}
+
+// Row r (texels 4r .. 4r+3) of one block: the mode-6 path when every active
+// lane holds mode 6, else the full decode
+__device__ __forceinline__ void bc7_decode_row(uint4 raw, int r, uint32_t (&out)[4]) {
+    if (__all_sync(__activemask(), bc7_is_mode6(raw))) {
+        Bc7Mode6(raw).row(r, [&](int k, uint32_t v) { out[k] = v; });
+    } else {
+        bc7_decode_generic(raw, [&](int i, uint32_t v) {
+            if ((i >> 2) == r) out[i & 3] = v;
+        });
     }
 }
 

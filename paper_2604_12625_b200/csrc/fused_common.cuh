@@ -207,21 +207,24 @@ __device__ __forceinline__ void gelu_epilogue2_h16(uint32_t d0, uint32_t a0, uin
     ptx::tmem_st_x8(a1, h);
 }
 
-// ---- windowed F_uvt (large R3, C = 128): per-warp window of the tau-blended
-// slice covering the F_uvt texels one F_uv chunk of this warp's 32 columns
-// can touch.  wxb / wyb = window width / height in 4x4 blocks (margin 2 for
-// the bilinear neighbour and block misalignment).
-struct UvtWindow {
-    int wxb, wyb;
-    uint32_t pitch, bytes;   // bytes per window row, per warp window
+// ---- F_uvt ring (large R3, C = 128): instead of the whole tau-blended slice
+// (R3^2 x 8 B = 32 KB for the H profile, which would halve residency), the CTA
+// keeps a ring of `rows` F_uvt rows (all R3 columns; row y in ring row
+// y mod rows) covering the rows one F_uv chunk samples, and stages the new
+// block rows at each chunk start with all 128 threads (one block row of one
+// 4x4 block of both slices per thread).
+struct UvtRing {
+    int rows;          // ring rows: a power of two, 4 x the block rows a chunk can span
+    uint32_t pitch;    // bytes per ring row (R3 x f16x4)
+    uint32_t bytes;
 };
-__host__ __device__ inline UvtWindow uvt_window(int R3, int C, int chunk_rows) {
-    UvtWindow w;
-    w.wxb = (32 * R3 / C) / 4 + 2;
-    w.wyb = (chunk_rows * R3 / C) / 4 + 2;
-    while (w.wyb & (w.wyb - 1)) ++w.wyb;   // ring of a power-of-two number of block rows
-    w.pitch = (uint32_t)w.wxb * 4u * 8u;
-    w.bytes = (uint32_t)w.wyb * 4u * w.pitch;
+__host__ __device__ inline UvtRing uvt_ring(int R3, int C, int chunk_rows) {
+    UvtRing w;
+    int brows = (chunk_rows * R3 / C + 2 + 3) / 4 + 1;   // F_uvt rows of a chunk (+ bilinear, misalignment)
+    while (brows & (brows - 1)) ++brows;
+    w.rows = 4 * brows;
+    w.pitch = (uint32_t)R3 * 8u;
+    w.bytes = (uint32_t)w.rows * w.pitch;
     return w;
 }
 
@@ -310,8 +313,8 @@ __device__ __forceinline__ void copy_prepacked_weights(const KParams& p, const T
 // (the MLP's B operands come prepacked: copy_prepacked_weights).
 // Executed by threads tid = 0 .. nthr-1 of the CTA.
 // win_pitch == 0: the whole tau-blended F_uvt slice goes to smem (row offsets
-// y * R3 * 8); > 0: the kernel stages per-warp ring windows of win_rows (a
-// power of two) F_uvt rows itself and the row table holds ring-row offsets
+// y * R3 * 8); > 0: the kernel stages a ring of win_rows (a power of two)
+// F_uvt rows itself (UvtRing) and the row table holds ring-row offsets
 template <int H, int FMT_UV, int C>
 __device__ __forceinline__ void unit_prologue(const KParams& p, const TConst& tc, int k, uint8_t* smem,
                                               const FusedSmem& L, int tid, int nthr, uint32_t win_pitch = 0,

@@ -45,8 +45,8 @@ constexpr int kThreads = 128;
 
 // FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
 // no format switch, row pointers instead of 64-bit index arithmetic
-// WIN: F_uvt staged per chunk in per-warp windows instead of the whole slice
-// (large R3: the H profile's 32 KB slice would halve residency)
+// WIN: F_uvt staged per chunk into a ring of rows (UvtRing) instead of the
+// whole slice (large R3: the H profile's 32 KB slice would halve residency)
 // OUTK: 0 any format / addressing, 1 (FULL8) decode_full RGBA8, 2 (TILES8)
 // decode_tiles RGBA8 (core + mirrored border with 32-bit offsets from the slot)
 template <int H, int FMT_UV, int CT, int OUTK, bool WIN>
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     const int B = p.B, P = p.P, R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
     static_assert(!WIN || CT == 128, "windowed F_uvt is built for C = 128");
-    const UvtWindow win = uvt_window(R3, C, chunk_rows);
+    const UvtRing ring = uvt_ring(R3, C, chunk_rows);   // WIN: the F_uvt ring
 #if NDGI_CHECKED
     uint32_t smem_total;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(smem_total));   // bytes from the smem base
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         __syncthreads();  // previous unit's MMAs complete and all smem readers done
         {
             copy_prepacked_weights<H>(p, tc, k, smem, L, tid, kThreads);
-            unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads, WIN ? win.pitch : 0u, win.wyb * 4);
+            unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads, WIN ? ring.pitch : 0u, ring.rows);
         }
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
         ndgi_jitter(2u);
@@ -153,25 +153,14 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const float sx = fmaf((float)i + 0.5f, sc3, -0.5f);
             const float flx = floorf(sx);
             const int x0 = clampi((int)flx, 0, R3 - 1), x1 = clampi((int)flx + 1, 0, R3 - 1);
-            if constexpr (WIN) {
-                // this warp's window starts at the block column of its lane 0
-                const int wx0 = __shfl_sync(0xffffffffu, x0, 0) & ~3;
-                const uint32_t wb = L.uvt + (uint32_t)warp * win.bytes;
-                sCol[i] = make_uint4(wb + (uint32_t)(x0 - wx0) * 8u, wb + (uint32_t)(x1 - wx0) * 8u,
-                                     pack_f16x2(sx - flx, sx - flx), sUt[i]);
-            } else {
-                sCol[i] = make_uint4(L.uvt + (uint32_t)x0 * 8u, L.uvt + (uint32_t)x1 * 8u, pack_f16x2(sx - flx, sx - flx),
-                                     sUt[i]);
-            }
+            sCol[i] = make_uint4(L.uvt + (uint32_t)x0 * 8u, L.uvt + (uint32_t)x1 * 8u, pack_f16x2(sx - flx, sx - flx),
+                                 sUt[i]);
         }
         if constexpr (BPR == 1) {   // V_ut of this thread's column: constant over the unit
 #pragma unroll
             for (int s = 0; s < S; ++s) ptx::tmem_st_x1(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A1 + 1, sUt[tid]);
         }
-        // WIN: window block column of this warp (lane 0's first x tap)
-        const int wbx0 = WIN ? (__shfl_sync(0xffffffffu, clampi((int)floorf(fmaf((float)tid + 0.5f, sc3, -0.5f)), 0, R3 - 1), 0) >> 2) : 0;
         const uint8_t* const wbase = smem;   // F_uvt taps: row offsets are ring rows (WIN) or slice rows
-        (void)wbx0;
         const uint8_t* uvmap = p.uv + p.uv_tile_bytes * k;
         // decoded F_uv chunk, row-major [chunk_rows][C] RGBA8 (each warp decodes
         // the blocks of its own 32 columns)
@@ -247,105 +236,103 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             __syncwarp();
         };
 
-        // WIN: this warp's ring window of the tau-blended F_uvt slice: wyb*4
-        // (a power of two) F_uvt rows x wxb*4 columns, F_uvt row y in ring row
-        // y mod (wyb*4); per chunk only the block rows not yet resident are
-        // decoded (same blend arithmetic as unit_prologue, so bit-identical to
-        // the whole-slice path)
+        // WIN: the CTA's F_uvt ring (UvtRing): at each chunk start the block rows
+        // the chunk samples that are not yet resident are decoded and tau-blended
+        // into ring rows y mod ring.rows by all 128 threads -- one (block row of
+        // a 4x4 block, both slices) per thread per round, the same blend
+        // arithmetic as unit_prologue's whole slice
         int w_lo = 1, w_hi = 0;   // resident block rows [w_lo, w_hi] (empty)
-        auto stage_window = [&](int jc, int nrows) {
+        auto stage_ring = [&](int jc, int nrows) {
             const int ymin = clampi((int)floorf(fmaf((float)jc + 0.5f, sc3, -0.5f)), 0, R3 - 1);
             const int ymax = clampi((int)floorf(fmaf((float)(jc + nrows - 1) + 0.5f, sc3, -0.5f)) + 1, 0, R3 - 1);
             const int blo = ymin >> 2, bhi = ymax >> 2;
-            const int nbm = R3 >> 2, ring = win.wyb;
-            const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
-            const float tau = tc.tau, omt = 1.0f - tau;
-            uint2* wdst = reinterpret_cast<uint2*>(smem + L.uvt + (uint32_t)warp * win.bytes);
-            const int WX = win.wxb * 4;
             // new block rows: [blo, bhi] minus the resident [w_lo, w_hi] (monotone strips)
             const int n0 = (w_hi >= w_lo && blo >= w_lo && blo <= w_hi) ? w_hi + 1 : blo;
             const int nnew = bhi - n0 + 1;
-            ndgi_jitter(4u);
-            __syncwarp();   // this warp's gathers of the previous chunk are done
-            if (nnew > 0) {
-                if (fmt_block4(p.fmt_uvt)) {
-                    // one BC7 / BC1 / BC3 block per lane (both slices' blocks: 2 * nnew * wxb <= 48
-                    // decodes), raw RGBA8 into this warp's part of the F_uv chunk
-                    // buffer (free between chunks: 16 rows x 128 B), then all lanes
-                    // blend texels into the ring
-                    const int nblk = nnew * win.wxb;             // block positions
-                    uint8_t* scratch = reinterpret_cast<uint8_t*>(sUv) + warp * 128;   // row r at + r * C * 4
-                    for (int g0 = 0; g0 < nblk; g0 += 16) {      // 16 positions = 32 blocks per round
-                        const int ng = nblk - g0 < 16 ? nblk - g0 : 16;
-                        {
-                            const int q = lane < 2 * ng ? lane : 0;   // spare lanes: duplicate, no store
-                            const int pos = g0 + (q >> 1), sl = q & 1;
-                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
-                            const int gbx = wbx0 + qx < nbm ? wbx0 + qx : nbm - 1;
-                            const uint8_t* src = vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0);
-                            uint32_t t[16];
-                            NDGI_CHECK(br >= 0 && br < nbm && gbx >= 0 && gbx < nbm);
-                            block4_decode(p.fmt_uvt, src, (size_t)br * nbm + gbx, [&](int i, uint32_t v) { t[i] = v; });
-                            if (lane < 2 * ng) {
-                                // scratch slot q: 64 B at row q >> 1, byte (q & 1) * 64
-                                uint4* d = reinterpret_cast<uint4*>(scratch + (size_t)(q >> 1) * C * 4 + (q & 1) * 64);
-#pragma unroll
-                                for (int r = 0; r < 4; ++r) d[r] = make_uint4(t[4 * r], t[4 * r + 1], t[4 * r + 2], t[4 * r + 3]);
-                            }
-                        }
-                        ndgi_jitter(7u);
-                        __syncwarp();
-                        for (int e = lane; e < ng * 16; e += 32) {
-                            const int pos = g0 + (e >> 4), i = e & 15;
-                            const int qx = pos % win.wxb, br = n0 + pos / win.wxb;
-                            if (wbx0 + qx >= nbm) continue;
-                            const uint32_t* sp = reinterpret_cast<const uint32_t*>(scratch + (size_t)(e >> 4) * C * 4);
-                            const uint32_t q0v = sp[i], q1v = sp[16 + i];
-                            float c[4];
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = (omt * u8f(q0v, qq) + tau * u8f(q1v, qq)) *
-                                        (1.0f / 255.0f);
-                            NDGI_CHECK((uint32_t)(((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)) * 8u < win.bytes);
-                            wdst[((br & (ring - 1)) * 4 + (i >> 2)) * WX + qx * 4 + (i & 3)] =
-                                make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
-                        }
-                        __syncwarp();
-                    }
-                } else {
-                    const int ntex = nnew * 4 * WX;
-                    for (int e = lane; e < ntex; e += 32) {
-                        const int gy = n0 * 4 + e / WX, gx = wbx0 * 4 + e % WX;
-                        if (gx >= R3 || gy >= R3) continue;
-                        const int g = gy * R3 + gx;
-                        float c[4];
-                        if (p.fmt_uvt == FMT_U8) {
-                            const uint32_t q0 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k0) + g);
-                            const uint32_t q1 = __ldg(reinterpret_cast<const uint32_t*>(vol + p.uvt_slice_bytes * tc.k1) + g);
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = (omt * u8f(q0, qq) + tau * u8f(q1, qq)) *
-                                        (1.0f / 255.0f);
-                        } else {
-                            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k0) + 4 * g;
-                            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(vol + p.uvt_slice_bytes * tc.k1) + 4 * g;
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
-                        }
-                        NDGI_CHECK((uint32_t)((gy & (4 * ring - 1)) * WX + e % WX) * 8u < win.bytes);
-                        wdst[((gy & (4 * ring - 1))) * WX + e % WX] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
-                    }
-                }
-            }
-            __syncwarp();
             w_lo = blo;
             w_hi = bhi;
+            if (nnew <= 0) return;                       // CTA-uniform
+            ndgi_jitter(4u);
+            __syncthreads();                             // every warp's gathers of the previous chunk are done
+            const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
+            const uint8_t* s0 = vol + p.uvt_slice_bytes * tc.k0;
+            const uint8_t* s1 = vol + p.uvt_slice_bytes * tc.k1;
+            const float tau = tc.tau, omt = 1.0f - tau;
+            const int nbx = (R3 + 3) >> 2;
+            if (p.fmt_uvt == FMT_BC1 || p.fmt_uvt == FMT_BC3) {
+                // BC1 / BC3: one whole block (both slices) per thread -- their
+                // decoders build a per-block palette, a row would redo it 4x
+                for (int pos = tid; pos < nnew * nbx; pos += kThreads) {
+                    const int bx = pos % nbx, by = n0 + pos / nbx;
+                    uint32_t t0[16], t1[16];
+                    block4_decode(p.fmt_uvt, s0, (size_t)by * nbx + bx, [&](int i, uint32_t v) { t0[i] = v; });
+                    block4_decode(p.fmt_uvt, s1, (size_t)by * nbx + bx, [&](int i, uint32_t v) { t1[i] = v; });
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float c[4];
+#pragma unroll
+                        for (int qq = 0; qq < 4; ++qq)
+                            c[qq] = (omt * u8f(t0[i], qq) + tau * u8f(t1[i], qq)) * (1.0f / 255.0f);
+                        const int gy = by * 4 + (i >> 2);
+                        NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)(bx * 4 + (i & 3)) * 8u + 8u <= ring.bytes);
+                        *reinterpret_cast<uint2*>(smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch +
+                                                  (bx * 4 + (i & 3)) * 8) =
+                            make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+                    }
+                }
+                ndgi_jitter(7u);
+                __syncthreads();
+                return;
+            }
+            const int items = nnew * nbx * 4;            // (block row of a block) items
+            for (int it = tid; it < items; it += kThreads) {
+                const int r = it & 3, pos = it >> 2;
+                const int bx = pos % nbx, by = n0 + pos / nbx;
+                const int gy = by * 4 + r;                // F_uvt row
+                uint32_t q0[4], q1[4];
+                float c[4][4];
+                if (fmt_block4(p.fmt_uvt)) {
+                    NDGI_CHECK(by < nbx);
+                    block4_decode_row(p.fmt_uvt, s0, (size_t)by * nbx + bx, r, q0);
+                    block4_decode_row(p.fmt_uvt, s1, (size_t)by * nbx + bx, r, q1);
+#pragma unroll
+                    for (int x = 0; x < 4; ++x)
+#pragma unroll
+                        for (int qq = 0; qq < 4; ++qq)
+                            c[x][qq] = (omt * u8f(q0[x], qq) + tau * u8f(q1[x], qq)) * (1.0f / 255.0f);
+                } else {
+                    if (gy >= R3) continue;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const int g = gy * R3 + min(bx * 4 + x, R3 - 1);
+                        if (p.fmt_uvt == FMT_U8) {
+                            const uint32_t a0 = __ldg(reinterpret_cast<const uint32_t*>(s0) + g);
+                            const uint32_t a1 = __ldg(reinterpret_cast<const uint32_t*>(s1) + g);
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[x][qq] = (omt * u8f(a0, qq) + tau * u8f(a1, qq)) * (1.0f / 255.0f);
+                        } else {
+                            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(s0) + 4 * g;
+                            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(s1) + 4 * g;
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[x][qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
+                        }
+                    }
+                }
+                uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    if (bx * 4 + x >= R3) break;
+                    NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)(bx * 4 + x) * 8u + 8u <= ring.bytes);
+                    *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
+                        make_uint2(pack_f16x2(c[x][0], c[x][1]), pack_f16x2(c[x][2], c[x][3]));
+                }
+            }
+            ndgi_jitter(7u);
+            __syncthreads();
         };
 
-        // one layer for all S items of the step: A written by all 128 threads ->
-        // CTA barrier -> one elected lane of warp 0 issues S x (K/16) MMAs and
-        // commits them to d_ready -> everyone waits for the accumulators
         auto run_layer = [&](auto layer) {
             constexpr int l = decltype(layer)::value;
             ptx::tmem_wait_st();
@@ -511,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         const int crows = p.strip_rows < chunk_rows ? p.strip_rows : chunk_rows;
         const int chunk_items = crows * BPR;
         for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
-        if constexpr (WIN) stage_window(j_begin + c0 / BPR, crows);   // uses the F_uv chunk buffer as scratch
+        if constexpr (WIN) stage_ring(j_begin + c0 / BPR, crows);
         if (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) decode_chunk(j_begin + c0 / BPR, crows);
         for (int it = c0; it < c0 + chunk_items; it += S) {
             if constexpr (BPR == 1 && S == 2) {
@@ -603,7 +590,7 @@ cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
     constexpr bool kWinOk = H == 16 && CT == 128;
     const bool win = kWinOk && p.R3 > 32;
     uint32_t smem = L.total;
-    if (win) smem = L.uvt + 4u * uvt_window(p.R3, CT, kChunkTexels / CT).bytes;
+    if (win) smem = L.uvt + uvt_ring(p.R3, CT, kChunkTexels / CT).bytes;
     const bool tiles8 = !p.full && p.out_fmt == OUT_RGBA8;
     auto pick = [&](auto ok, auto w) {
         return ndgi_fused_kernel<H, FMT_UV, CT, decltype(ok)::value, decltype(w)::value && kWinOk>;
