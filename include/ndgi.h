@@ -114,8 +114,10 @@ typedef enum {
  *   k = (a * tiles_y + ty) * tiles_x + tx,  num_tiles = atlases*tiles_y*tiles_x.
  * Constraints (NDGI_ERR_ARG otherwise): abi_version == NDGI_ABI_VERSION;
  *   num_tiles >= 1; core >= 4, core % 4 == 0; border < core;
- *   BC7 maps need resolutions that are multiples of 4; all resolutions >= 1;
- *   uvt_depth, line_t >= 1; 1 <= hidden <= 256; fmt_line is U8 or F16.
+ *   block-compressed maps need resolutions that are multiples of 4 (BC5 line
+ *   maps: line_res and line_t); all resolutions >= 1; uvt_depth, line_t >= 1;
+ *   1 <= hidden <= 256; fmt_uv / fmt_uvt in {BC7, U8, F16, BC1, BC3};
+ *   fmt_line in {U8, F16, BC5}.
  * NDGI_MODE_FAST additionally needs (NDGI_ERR_UNSUPPORTED otherwise):
  *   core in {128, 256}, uv_res == core (R2), hidden in {16, 64}
  *   (Table 3), border_mode == MIRROR, uvt_res <= 64, line_res <= 256.
