@@ -923,6 +923,7 @@ def main():
         import torch.distributed as dist_mod
         if args.backend == "nccl":
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            os.environ.setdefault("NCCL_DEBUG", "INFO")    # NCCL's init log (transports, NVLS) on stderr
         dist_mod.init_process_group(args.backend)
         dist = dist_mod
     try:
