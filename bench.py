@@ -106,6 +106,12 @@ class ClockSampler:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # let nvidia-smi start up (its first queries disturb the GPU) before
+            # the caller's timed region begins
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 2.0:
+                time.sleep(0.01)
+            time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
