@@ -21,6 +21,9 @@ CASES = {
     "M64": (S.layout(1, 2, 1, "M64", uvt_depth=4, line_t=4), "mixed"),
     "C256": (S.layout(1, 1, 1, "M", core=256, uv_res=256, uvt_depth=4, line_t=4), "smooth"),
     "bc3": (S.layout(1, 2, 1, "M", uvt_depth=4, line_t=8, fmt_uv="bc3", fmt_uvt="bc3", fmt_line="bc5"), "mixed"),
+    "ring-R3=40-u8": (S.layout(1, 2, 1, "M", uvt_res=40, uvt_depth=4, line_t=4, fmt_uv="u8", fmt_uvt="u8"), "smooth"),
+    "ring-R3=56-bc1": (S.layout(1, 2, 1, "M", uvt_res=56, uvt_depth=4, line_t=8, fmt_uv="bc1", fmt_uvt="bc1",
+                                fmt_line="bc5"), "mixed"),
 }
 
 

@@ -239,3 +239,33 @@ def test_wide_border_both_mirrors(border):
     for r in range(2):
         mx, mean = _err(y[r], exp[r])
         assert mx <= FAST_MAX and mean <= FAST_MEAN
+
+
+RING_CASES = {
+    # the F_uvt ring (R3 > 32) off the H profile's power-of-two size
+    "R3=48-bc7": S.layout(1, 2, 1, "M", uvt_res=48, uvt_depth=4, line_t=4),
+    "R3=40-u8": S.layout(1, 2, 1, "M", uvt_res=40, uvt_depth=4, line_t=4, fmt_uv="u8", fmt_uvt="u8"),
+    "R3=36-f16": S.layout(1, 2, 1, "M", uvt_res=36, uvt_depth=4, line_t=4, fmt_uv="f16", fmt_uvt="f16",
+                          fmt_line="f16"),
+    "R3=33-u8": S.layout(1, 2, 1, "M", uvt_res=33, uvt_depth=3, line_t=4, fmt_uv="u8", fmt_uvt="u8"),
+    "R3=56-bc1": S.layout(1, 2, 1, "M", uvt_res=56, uvt_depth=4, line_t=8, fmt_uv="bc1", fmt_uvt="bc1",
+                          fmt_line="bc5"),
+}
+
+
+@pytest.mark.parametrize("name", list(RING_CASES))
+def test_uvt_ring_sizes(name):
+    """F_uvt rings for R3 in (32, 64] that are not powers of two, including
+    dense maps whose R3 is not a multiple of 4 (ring staging of partial block
+    columns): decode_full and decode_tiles with 4-row strips vs the oracle."""
+    lay = RING_CASES[name]
+    th = S.make_theta(lay, 23, "mixed")
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    for t in (0.2, 0.95):
+        y = gpu_full(ctx, t, "rgba32f", "fast")[0, 0]
+        mx, mean = _err(y, M.decode_full(t, NTHR)[0])
+        assert mx <= FAST_MAX and mean <= FAST_MEAN, (name, t, mx, mean)
+    got = gpu_tiles(ctx, [1], 0.61, "rgba32f")      # n = 1: 4-row strips, ring restaged per strip
+    mx, mean = _err(got, M.decode_tiles([1], 0.61, NTHR))
+    assert mx <= FAST_MAX and mean <= FAST_MEAN, (name, mx, mean)
