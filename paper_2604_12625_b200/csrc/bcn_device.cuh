@@ -145,15 +145,10 @@ __device__ __forceinline__ void block4_decode(int fmt, const uint8_t* base, size
     }
 }
 
-// row r (texels 4r .. 4r+3) of block bi of a BC7 / BC1 / BC3 map
-__device__ __forceinline__ void block4_decode_row(int fmt, const uint8_t* base, size_t bi, int r, uint32_t (&out)[4]) {
-    if (fmt == FMT_BC1 || fmt == FMT_BC3) {
-        block4_decode(fmt, base, bi, [&](int i, uint32_t v) {
-            if ((i >> 2) == r) out[i & 3] = v;
-        });
-    } else {
-        bc7_decode_row(__ldg(reinterpret_cast<const uint4*>(base) + bi), r, out);
-    }
+// row r (texels 4r .. 4r+3) of BC7 block bi (the F_uvt ring's BC7 staging;
+// BC1 / BC3 blocks are staged whole)
+__device__ __forceinline__ void block4_decode_row(const uint8_t* base, size_t bi, int r, uint32_t (&out)[4]) {
+    bc7_decode_row(__ldg(reinterpret_cast<const uint4*>(base) + bi), r, out);
 }
 
 // BC5 texel (x, y) of a [ry][rx] 2-channel map: packed c0 | c1 << 8

@@ -21,9 +21,6 @@ constexpr int kChunkTexels = 2048;             // F_uv texels decoded per chunk 
 #ifndef NDGI_SLOTS16
 #define NDGI_SLOTS16 2
 #endif
-#ifndef NDGI_GROUPS16
-#define NDGI_GROUPS16 1
-#endif
 
 template <int H>
 struct FusedCfg {
@@ -44,8 +41,7 @@ struct FusedCfg {
     static constexpr uint32_t TM_D = H == 16 ? 16 : 64;  // H columns (fp32 accumulators)
     static constexpr uint32_t SLOT_COLS = H == 16 ? 32 : 128;
     static constexpr int SLOTS = H == 16 ? NDGI_SLOTS16 : 1;   // 128-texel items per MMA step (one TMEM slot each)
-    static constexpr int GROUPS = H == 16 ? NDGI_GROUPS16 : 1;   // independent step groups (ping-pong)
-    static constexpr uint32_t TM_COLS = GROUPS * SLOTS * SLOT_COLS < 32 ? 32 : GROUPS * SLOTS * SLOT_COLS;
+    static constexpr uint32_t TM_COLS = SLOTS * SLOT_COLS < 32 ? 32 : SLOTS * SLOT_COLS;
     static constexpr int MIN_CTAS = H == 16 ? NDGI_MIN_CTAS16 : 4;   // register budget: 64 / 128 per thread
     static constexpr int B1_BYTES = H * 16 * 2;
     static constexpr int B2_BYTES = H * K2 * 2;
@@ -189,22 +185,6 @@ __device__ __forceinline__ void gelu_epilogue_h16(uint32_t d0, uint32_t a0, uint
         }
         ptx::tmem_st_x8(a0 + s * stride, g);
     }
-}
-
-// h = 16, two items: both accumulators loaded before one wait, 16 independent
-// GELU pairs in flight (more ILP for the MUFU pipe)
-__device__ __forceinline__ void gelu_epilogue2_h16(uint32_t d0, uint32_t a0, uint32_t d1, uint32_t a1) {
-    uint32_t x[16], y[16], g[8], h[8];
-    ptx::tmem_ld_x16(d0, x);
-    ptx::tmem_ld_x16(d1, y);
-    ptx::tmem_wait_ld();
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        g[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(x[2 * q]), __uint_as_float(x[2 * q + 1])));
-        h[q] = gelu_scaled_f16x2(pack_f16x2(__uint_as_float(y[2 * q]), __uint_as_float(y[2 * q + 1])));
-    }
-    ptx::tmem_st_x8(a0, g);
-    ptx::tmem_st_x8(a1, h);
 }
 
 // ---- F_uvt ring (large R3, C = 128): instead of the whole tau-blended slice

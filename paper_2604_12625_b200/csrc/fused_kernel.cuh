@@ -39,9 +39,6 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
-#ifndef NDGI_JOINT_EPI
-#define NDGI_JOINT_EPI 1
-#endif
 
 // FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
 // no format switch, row pointers instead of 64-bit index arithmetic
@@ -293,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 float c[4][4];
                 if (fmt_block4(p.fmt_uvt)) {
                     NDGI_CHECK(by < nbx);
-                    block4_decode_row(p.fmt_uvt, s0, (size_t)by * nbx + bx, r, q0);
-                    block4_decode_row(p.fmt_uvt, s1, (size_t)by * nbx + bx, r, q1);
+                    block4_decode_row(s0, (size_t)by * nbx + bx, r, q0);
+                    block4_decode_row(s1, (size_t)by * nbx + bx, r, q1);
 #pragma unroll
                     for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -478,7 +475,6 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         };
 
         auto epilogues = [&]() {
-#if NDGI_JOINT_EPI
             if constexpr (H == 16) {
 #if NDGI_F16ACC
                 gelu_epilogue_h16_f16acc<S>(tm_lane + Cfg::TM_D, tm_lane + Cfg::TM_A23, Cfg::SLOT_COLS);
@@ -487,7 +483,6 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 #endif
                 return;
             }
-#endif
 #pragma unroll
             for (int s = 0; s < S; ++s)
                 gelu_epilogue<H>(tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_D, tm_lane + s * Cfg::SLOT_COLS + Cfg::TM_A23);

@@ -29,79 +29,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-// bounded wait: a tensor-core op that never completes traps (launch failure)
-// after ~4 s instead of hanging the device
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t spins = 0;
-    uint64_t t0 = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if ((++spins & 63u) == 0) {
-            const uint64_t now = globaltimer_ns();
-            if (t0 == 0) t0 = now;
-            else if (now - t0 > 4000000000ull) __trap();
-        }
-    }
-}
-
-#ifndef NDGI_WAIT_HINT_NS
-#define NDGI_WAIT_HINT_NS 0
-#endif
-__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity) {
-#if NDGI_WAIT_HINT_NS > 0
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "n"(NDGI_WAIT_HINT_NS)
-        : "memory");
-    return ok != 0;
-#else
-    return mbar_try_wait(bar, parity);
-#endif
-}
-__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
-#ifndef NDGI_WAITMODE
-#define NDGI_WAITMODE 0
-#endif
-// hot-loop wait: try_wait suspends the warp in hardware (optionally with a
-// suspend-time hint); traps after ~2^28 polls so a lost commit cannot hang.
-// NDGI_WAITMODE 1: non-suspending test_wait poll; 2: poll + short nanosleep
+// bounded wait (debug hooks): traps after 2^28 polls so a lost commit cannot hang
 __device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
-#if NDGI_WAITMODE == 1
-    while (!mbar_test_wait(bar, parity))
-        if (++n == (1u << 30)) __trap();
-#elif NDGI_WAITMODE == 2
-    while (!mbar_test_wait(bar, parity)) {
-        __nanosleep(32);
+    while (!mbar_try_wait(bar, parity))
         if (++n == (1u << 28)) __trap();
-    }
-#else
-    while (!mbar_try_wait_hint(bar, parity))
-        if (++n == (1u << 28)) __trap();
-#endif
 }
 
-// hot-loop wait without the poll counter: the whole loop is TRYWAIT + branch
-// (the CUTLASS-style wait); used where the issuing code is unconditional
+// hot-loop wait: the whole loop is TRYWAIT + branch (TRYWAIT suspends the
+// warp in hardware until the phase completes or a time limit)
 #ifndef NDGI_SPIN_HINT_NS
 #define NDGI_SPIN_HINT_NS 0
 #endif
@@ -129,13 +65,6 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// shared-memory atomic add with acquire-release semantics at CTA scope
-__device__ __forceinline__ uint32_t atom_add_acqrel_cta(uint32_t addr, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-    return old;
-}
-
 // one lane of the (converged) warp returns true
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
@@ -145,11 +74,6 @@ __device__ __forceinline__ bool elect_one() {
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(pred));
     return pred != 0;
-}
-
-// named barrier over `n` threads (multiple of 32)
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // ---- fences ------------------------------------------------------------------
@@ -213,12 +137,6 @@ __device__ __forceinline__ void tmem_st_x8(uint32_t taddr, const uint32_t (&r)[8
                  "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                  : "memory");
 }
-// 8 packed f16x2 -> 16 columns holding one 16-bit value each (f16 accumulator layout)
-__device__ __forceinline__ void tmem_st_x8_unpack16(uint32_t taddr, const uint32_t (&r)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.unpack::16b.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
-                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ---- MMA: D[tmem] (+)= A[tmem] x B[smem]^T, kind::f16, cta_group::1 ---------
@@ -229,16 +147,6 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// D[tmem] (+)= A[smem] x B[smem]^T
-__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                           uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 // arrive on an mbarrier when all prior tcgen05 async ops of this thread complete
