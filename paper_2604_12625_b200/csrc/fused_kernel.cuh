@@ -40,6 +40,7 @@ namespace ndgi {
 constexpr int kThreads = 128;
 
 
+
 // FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
 // no format switch, row pointers instead of 64-bit index arithmetic
 // WIN: F_uvt staged per chunk into a ring of rows (UvtRing) instead of the
@@ -335,7 +336,11 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncthreads();
-            if (warp == 0) {
+            // the issuing warp rotates with the layer for the H ring and h = 64
+            // kernels (each warp sits on its own SMSP; one warp carrying all
+            // the issue work makes the others wait for it at every barrier):
+            // measured H +0.9 %, M.64 +1.1 %, but M -0.7 %, so M keeps warp 0
+            if (warp == ((WIN || H == 64) ? (int)(decltype(layer)::value % 4) : 0)) {
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
 #pragma unroll
