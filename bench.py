@@ -636,10 +636,19 @@ def vt_latency(ndgi, torch, args):
     evs[-1].record(stream)
     evs[-1].synchronize()
     fd = sorted(evs[f].elapsed_time(evs[f + 1]) * 1e3 for f in range(16, 64))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(int(2e-3 * 1.9e9))
+    e0.record(stream)
+    for f in range(64):
+        ndgi.ndgi_debug_null_launch(stream)
+    e1.record(stream)
+    e1.synchronize()
+    fa = e0.elapsed_time(e1) * 1e3 / 64
     res["floor"] = {"p50": statistics.median(fl), "host_call_us_p50": statistics.median(fh),
-                    "device_p50": fd[len(fd) // 2],
-                    "what": "empty kernel via ndgi_debug_null_launch, events around the Python call (p50) and "
-                            "queued ahead (device_p50)"}
+                    "device_p50": fd[len(fd) // 2], "device_avg": fa,
+                    "what": "empty kernel via ndgi_debug_null_launch, events around the Python call (p50), "
+                            "queued ahead with an event pair per launch (device_p50), queued ahead with no events "
+                            "in between (device_avg)"}
     for n in (8, 32, 128, 512):
         batches = S.vt_batches(lay["num_tiles"], n, 16 + 64, seed)
         cache = torch.empty((n, 136, 136, 4), dtype=torch.uint8, device="cuda")
@@ -675,12 +684,24 @@ def vt_latency(ndgi, torch, args):
         evs[-1].record(stream)
         evs[-1].synchronize()
         dev = sorted(evs[f].elapsed_time(evs[f + 1]) * 1e3 for f in range(16, len(batches)))
+        # the same stream of batches with no events in between (an event record
+        # between launches costs ~4 us of device time itself): average per batch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(int(2e-3 * 1.9e9))
+        e0.record(stream)
+        for f, (b, t) in enumerate(batches):
+            ndgi.ndgi_decode_tiles(ctx, ids[f], None, n, n, t, cache, "rgba8", "fast", stream)
+        e1.record(stream)
+        e1.synchronize()
+        dev_avg = e0.elapsed_time(e1) * 1e3 / len(batches)
         res[str(n)] = {"p50": p50, "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))],
                        "gtexel_s": n * 136 * 136 / (p50 * 1e-6) / 1e9, "host_call_us_p50": host[len(host) // 2],
-                       "device_p50": dev[len(dev) // 2], "device_p99": dev[min(len(dev) - 1, int(0.99 * len(dev)))]}
+                       "device_p50": dev[len(dev) // 2], "device_p99": dev[min(len(dev) - 1, int(0.99 * len(dev)))],
+                       "device_avg": dev_avg}
     res["how"] = ("p50/p99: events around the Python call of ndgi.TileDecoder (ndgi_decode_tiles bound to the "
                   "render loop's fixed id/cache buffers; host enqueue inside the events); device_p50/p99: per-batch "
-                  "device time with launches queued ahead of the GPU")
+                  "device time with launches queued ahead of the GPU, an event pair around each (each event record "
+                  "adds ~4 us); device_avg: the same batches back to back between two events, per batch")
     return res
 
 

@@ -441,6 +441,12 @@ NDGI_API ndgi_status ndgi_debug_gelu_split(uint32_t hidden, uint32_t* mufu_pairs
  * through the C ABI (bench.py times it beside ndgi_decode_tiles). */
 NDGI_API ndgi_status ndgi_debug_null_launch(void* stream);
 
+/* Launch-cost probes beside the floor: kind 0 = the empty kernel above, 1 = an
+ * empty kernel with the fused kernel's parameter block, 2 = an empty 256-CTA
+ * grid with 24 KB of dynamic smem, 3 = 256 CTAs allocating and freeing 64
+ * TMEM columns.  Errors: ARG, CUDA. */
+NDGI_API ndgi_status ndgi_debug_launch_probe(int kind, void* stream);
+
 /* tcgen05 round-trip microbenchmark (st A, barrier, MMA M128N16K16, commit,
  * mbarrier wait, ld D) on one CTA: SM cycles per iteration.  Synchronous. */
 NDGI_API ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_iter);

@@ -71,6 +71,7 @@ _SIGS = {
     "ndgi_debug_gelu_split": (_I, [_U32, C.POINTER(_U32), C.POINTER(_I)]),
     "ndgi_debug_mma_latency": (_I, [_U32, C.POINTER(C.c_double)]),
     "ndgi_debug_null_launch": (_I, [_P]),
+    "ndgi_debug_launch_probe": (_I, [_I, _P]),
     "ndgi_debug_tmem_f16_probe": (_I, [_P]),
     "ndgi_vt_create": (_I, [_U32, _U32, _U32, C.POINTER(C.c_void_p)]),
     "ndgi_vt_free": (_I, [_P]),
@@ -279,6 +280,11 @@ def ndgi_debug_gelu_split(hidden: int) -> tuple[int, bool]:
 def ndgi_debug_null_launch(stream=None) -> None:
     """An empty kernel through the C ABI (the VT launch-latency floor)."""
     _check(_lib.ndgi_debug_null_launch(_stream_ptr(stream)), "ndgi_debug_null_launch")
+
+
+def ndgi_debug_launch_probe(kind: int, stream=None) -> None:
+    """Launch-cost probes (0 empty, 1 + fused param block, 2 256-CTA grid with smem, 3 TMEM alloc)."""
+    _check(_lib.ndgi_debug_launch_probe(int(kind), _stream_ptr(stream)), "ndgi_debug_launch_probe")
 
 
 def ndgi_debug_mma_latency(iters: int = 1000) -> float:

@@ -141,8 +141,41 @@ cudaError_t gelu_rate(uint32_t iters, uint32_t mufu_pairs, int pack, float* ms, 
 // the VT latency floor: an empty kernel launched through the same C-ABI path
 __global__ void null_kernel() {}
 
-cudaError_t null_launch(cudaStream_t s) {
-    null_kernel<<<1, 32, 0, s>>>();
+// launch-cost probes (ndgi_debug_null_launch kind > 0): what a fused-kernel
+// launch adds to an empty one -- its parameter block, its grid with dynamic
+// smem, and the TMEM allocation of every CTA
+__global__ void null_param_kernel(const __grid_constant__ KParams p) {
+    if (p.units == 0xffffffffu) p.err[0] = 1u;
+}
+__global__ void __launch_bounds__(128, 8) null_grid_kernel() {
+    extern __shared__ uint8_t sm[];
+    if (threadIdx.x == 1000) sm[0] = 0;
+}
+__global__ void __launch_bounds__(128, 8) tmem_alloc_kernel() {
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(slot) : "memory");
+}
+
+cudaError_t null_launch(cudaStream_t s, int kind) {
+    if (kind == 1) {
+        static KParams p{};
+        null_param_kernel<<<1, 32, 0, s>>>(p);
+    } else if (kind == 2) {
+        cudaFuncSetAttribute(null_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * 1024);
+        null_grid_kernel<<<256, 128, 24 * 1024, s>>>();
+    } else if (kind == 3) {
+        tmem_alloc_kernel<<<256, 128, 0, s>>>();
+    } else {
+        null_kernel<<<1, 32, 0, s>>>();
+    }
     return cudaGetLastError();
 }
 

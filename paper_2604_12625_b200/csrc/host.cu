@@ -43,7 +43,7 @@ cudaError_t launch_bc7_map(const void* blocks, uint32_t w, uint32_t h, uint8_t* 
 cudaError_t bc7_decode_hw(const void* blocks, uint32_t w, uint32_t h, uint8_t* rgba);
 cudaError_t gelu_rate(uint32_t iters, uint32_t mufu_pairs, int pack, float* ms, double* acts);
 int fused_gelu_mufu_pairs(int H);
-cudaError_t null_launch(cudaStream_t s);
+cudaError_t null_launch(cudaStream_t s, int kind);
 int fused_f16acc();
 cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter);
 cudaError_t tmem_f16_probe(uint32_t* host_out);
@@ -858,7 +858,13 @@ ndgi_status ndgi_debug_gelu_split(uint32_t hidden, uint32_t* mufu_pairs_of_16, i
 }
 
 ndgi_status ndgi_debug_null_launch(void* stream) {
-    const cudaError_t e = ndgi::null_launch(static_cast<cudaStream_t>(stream));
+    const cudaError_t e = ndgi::null_launch(static_cast<cudaStream_t>(stream), 0);
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "null launch");
+}
+
+ndgi_status ndgi_debug_launch_probe(int kind, void* stream) {
+    if (kind < 0 || kind > 3) return fail(NDGI_ERR_ARG, "kind must be 0..3");
+    const cudaError_t e = ndgi::null_launch(static_cast<cudaStream_t>(stream), kind);
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "null launch");
 }
 
