@@ -269,3 +269,31 @@ def test_uvt_ring_sizes(name):
     got = gpu_tiles(ctx, [1], 0.61, "rgba32f")      # n = 1: 4-row strips, ring restaged per strip
     mx, mean = _err(got, M.decode_tiles([1], 0.61, NTHR))
     assert mx <= FAST_MAX and mean <= FAST_MEAN, (name, mx, mean)
+
+
+EDGE_CASES = {
+    "C256-R3=64": S.layout(1, 1, 1, "H", core=256, uv_res=256, uvt_depth=3, line_t=4),   # whole 32 KB slice
+    "D1-T1": S.layout(1, 2, 1, "M", uvt_depth=1, line_t=1),                             # single slice / row
+    "R3=4-U=1": S.layout(1, 2, 1, "M", uvt_res=4, line_res=1, uvt_depth=2, line_t=3),   # smallest maps
+    "M64-C256": S.layout(1, 1, 1, "M64", core=256, uv_res=256, uvt_depth=2, line_t=2),
+}
+
+
+@pytest.mark.parametrize("name", list(EDGE_CASES))
+def test_fast_layout_edges(name):
+    """FAST-mode layouts at the edges of what the fused kernel takes: C = 256
+    with the whole R3 = 64 slice in smem, a single F_uvt slice and line row
+    (k0 = k1, r0 = r1), the smallest maps (R3 = 4, U = 1), h = 64 with C = 256 —
+    decode_full at t = 0, 0.5, 1 and decode_tiles against the oracle."""
+    lay = EDGE_CASES[name]
+    th = S.make_theta(lay, 31, "mixed")
+    M = oracle.Model(lay, th)
+    ctx = _load(lay, th)
+    for t in (0.0, 0.5, 1.0):
+        y = gpu_full(ctx, t, "rgba32f", "fast")[0, 0]
+        mx, mean = _err(y, M.decode_full(t, NTHR)[0])
+        assert mx <= FAST_MAX and mean <= FAST_MEAN, (name, t, mx, mean)
+    ids = list(range(lay["num_tiles"]))
+    got = gpu_tiles(ctx, ids, 0.7, "rgba32f")
+    mx, mean = _err(got, M.decode_tiles(ids, 0.7, NTHR))
+    assert mx <= FAST_MAX and mean <= FAST_MEAN, (name, mx, mean)
