@@ -288,6 +288,130 @@ __device__ __forceinline__ void copy_prepacked_weights(const KParams& p, const T
     }
 }
 
+// a2 for decode_tiles (VT): the same results as copy_prepacked_weights +
+// unit_prologue for BC7 F_uvt (R3 <= 32) and u8 line maps, restructured for
+// latency -- a small VT batch runs one unit per CTA and waits on it.  Every
+// global read of the unit (weights, both slices' F_uvt blocks, the line-map
+// taps) is issued before any is consumed (one HBM latency instead of three),
+// and the F_uvt blocks are decoded one per thread (both slices over all 128
+// threads) into `scratch` (>= 2 * (R3/4)^2 * 64 B: the F_uv chunk buffer, free
+// here), then blended 8 texels per thread after a CTA barrier.
+template <int H, int C>
+__device__ __forceinline__ void unit_prologue_vt(const KParams& p, const TConst& tc, int k, uint8_t* smem,
+                                                 const FusedSmem& L, int tid, uint8_t* scratch) {
+    using Cfg = FusedCfg<H>;
+    constexpr int NW = (int)(WPack<H>::B_BYTES / 16);   // 16-B chunks of the B operands
+    static_assert(NW <= 2 * 128 && Cfg::B1_BYTES / 16 <= 128, "two chunks per thread, B1 in the first");
+    const int R3 = p.R3, nbx = R3 >> 2, nb = nbx * nbx;
+    // ---- issue every load of the unit
+    const uint8_t* wbase = p.wpack + (size_t)WPack<H>::BYTES * k;
+    const uint4* wsrc = reinterpret_cast<const uint4*>(wbase);
+    const uint4 w0 = tid < NW ? __ldg(wsrc + tid) : make_uint4(0u, 0u, 0u, 0u);
+    const uint4 w1 = tid + 128 < NW ? __ldg(wsrc + tid + 128) : make_uint4(0u, 0u, 0u, 0u);
+    // the threads that patch layer 1's bias column (chunk tid holds K = 0 of B1
+    // row n) fetch [b1[n], W1[n][12..15]] now as well
+    const float* G = reinterpret_cast<const float*>(wbase + WPack<H>::B_BYTES);
+    const bool patch = tid < Cfg::B1_BYTES / 16 && !((tid >> 3) & 1);
+    const int pn = (tid >> 4) * 8 + (tid & 7);
+    float g5[5];
+#pragma unroll
+    for (int g = 0; g < 5; ++g) g5[g] = patch ? __ldg(G + pn * 5 + g) : 0.f;
+    const int sl = tid >= nb, bi = tid - (sl ? nb : 0);   // this thread's F_uvt item (slice, block)
+    const bool fitem = tid < 2 * nb;
+    const uint8_t* vol = p.uvt + p.uvt_tile_bytes * k;
+    const uint4 fblk = fitem ? __ldg(reinterpret_cast<const uint4*>(vol + p.uvt_slice_bytes * (sl ? tc.k1 : tc.k0)) + bi)
+                             : make_uint4(0u, 0u, 0u, 0u);
+    const float scu = (float)p.U * (1.0f / (float)C);
+    const uint8_t* ut = p.ut + p.line_tile_bytes * k;
+    const uint8_t* vt = p.vt + p.line_tile_bytes * k;
+    uint32_t lt[2][4];   // per line entry e = tid, tid + 128: (x0, r0), (x1, r0), (x0, r1), (x1, r1) as u8 pairs
+    float lfx[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int e = tid + 128 * h, i = e % C;
+        const uint8_t* m = e < C ? ut : vt;
+        const float sx = fmaf((float)i + 0.5f, scu, -0.5f);
+        const float fl = floorf(sx);
+        lfx[h] = sx - fl;
+        const int x0 = clampi((int)fl, 0, p.U - 1), x1 = clampi((int)fl + 1, 0, p.U - 1);
+        const uint16_t* mh = reinterpret_cast<const uint16_t*>(m);
+        lt[h][0] = __ldg(mh + tc.r0 * p.U + x0);
+        lt[h][1] = __ldg(mh + tc.r0 * p.U + x1);
+        lt[h][2] = __ldg(mh + tc.r1 * p.U + x0);
+        lt[h][3] = __ldg(mh + tc.r1 * p.U + x1);
+    }
+    // ---- weights -> smem (gamma(t) folded into layer 1's bias, as copy_prepacked_weights)
+    {
+        uint4* dst = reinterpret_cast<uint4*>(smem + L.b1);
+        if (tid < NW) {
+            uint4 v = w0;
+            if (patch) {
+                float acc = g5[0];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) acc = fmaf(g5[1 + g], tc.gamma[g], acc);
+                const uint32_t hb = (uint32_t)__half_as_ushort(__float2half_rn(kGeluA * acc));
+                v.x = (v.x & 0xffff0000u) | hb;
+            }
+            dst[tid] = v;
+        }
+        if (tid + 128 < NW) dst[tid + 128] = w1;   // chunks >= 128 are past B1 (no patch)
+    }
+    // ---- F_uvt: one block per thread -> scratch (raw RGBA8, 64 B per item)
+    if (fitem) {
+        uint32_t t16[16];
+        bc7_decode(fblk, [&](int i, uint32_t v) { t16[i] = v; });
+        uint4* d = reinterpret_cast<uint4*>(scratch + (size_t)tid * 64);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) d[r] = make_uint4(t16[4 * r], t16[4 * r + 1], t16[4 * r + 2], t16[4 * r + 3]);
+    }
+    // ---- line maps (R5) from the preloaded taps
+    {
+        uint32_t* sUt = reinterpret_cast<uint32_t*>(smem + L.utcol);
+        uint4* sRow = reinterpret_cast<uint4*>(smem + L.rowtab);
+        const float rho = tc.rho, omr = 1.0f - rho;
+        const float sc3 = (float)R3 * (1.0f / (float)C);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + 128 * h, i = e % C;
+            const float fx = lfx[h];
+            float c[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const float v00 = u8f(lt[h][0], q), v10 = u8f(lt[h][1], q), v01 = u8f(lt[h][2], q),
+                            v11 = u8f(lt[h][3], q);
+                const float v = (1.f - fx) * omr * v00 + fx * omr * v10 + (1.f - fx) * rho * v01 + fx * rho * v11;
+                c[q] = v * (1.0f / 255.0f);
+            }
+            if (e < C) {
+                sUt[i] = pack_f16x2(c[0], c[1]);
+            } else {
+                const float sy = fmaf((float)i + 0.5f, sc3, -0.5f);
+                const float fly = floorf(sy);
+                const int y0 = clampi((int)fly, 0, R3 - 1), y1 = clampi((int)fly + 1, 0, R3 - 1);
+                sRow[i] = make_uint4((uint32_t)y0 * R3 * 8u, (uint32_t)y1 * R3 * 8u, pack_f16x2(sy - fly, sy - fly),
+                                     pack_f16x2(c[0], c[1]));
+            }
+        }
+    }
+    ndgi_jitter(9u);
+    __syncthreads();   // scratch complete
+    // ---- tau-blend both slices -> the f16x4 slice (R4, R17), same arithmetic as unit_prologue
+    {
+        uint2* sUvt = reinterpret_cast<uint2*>(smem + L.uvt);
+        const float tau = tc.tau, omt = 1.0f - tau;
+        const uint32_t* sc = reinterpret_cast<const uint32_t*>(scratch);
+        for (int e = tid; e < R3 * R3; e += 128) {
+            const int y = e / R3, x = e % R3;
+            const int b = (y >> 2) * nbx + (x >> 2), i = (y & 3) * 4 + (x & 3);
+            const uint32_t q0 = sc[b * 16 + i], q1 = sc[(nb + b) * 16 + i];
+            float c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = (omt * u8f(q0, q) + tau * u8f(q1, q)) * (1.0f / 255.0f);
+            sUvt[e] = make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
+        }
+    }
+}
+
 // a2: one unit's feature parameters -> shared memory: the tau-blended F_uvt
 // slice, V_ut per column and the per-row gather table (F_uvt y taps, V_vt)
 // (the MLP's B operands come prepacked: copy_prepacked_weights).

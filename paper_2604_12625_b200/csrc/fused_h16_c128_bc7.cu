@@ -6,3 +6,11 @@ namespace ndgi {
 template cudaError_t launch_fused_t<16, FMT_BC7, 128>(const KParams& p, int num_sms, cudaStream_t s);
 template cudaError_t launch_fused_t<16, FMT_BC7_TEX, 128>(const KParams& p, int num_sms, cudaStream_t s);
 }  // namespace ndgi
+
+#if NDGI_TIMELINE
+// diagnostic builds only: the block-0 stage stamps of the last launch of a
+// (h = 16, C = 128, BC7) fused kernel
+extern "C" __attribute__((visibility("default"))) int ndgi_debug_timeline(unsigned long long* out16) {
+    return (int)cudaMemcpyFromSymbol(out16, ndgi::g_ndgi_timeline, 16 * sizeof(unsigned long long));
+}
+#endif

@@ -39,6 +39,19 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
+// NDGI_TIMELINE=1 (diagnostic builds only): %globaltimer stamps of block 0's
+// thread 0 at the stages of its first unit -> g_ndgi_timeline[16]
+#ifndef NDGI_TIMELINE
+#define NDGI_TIMELINE 0
+#endif
+#if NDGI_TIMELINE
+__device__ unsigned long long g_ndgi_timeline[16];
+#define NDGI_STAMP(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && tl_on) { unsigned long long _t; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t)); g_ndgi_timeline[i] = _t; } } while (0)
+#else
+#define NDGI_STAMP(i) do {} while (0)
+#endif
+
 
 
 // FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
@@ -56,6 +69,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     constexpr int BPR = CT / kThreads;          // 128-texel MMA blocks per row
     constexpr int chunk_rows = kChunkTexels / CT;
     extern __shared__ __align__(1024) uint8_t smem[];
+#if NDGI_TIMELINE
+    bool tl_on = true;
+#endif
+    NDGI_STAMP(0);
     const FusedSmem L = fused_smem_layout<H>(C, p.R3);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t bars = ptx::smem_addr(smem + L.bars);
@@ -77,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    NDGI_STAMP(1);
 
     const int B = p.B, P = p.P, R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
@@ -133,10 +151,21 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         // ---- a2: tile parameters -> shared memory -----------------------------------
         ndgi_jitter(1u);
         __syncthreads();  // previous unit's MMAs complete and all smem readers done
-        {
+        NDGI_STAMP(2);
+        bool vt_prologue = false;
+        if constexpr (TILES8 && !WIN && H == 16 && BPR == 1 && FMT_UV != FMT_BC7_TEX) {
+            // small VT batches are latency-bound: the overlapped prologue
+            vt_prologue = p.fmt_uvt == FMT_BC7 && p.fmt_line == FMT_U8 && R3 <= 32;
+            if (vt_prologue) {
+                unit_prologue_vt<H, C>(p, tc, k, smem, L, tid, smem + L.uvc);
+            }
+        }
+        if (!vt_prologue) {
             copy_prepacked_weights<H>(p, tc, k, smem, L, tid, kThreads);
+            NDGI_STAMP(3);
             unit_prologue<H, FMT_UV, C>(p, tc, k, smem, L, tid, kThreads, WIN ? ring.pitch : 0u, ring.rows);
         }
+        NDGI_STAMP(4);
         ptx::fence_proxy_async_smem();  // B operands written by the generic proxy -> tensor core
         ndgi_jitter(2u);
         __syncthreads();
@@ -499,7 +528,9 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         const int chunk_items = crows * BPR;
         for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
         if constexpr (WIN) stage_ring(j_begin + c0 / BPR, crows);
+        NDGI_STAMP(5);
         if (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) decode_chunk(j_begin + c0 / BPR, crows);
+        NDGI_STAMP(6);
         for (int it = c0; it < c0 + chunk_items; it += S) {
             if constexpr (BPR == 1 && S == 2) {
                 gather_rows2(j_begin + it, it - c0);
@@ -512,16 +543,24 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             run_layer(L1{});
             epilogues();
             run_layer(L2{});
+            NDGI_STAMP(7 + ((it - c0) / S < 4 ? (it - c0) / S : 3));
 #pragma unroll
             for (int s = 0; s < S; ++s) output(j_begin + (it + s) / BPR, (it + s) % BPR, s);
         }
         }
     }
 
+#if NDGI_TIMELINE
+        tl_on = false;
+#endif
     // ---- teardown --------------------------------------------------------------------
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc<Cfg::TM_COLS>(tmem);
+#if NDGI_TIMELINE
+    tl_on = true;
+#endif
+    NDGI_STAMP(11);
 }
 
 // ---- host-side launch helpers ---------------------------------------------------
