@@ -311,10 +311,14 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 __syncthreads();
                 return;
             }
+            const bool nbx_pow2 = (nbx & (nbx - 1)) == 0;
+            const int nbx_log2 = __ffs(nbx) - 1;
             const int items = nnew * nbx * 4;            // (block row of a block) items
             for (int it = tid; it < items; it += kThreads) {
                 const int r = it & 3, pos = it >> 2;
-                const int bx = pos % nbx, by = n0 + pos / nbx;
+                // nbx = 16 for the H profile: shifts instead of an integer division
+                const int bx = nbx_pow2 ? pos & (nbx - 1) : pos % nbx;
+                const int by = n0 + (nbx_pow2 ? pos >> nbx_log2 : pos / nbx);
                 const int gy = by * 4 + r;                // F_uvt row
                 uint32_t q0[4], q1[4];
                 float c[4][4];
