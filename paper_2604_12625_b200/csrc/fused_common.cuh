@@ -73,6 +73,11 @@ __device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
     asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
     return r;
 }
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
 // a + f (b - a), packed
 __device__ __forceinline__ uint32_t hlerp2(uint32_t a, uint32_t b, uint32_t f2) { return hfma2(f2, hsub2(b, a), a); }
 

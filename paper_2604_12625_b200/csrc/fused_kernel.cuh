@@ -39,6 +39,10 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
+#ifndef NDGI_RING_F16
+#define NDGI_RING_F16 1
+#endif
+
 // NDGI_TIMELINE=1 (diagnostic builds only): %globaltimer stamps of block 0's
 // thread 0 at the stages of its first unit -> g_ndgi_timeline[16]
 #ifndef NDGI_TIMELINE
@@ -322,6 +326,33 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 const int gy = by * 4 + r;                // F_uvt row
                 uint32_t q0[4], q1[4];
                 float c[4][4];
+#if NDGI_RING_F16
+                if (fmt_block4(p.fmt_uvt) || (p.fmt_uvt == FMT_U8 && R3 % 4 == 0)) {
+                    // tau-blend on f16x2 (exact integer operands, three roundings)
+                    if (fmt_block4(p.fmt_uvt)) {
+                        NDGI_CHECK(by < nbx);
+                        block4_decode_row(s0, (size_t)by * nbx + bx, r, q0);
+                        block4_decode_row(s1, (size_t)by * nbx + bx, r, q1);
+                    } else {
+                        const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(s0) + (gy * R3 + bx * 4) / 4);
+                        const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(s1) + (gy * R3 + bx * 4) / 4);
+                        q0[0] = a0.x; q0[1] = a0.y; q0[2] = a0.z; q0[3] = a0.w;
+                        q1[0] = a1.x; q1[1] = a1.y; q1[2] = a1.z; q1[3] = a1.w;
+                    }
+                    const uint32_t tau2 = pack_f16x2(tc.tau, tc.tau), inv2 = 0x1C041C04u;   // f16x2(1/255)
+                    uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        uint32_t arg, aba, brg, bba;
+                        u8x4_to_h2(q0[x], arg, aba);
+                        u8x4_to_h2(q1[x], brg, bba);
+                        *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
+                            make_uint2(hmul2(hfma2(tau2, hsub2(brg, arg), arg), inv2),
+                                       hmul2(hfma2(tau2, hsub2(bba, aba), aba), inv2));
+                    }
+                    continue;
+                }
+#endif
                 if (fmt_block4(p.fmt_uvt)) {
                     NDGI_CHECK(by < nbx);
                     block4_decode_row(s0, (size_t)by * nbx + bx, r, q0);
