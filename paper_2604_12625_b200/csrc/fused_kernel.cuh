@@ -327,6 +327,20 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 uint32_t q0[4], q1[4];
                 float c[4][4];
 #if NDGI_RING_F16
+                if (p.fmt_uvt == FMT_F16 && R3 % 4 == 0) {
+                    // f16 slices: h0 + tau (h1 - h0) directly on f16x2
+                    const uint32_t tau2 = pack_f16x2(tc.tau, tc.tau);
+                    const uint2* h0 = reinterpret_cast<const uint2*>(s0) + gy * R3 + bx * 4;
+                    const uint2* h1 = reinterpret_cast<const uint2*>(s1) + gy * R3 + bx * 4;
+                    uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const uint2 a = __ldg(h0 + x), b = __ldg(h1 + x);
+                        *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
+                            make_uint2(hfma2(tau2, hsub2(b.x, a.x), a.x), hfma2(tau2, hsub2(b.y, a.y), a.y));
+                    }
+                    continue;
+                }
                 if (fmt_block4(p.fmt_uvt) || (p.fmt_uvt == FMT_U8 && R3 % 4 == 0)) {
                     // tau-blend on f16x2 (exact integer operands, three roundings)
                     if (fmt_block4(p.fmt_uvt)) {
