@@ -145,10 +145,30 @@ __device__ __forceinline__ void block4_decode(int fmt, const uint8_t* base, size
     }
 }
 
-// row r (texels 4r .. 4r+3) of BC7 block bi (the F_uvt ring's BC7 staging;
-// BC1 / BC3 blocks are staged whole)
-__device__ __forceinline__ void block4_decode_row(const uint8_t* base, size_t bi, int r, uint32_t (&out)[4]) {
-    bc7_decode_row(__ldg(reinterpret_cast<const uint4*>(base) + bi), r, out);
+// row r (texels 4r .. 4r+3) of block bi of a BC7 / BC1 / BC3 map (the F_uvt
+// ring's staging: one block row per thread, so all 128 threads take part; the
+// BC1 / BC3 palettes are rebuilt per row -- their cost is small next to a
+// chunk start with three of four warps idle at the barrier)
+__device__ __forceinline__ void block4_decode_row(int fmt, const uint8_t* base, size_t bi, int r, uint32_t (&out)[4]) {
+    if (fmt == FMT_BC1) {
+        const uint2 w = __ldg(reinterpret_cast<const uint2*>(base) + bi);
+        uint32_t pal[4];
+        bc1_palette(w.x, false, pal);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) out[x] = sel4(pal, (w.y >> (8 * r + 2 * x)) & 3u);
+    } else if (fmt == FMT_BC3) {
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(base) + bi);
+        uint32_t pal[4], alo, ahi;
+        bc1_palette(raw.z, true, pal);
+        bc4_palette_packed(raw.x, alo, ahi);
+        const uint32_t aidx = (uint32_t)((((uint64_t)raw.y << 32) | raw.x) >> (16 + 12 * r));   // 4 x 3 bits
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            out[x] = __byte_perm(sel4(pal, (raw.w >> (8 * r + 2 * x)) & 3u), __byte_perm(alo, ahi, (aidx >> (3 * x)) & 7u),
+                                 0x4210u);
+    } else {
+        bc7_decode_row(__ldg(reinterpret_cast<const uint4*>(base) + bi), r, out);
+    }
 }
 
 // BC5 texel (x, y) of a [ry][rx] 2-channel map: packed c0 | c1 << 8

@@ -39,9 +39,6 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
-#ifndef NDGI_RING_F16
-#define NDGI_RING_F16 1
-#endif
 
 // NDGI_TIMELINE=1 (diagnostic builds only): %globaltimer stamps of block 0's
 // thread 0 at the stages of its first unit -> g_ndgi_timeline[16]
@@ -270,8 +267,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         // WIN: the CTA's F_uvt ring (UvtRing): at each chunk start the block rows
         // the chunk samples that are not yet resident are decoded and tau-blended
         // into ring rows y mod ring.rows by all 128 threads -- one (block row of
-        // a 4x4 block, both slices) per thread per round, the same blend
-        // arithmetic as unit_prologue's whole slice
+        // a 4x4 block, both slices) per thread per round
         int w_lo = 1, w_hi = 0;   // resident block rows [w_lo, w_hi] (empty)
         auto stage_ring = [&](int jc, int nrows) {
             const int ymin = clampi((int)floorf(fmaf((float)jc + 0.5f, sc3, -0.5f)), 0, R3 - 1);
@@ -289,32 +285,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const uint8_t* s0 = vol + p.uvt_slice_bytes * tc.k0;
             const uint8_t* s1 = vol + p.uvt_slice_bytes * tc.k1;
             const float tau = tc.tau, omt = 1.0f - tau;
+            const uint32_t tau2 = pack_f16x2(tau, tau);
             const int nbx = (R3 + 3) >> 2;
-            if (p.fmt_uvt == FMT_BC1 || p.fmt_uvt == FMT_BC3) {
-                // BC1 / BC3: one whole block (both slices) per thread -- their
-                // decoders build a per-block palette, a row would redo it 4x
-                for (int pos = tid; pos < nnew * nbx; pos += kThreads) {
-                    const int bx = pos % nbx, by = n0 + pos / nbx;
-                    uint32_t t0[16], t1[16];
-                    block4_decode(p.fmt_uvt, s0, (size_t)by * nbx + bx, [&](int i, uint32_t v) { t0[i] = v; });
-                    block4_decode(p.fmt_uvt, s1, (size_t)by * nbx + bx, [&](int i, uint32_t v) { t1[i] = v; });
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float c[4];
-#pragma unroll
-                        for (int qq = 0; qq < 4; ++qq)
-                            c[qq] = (omt * u8f(t0[i], qq) + tau * u8f(t1[i], qq)) * (1.0f / 255.0f);
-                        const int gy = by * 4 + (i >> 2);
-                        NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)(bx * 4 + (i & 3)) * 8u + 8u <= ring.bytes);
-                        *reinterpret_cast<uint2*>(smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch +
-                                                  (bx * 4 + (i & 3)) * 8) =
-                            make_uint2(pack_f16x2(c[0], c[1]), pack_f16x2(c[2], c[3]));
-                    }
-                }
-                ndgi_jitter(7u);
-                __syncthreads();
-                return;
-            }
             const bool nbx_pow2 = (nbx & (nbx - 1)) == 0;
             const int nbx_log2 = __ffs(nbx) - 1;
             const int items = nnew * nbx * 4;            // (block row of a block) items
@@ -324,15 +296,12 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                 const int bx = nbx_pow2 ? pos & (nbx - 1) : pos % nbx;
                 const int by = n0 + (nbx_pow2 ? pos >> nbx_log2 : pos / nbx);
                 const int gy = by * 4 + r;                // F_uvt row
-                uint32_t q0[4], q1[4];
-                float c[4][4];
-#if NDGI_RING_F16
-                if (p.fmt_uvt == FMT_F16 && R3 % 4 == 0) {
+                uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
+                NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)min(bx * 4 + 4, R3) * 8u <= ring.bytes);
+                if (R3 % 4 == 0 && p.fmt_uvt == FMT_F16) {
                     // f16 slices: h0 + tau (h1 - h0) directly on f16x2
-                    const uint32_t tau2 = pack_f16x2(tc.tau, tc.tau);
                     const uint2* h0 = reinterpret_cast<const uint2*>(s0) + gy * R3 + bx * 4;
                     const uint2* h1 = reinterpret_cast<const uint2*>(s1) + gy * R3 + bx * 4;
-                    uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
                         const uint2 a = __ldg(h0 + x), b = __ldg(h1 + x);
@@ -341,20 +310,22 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                     }
                     continue;
                 }
-                if (fmt_block4(p.fmt_uvt) || (p.fmt_uvt == FMT_U8 && R3 % 4 == 0)) {
-                    // tau-blend on f16x2 (exact integer operands, three roundings)
+                if (R3 % 4 == 0) {
+                    // BC7 / BC1 / BC3 block rows and u8 texels: bytes -> exact f16
+                    // integers, q0 + tau (q1 - q0) and x 1/255 on f16x2 (three
+                    // roundings)
+                    uint32_t q0[4], q1[4];
                     if (fmt_block4(p.fmt_uvt)) {
                         NDGI_CHECK(by < nbx);
-                        block4_decode_row(s0, (size_t)by * nbx + bx, r, q0);
-                        block4_decode_row(s1, (size_t)by * nbx + bx, r, q1);
+                        block4_decode_row(p.fmt_uvt, s0, (size_t)by * nbx + bx, r, q0);
+                        block4_decode_row(p.fmt_uvt, s1, (size_t)by * nbx + bx, r, q1);
                     } else {
                         const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(s0) + (gy * R3 + bx * 4) / 4);
                         const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(s1) + (gy * R3 + bx * 4) / 4);
                         q0[0] = a0.x; q0[1] = a0.y; q0[2] = a0.z; q0[3] = a0.w;
                         q1[0] = a1.x; q1[1] = a1.y; q1[2] = a1.z; q1[3] = a1.w;
                     }
-                    const uint32_t tau2 = pack_f16x2(tc.tau, tc.tau), inv2 = 0x1C041C04u;   // f16x2(1/255)
-                    uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
+                    const uint32_t inv2 = 0x1C041C04u;   // f16x2(1/255)
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
                         uint32_t arg, aba, brg, bba;
@@ -366,41 +337,30 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
                     }
                     continue;
                 }
-#endif
-                if (fmt_block4(p.fmt_uvt)) {
-                    NDGI_CHECK(by < nbx);
-                    block4_decode_row(s0, (size_t)by * nbx + bx, r, q0);
-                    block4_decode_row(s1, (size_t)by * nbx + bx, r, q1);
+                // dense maps with R3 % 4 != 0 (the last block column partial):
+                // per texel in fp32
+                if (gy >= R3) continue;
+                float c[4][4];
 #pragma unroll
-                    for (int x = 0; x < 4; ++x)
+                for (int x = 0; x < 4; ++x) {
+                    const int g = gy * R3 + min(bx * 4 + x, R3 - 1);
+                    if (p.fmt_uvt == FMT_U8) {
+                        const uint32_t a0 = __ldg(reinterpret_cast<const uint32_t*>(s0) + g);
+                        const uint32_t a1 = __ldg(reinterpret_cast<const uint32_t*>(s1) + g);
 #pragma unroll
                         for (int qq = 0; qq < 4; ++qq)
-                            c[x][qq] = (omt * u8f(q0[x], qq) + tau * u8f(q1[x], qq)) * (1.0f / 255.0f);
-                } else {
-                    if (gy >= R3) continue;
+                            c[x][qq] = (omt * u8f(a0, qq) + tau * u8f(a1, qq)) * (1.0f / 255.0f);
+                    } else {
+                        const uint16_t* h0 = reinterpret_cast<const uint16_t*>(s0) + 4 * g;
+                        const uint16_t* h1 = reinterpret_cast<const uint16_t*>(s1) + 4 * g;
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        const int g = gy * R3 + min(bx * 4 + x, R3 - 1);
-                        if (p.fmt_uvt == FMT_U8) {
-                            const uint32_t a0 = __ldg(reinterpret_cast<const uint32_t*>(s0) + g);
-                            const uint32_t a1 = __ldg(reinterpret_cast<const uint32_t*>(s1) + g);
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[x][qq] = (omt * u8f(a0, qq) + tau * u8f(a1, qq)) * (1.0f / 255.0f);
-                        } else {
-                            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(s0) + 4 * g;
-                            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(s1) + 4 * g;
-#pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
-                                c[x][qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
-                        }
+                        for (int qq = 0; qq < 4; ++qq)
+                            c[x][qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
                     }
                 }
-                uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
 #pragma unroll
                 for (int x = 0; x < 4; ++x) {
                     if (bx * 4 + x >= R3) break;
-                    NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)(bx * 4 + x) * 8u + 8u <= ring.bytes);
                     *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
                         make_uint2(pack_f16x2(c[x][0], c[x][1]), pack_f16x2(c[x][2], c[x][3]));
                 }

@@ -157,6 +157,7 @@ FAST_CASES = {
     "bc1-bc5-mixed": (S.layout(1, 2, 1, "M", uvt_depth=4, line_t=8, fmt_uv="bc1", fmt_uvt="bc1", fmt_line="bc5"),
                       "mixed"),
     "H-bc3": (S.layout(1, 1, 2, "H", fmt_uv="bc3", fmt_uvt="bc3", fmt_line="bc5"), "mixed"),   # windowed F_uvt
+    "H-bc1": (S.layout(1, 1, 2, "H", fmt_uv="bc1", fmt_uvt="bc1", fmt_line="bc5"), "mixed"),   # 3-colour blocks too
 }
 
 
