@@ -149,14 +149,16 @@ __device__ __forceinline__ void block4_decode(int fmt, const uint8_t* base, size
 // ring's staging: one block row per thread, so all 128 threads take part; the
 // BC1 / BC3 palettes are rebuilt per row -- their cost is small next to a
 // chunk start with three of four warps idle at the barrier)
-__device__ __forceinline__ void block4_decode_row(int fmt, const uint8_t* base, size_t bi, int r, uint32_t (&out)[4]) {
-    if (fmt == FMT_BC1) {
+template <int FMT>
+__device__ __forceinline__ void block4_decode_row(const uint8_t* base, size_t bi, int r, uint32_t (&out)[4]) {
+    static_assert(FMT == FMT_BC7 || FMT == FMT_BC1 || FMT == FMT_BC3, "4x4 block formats");
+    if constexpr (FMT == FMT_BC1) {
         const uint2 w = __ldg(reinterpret_cast<const uint2*>(base) + bi);
         uint32_t pal[4];
         bc1_palette(w.x, false, pal);
 #pragma unroll
         for (int x = 0; x < 4; ++x) out[x] = sel4(pal, (w.y >> (8 * r + 2 * x)) & 3u);
-    } else if (fmt == FMT_BC3) {
+    } else if constexpr (FMT == FMT_BC3) {
         const uint4 raw = __ldg(reinterpret_cast<const uint4*>(base) + bi);
         uint32_t pal[4], alo, ahi;
         bc1_palette(raw.z, true, pal);

@@ -287,82 +287,100 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const float tau = tc.tau, omt = 1.0f - tau;
             const uint32_t tau2 = pack_f16x2(tau, tau);
             const int nbx = (R3 + 3) >> 2;
-            const bool nbx_pow2 = (nbx & (nbx - 1)) == 0;
-            const int nbx_log2 = __ffs(nbx) - 1;
             const int items = nnew * nbx * 4;            // (block row of a block) items
-            for (int it = tid; it < items; it += kThreads) {
-                const int r = it & 3, pos = it >> 2;
-                // nbx = 16 for the H profile: shifts instead of an integer division
-                const int bx = nbx_pow2 ? pos & (nbx - 1) : pos % nbx;
-                const int by = n0 + (nbx_pow2 ? pos >> nbx_log2 : pos / nbx);
-                const int gy = by * 4 + r;                // F_uvt row
-                uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
-                NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)min(bx * 4 + 4, R3) * 8u <= ring.bytes);
-                if (R3 % 4 == 0 && p.fmt_uvt == FMT_F16) {
-                    // f16 slices: h0 + tau (h1 - h0) directly on f16x2
-                    const uint2* h0 = reinterpret_cast<const uint2*>(s0) + gy * R3 + bx * 4;
-                    const uint2* h1 = reinterpret_cast<const uint2*>(s1) + gy * R3 + bx * 4;
+            // the item loop specialised per format (no per-item format branches)
+            auto stage_items = [&](auto fmt_c) {
+                constexpr int F = decltype(fmt_c)::value;
+                const bool nbx_pow2 = (nbx & (nbx - 1)) == 0;
+                const int nbx_log2 = __ffs(nbx) - 1;
+                for (int it = tid; it < items; it += kThreads) {
+                    const int r = it & 3, pos = it >> 2;
+                    // nbx = 16 for the H profile: shifts instead of an integer division
+                    const int bx = nbx_pow2 ? pos & (nbx - 1) : pos % nbx;
+                    const int by = n0 + (nbx_pow2 ? pos >> nbx_log2 : pos / nbx);
+                    const int gy = by * 4 + r;            // F_uvt row
+                    uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
+                    NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)min(bx * 4 + 4, R3) * 8u <= ring.bytes);
+                    if constexpr (F == FMT_F16) {
+                        // f16 slices: h0 + tau (h1 - h0) directly on f16x2
+                        const uint2* h0 = reinterpret_cast<const uint2*>(s0) + gy * R3 + bx * 4;
+                        const uint2* h1 = reinterpret_cast<const uint2*>(s1) + gy * R3 + bx * 4;
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        const uint2 a = __ldg(h0 + x), b = __ldg(h1 + x);
-                        *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
-                            make_uint2(hfma2(tau2, hsub2(b.x, a.x), a.x), hfma2(tau2, hsub2(b.y, a.y), a.y));
-                    }
-                    continue;
-                }
-                if (R3 % 4 == 0) {
-                    // BC7 / BC1 / BC3 block rows and u8 texels: bytes -> exact f16
-                    // integers, q0 + tau (q1 - q0) and x 1/255 on f16x2 (three
-                    // roundings)
-                    uint32_t q0[4], q1[4];
-                    if (fmt_block4(p.fmt_uvt)) {
-                        NDGI_CHECK(by < nbx);
-                        block4_decode_row(p.fmt_uvt, s0, (size_t)by * nbx + bx, r, q0);
-                        block4_decode_row(p.fmt_uvt, s1, (size_t)by * nbx + bx, r, q1);
+                        for (int x = 0; x < 4; ++x) {
+                            const uint2 a = __ldg(h0 + x), b = __ldg(h1 + x);
+                            *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
+                                make_uint2(hfma2(tau2, hsub2(b.x, a.x), a.x), hfma2(tau2, hsub2(b.y, a.y), a.y));
+                        }
                     } else {
-                        const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(s0) + (gy * R3 + bx * 4) / 4);
-                        const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(s1) + (gy * R3 + bx * 4) / 4);
-                        q0[0] = a0.x; q0[1] = a0.y; q0[2] = a0.z; q0[3] = a0.w;
-                        q1[0] = a1.x; q1[1] = a1.y; q1[2] = a1.z; q1[3] = a1.w;
-                    }
-                    const uint32_t inv2 = 0x1C041C04u;   // f16x2(1/255)
+                        // BC7 / BC1 / BC3 block rows and u8 texels: bytes -> exact
+                        // f16 integers, q0 + tau (q1 - q0) and x 1/255 on f16x2
+                        // (three roundings)
+                        uint32_t q0[4], q1[4];
+                        if constexpr (F == FMT_U8) {
+                            const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(s0) + (gy * R3 + bx * 4) / 4);
+                            const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(s1) + (gy * R3 + bx * 4) / 4);
+                            q0[0] = a0.x; q0[1] = a0.y; q0[2] = a0.z; q0[3] = a0.w;
+                            q1[0] = a1.x; q1[1] = a1.y; q1[2] = a1.z; q1[3] = a1.w;
+                        } else {
+                            NDGI_CHECK(by < nbx);
+                            block4_decode_row<F>(s0, (size_t)by * nbx + bx, r, q0);
+                            block4_decode_row<F>(s1, (size_t)by * nbx + bx, r, q1);
+                        }
+                        const uint32_t inv2 = 0x1C041C04u;   // f16x2(1/255)
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        uint32_t arg, aba, brg, bba;
-                        u8x4_to_h2(q0[x], arg, aba);
-                        u8x4_to_h2(q1[x], brg, bba);
-                        *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
-                            make_uint2(hmul2(hfma2(tau2, hsub2(brg, arg), arg), inv2),
-                                       hmul2(hfma2(tau2, hsub2(bba, aba), aba), inv2));
+                        for (int x = 0; x < 4; ++x) {
+                            uint32_t arg, aba, brg, bba;
+                            u8x4_to_h2(q0[x], arg, aba);
+                            u8x4_to_h2(q1[x], brg, bba);
+                            *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
+                                make_uint2(hmul2(hfma2(tau2, hsub2(brg, arg), arg), inv2),
+                                           hmul2(hfma2(tau2, hsub2(bba, aba), aba), inv2));
+                        }
                     }
-                    continue;
                 }
+            };
+            if (R3 % 4 == 0) {
+                switch (p.fmt_uvt) {   // CTA-uniform
+                    case FMT_BC7: stage_items(std::integral_constant<int, FMT_BC7>{}); break;
+                    case FMT_BC1: stage_items(std::integral_constant<int, FMT_BC1>{}); break;
+                    case FMT_BC3: stage_items(std::integral_constant<int, FMT_BC3>{}); break;
+                    case FMT_U8: stage_items(std::integral_constant<int, FMT_U8>{}); break;
+                    default: stage_items(std::integral_constant<int, FMT_F16>{}); break;
+                }
+            } else {
                 // dense maps with R3 % 4 != 0 (the last block column partial):
                 // per texel in fp32
-                if (gy >= R3) continue;
-                float c[4][4];
+                for (int it = tid; it < items; it += kThreads) {
+                    const int r = it & 3, pos = it >> 2;
+                    const int bx = pos % nbx, by = n0 + pos / nbx;
+                    const int gy = by * 4 + r;
+                    if (gy >= R3) continue;
+                    uint8_t* dst = smem + L.uvt + (uint32_t)(gy & (ring.rows - 1)) * ring.pitch;
+                    NDGI_CHECK((uint32_t)((gy & (ring.rows - 1)) * ring.pitch) + (uint32_t)min(bx * 4 + 4, R3) * 8u <= ring.bytes);
+                    float c[4][4];
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    const int g = gy * R3 + min(bx * 4 + x, R3 - 1);
-                    if (p.fmt_uvt == FMT_U8) {
-                        const uint32_t a0 = __ldg(reinterpret_cast<const uint32_t*>(s0) + g);
-                        const uint32_t a1 = __ldg(reinterpret_cast<const uint32_t*>(s1) + g);
+                    for (int x = 0; x < 4; ++x) {
+                        const int g = gy * R3 + min(bx * 4 + x, R3 - 1);
+                        if (p.fmt_uvt == FMT_U8) {
+                            const uint32_t a0 = __ldg(reinterpret_cast<const uint32_t*>(s0) + g);
+                            const uint32_t a1 = __ldg(reinterpret_cast<const uint32_t*>(s1) + g);
 #pragma unroll
-                        for (int qq = 0; qq < 4; ++qq)
-                            c[x][qq] = (omt * u8f(a0, qq) + tau * u8f(a1, qq)) * (1.0f / 255.0f);
-                    } else {
-                        const uint16_t* h0 = reinterpret_cast<const uint16_t*>(s0) + 4 * g;
-                        const uint16_t* h1 = reinterpret_cast<const uint16_t*>(s1) + 4 * g;
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[x][qq] = (omt * u8f(a0, qq) + tau * u8f(a1, qq)) * (1.0f / 255.0f);
+                        } else {
+                            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(s0) + 4 * g;
+                            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(s1) + 4 * g;
 #pragma unroll
-                        for (int qq = 0; qq < 4; ++qq)
-                            c[x][qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
+                            for (int qq = 0; qq < 4; ++qq)
+                                c[x][qq] = omt * half_bits_to_float(__ldg(h0 + qq)) + tau * half_bits_to_float(__ldg(h1 + qq));
+                        }
                     }
-                }
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    if (bx * 4 + x >= R3) break;
-                    *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
-                        make_uint2(pack_f16x2(c[x][0], c[x][1]), pack_f16x2(c[x][2], c[x][3]));
+                    for (int x = 0; x < 4; ++x) {
+                        if (bx * 4 + x >= R3) break;
+                        *reinterpret_cast<uint2*>(dst + (bx * 4 + x) * 8) =
+                            make_uint2(pack_f16x2(c[x][0], c[x][1]), pack_f16x2(c[x][2], c[x][3]));
+                    }
                 }
             }
             ndgi_jitter(7u);
