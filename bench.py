@@ -436,6 +436,10 @@ def run_gpu(args, rank, world, dist):
                        "ms_per_step": ms2, "steps": a2.steps}
             del ctx2, th2, out2
 
+    vt_sharded = None
+    if dist is not None and workload == "c4" and not args.no_vt and not dec.stub and not args.scene_tiles:
+        vt_sharded = vt_sharded_leg(dec, dist, rank, world, ctx, scene_lay["num_tiles"])
+
     # ---------------- end to end through the host-buffer API (Theta H2D + decode + D2H)
     e2e = None
     if not dec.stub:
@@ -479,12 +483,55 @@ def run_gpu(args, rank, world, dist):
         "config": _workload_config(world, tiles_per_rank, workload),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 0 if dec.stub else args.steps,
         "clocks": clocks, **({"comm": comm} if comm else {}), "verify": verify, "weak_c2": weak_c2,
-        "texunit": texunit, **legs,
+        "texunit": texunit, **legs, **({"vt_sharded_us": vt_sharded} if vt_sharded else {}),
         "step_ms_p50": statistics.median(step_ms), "step_ms_max": max(step_ms),
     }
     if dec.stub:
         line["stub"] = "StubDecoder (CPU launcher test, not a measurement)"
     print(json.dumps(line), flush=True)
+
+
+def vt_sharded_leg(dec, dist, rank, world, ctx, n_scene):
+    """VT frames served by N GPUs (parallel.split_requests):
+    config 3's request stream over config 4's scene, each frame's requests split
+    by the owner rule k % N; rank g decodes its share from its shard (local
+    index k // N) with one ndgi_decode_tiles call.  Per frame, the device time
+    of every rank's call (launches queued back to back, an event pair per
+    frame) and the MAX over ranks; p50 / p99 of that max.  Every rank reaches
+    the all_reduce even if its decode fails (NaN times, reported)."""
+    from paper_2604_12625_b200 import parallel as par
+    ndgi, torch = dec.ndgi, dec.torch
+    stream = dec.stream
+    res = {}
+    for n in (8, 32, 128, 512):
+        if n > n_scene:
+            continue
+        frames = S.vt_batches(n_scene, n, 16 + 64, 3000)
+        times = np.full(len(frames), np.nan)
+        err = None
+        try:
+            cache = torch.empty((n, 136, 136, 4), dtype=torch.uint8, device=dec.device)
+            work = []
+            for ids, t in frames:
+                _, loc = par.local_requests(ids, world, rank)
+                work.append((torch.from_numpy(loc.astype(np.int32)).to(dec.device), len(loc), t))
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(frames) + 1)]
+            torch.cuda._sleep(int(2e-3 * 1.9e9))
+            for f, (loc, m, t) in enumerate(work):
+                evs[f].record(stream)
+                if m:
+                    ndgi.ndgi_decode_tiles(ctx, loc, None, m, n, t, cache, "rgba8", "fast", stream)
+            evs[-1].record(stream)
+            evs[-1].synchronize()
+            times = np.array([evs[f].elapsed_time(evs[f + 1]) * 1e3 for f in range(len(frames))])
+        except Exception as exc:  # pragma: no cover - reported, not hidden
+            err = repr(exc)
+        mx = np.sort(par.max_over_ranks_vec(times, dist, dec.device)[16:])
+        res[str(n)] = {"device_p50": float(mx[len(mx) // 2]), "device_p99": float(mx[min(len(mx) - 1, int(0.99 * len(mx)))]),
+                       "requests_per_rank_avg": n / world, **({"error": err} if err else {})}
+    res["how"] = ("per frame: max over ranks of the device time of each rank's ndgi_decode_tiles call for its "
+                  "k % N share (event pair per frame, launches queued ahead); p50/p99 over 64 frames")
+    return res
 
 
 def e2e_leg(dec, ctx, theta, per_t, tiles_per_rank, world, dist, args):

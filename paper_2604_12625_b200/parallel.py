@@ -31,6 +31,23 @@ def split_requests(tile_ids: np.ndarray, world: int) -> list[np.ndarray]:
     return [np.nonzero(tile_ids % world == g)[0] for g in range(world)]
 
 
+def local_requests(tile_ids: np.ndarray, world: int, rank: int) -> tuple[np.ndarray, np.ndarray]:
+    """A frame's requests served by `rank`: (positions in the frame, local tile
+    indices into the rank's shard).  shard_tiles(n, world, rank)[k // world] == k
+    for every k owned by the rank."""
+    tile_ids = np.asarray(tile_ids, dtype=np.int64)
+    pos = split_requests(tile_ids, world)[rank]
+    return pos, tile_ids[pos] // world
+
+
+def max_over_ranks_vec(values, dist, device=None) -> np.ndarray:
+    """Element-wise MAX of a per-rank float vector over the process group."""
+    import torch
+    t = torch.as_tensor(np.asarray(values, dtype=np.float64), device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().numpy()
+
+
 def tile_digests(tiles_u8) -> "torch.Tensor":
     """Order-independent 64-bit digest per decoded tile.
 

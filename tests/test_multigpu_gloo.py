@@ -40,6 +40,15 @@ def test_shard_rule():
     parts = par.split_requests(ids, 2)
     assert sorted(np.concatenate(parts).tolist()) == list(range(5))
     assert all((ids[p] % 2 == g).all() for g, p in enumerate(parts))
+    # a rank's share of a frame indexes its own shard: shard[k // N] == k
+    for world in (2, 3, 8):
+        frame = np.random.default_rng(world).choice(16384, 512, replace=False)
+        served = []
+        for g in range(world):
+            pos, loc = par.local_requests(frame, world, g)
+            assert (par.shard_tiles(16384, world, g)[loc] == frame[pos]).all()
+            served += pos.tolist()
+        assert sorted(served) == list(range(512))
 
 
 def _worker(rank, world, port, out):
@@ -56,8 +65,9 @@ def _worker(rank, world, port, out):
     full = par.gather_digests(mine, dg, lay["num_tiles"], dist)
     sid, stl = par.gather_tile_sample(mine, q, [0, len(mine) - 1], dist)
     t = par.max_over_ranks(1.5 + rank, dist)
+    tv = par.max_over_ranks_vec([1.0 + rank, 5.0 - rank, 2.0], dist)
     if rank == 0:
-        out.put((full.tolist(), t, sid.tolist(), stl))
+        out.put((full.tolist(), t, sid.tolist(), stl, tv.tolist()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -71,11 +81,12 @@ def test_sharded_digests_match_single_process():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    full, t, sid, stl = q.get(timeout=120)
+    full, t, sid, stl, tv = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert t == 2.5                                          # max over ranks
+    assert tv == [2.0, 5.0, 2.0]                             # element-wise
     lay = S.layout(1, 5, 1, "M", core=8, border=2, uvt_res=4, uvt_depth=2, line_res=4, line_t=3, hidden=4)
     th = S.make_theta(lay, 77, "mixed")
     y = oracle.Model(lay, th).decode_tiles(np.arange(5), 0.4)
