@@ -365,6 +365,10 @@ def test_bad_ids_and_arguments():
         with pytest.raises(ndgi.NdgiError) as e:
             ndgi.ndgi_decode_tiles(ctx, ids, None, 4, 4, t, o)
         assert e.value.status == ndgi.ERR_RANGE
+    # an empty batch is an argument error (ndgi.h), not a launch
+    with pytest.raises(ndgi.NdgiError) as e:
+        ndgi.ndgi_decode_tiles(ctx, ids, None, 0, 4, 0.5, o)
+    assert e.value.status == ndgi.ERR_ARG
     lay_bad = dict(lay, hidden=8)
     th_bad = S.make_theta(lay_bad, 1)
     ctx_bad = _load(lay_bad, th_bad)
