@@ -456,6 +456,14 @@ NDGI_API ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_i
  * read with .pack::16b (8 words).  Synchronous. */
 NDGI_API ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out);
 
+/* Rounding probe of the f16-accumulator MMA: `ctas` CTAs x `iters` random
+ * M128 N16 K16 problems (A in TMEM, B in smem; f16 operands up to |x| 256),
+ * each issued once with an fp32 D and once with an f16 D; *mismatches counts
+ * the f16x2 output pairs where the f16 D differs from cvt.rn.f16x2 of the
+ * fp32 D, *pairs the pairs compared.  Synchronous.  Errors: ARG, CUDA. */
+NDGI_API ndgi_status ndgi_debug_f16d_probe(uint32_t seed, uint32_t iters, uint32_t ctas, uint64_t* mismatches,
+                                           uint64_t* pairs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,7 @@ _SIGS = {
     "ndgi_debug_null_launch": (_I, [_P]),
     "ndgi_debug_launch_probe": (_I, [_I, _P]),
     "ndgi_debug_tmem_f16_probe": (_I, [_P]),
+    "ndgi_debug_f16d_probe": (_I, [_U32, _U32, _U32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "ndgi_vt_create": (_I, [_U32, _U32, _U32, C.POINTER(C.c_void_p)]),
     "ndgi_vt_free": (_I, [_P]),
     "ndgi_vt_request": (_I, [_P, _P, _U32, _F, _P, _P, C.POINTER(_U32), C.POINTER(_F), C.POINTER(C.c_int32)]),
@@ -487,3 +488,11 @@ class Trainer:
             self.close()
         except Exception:
             pass
+
+
+def ndgi_debug_f16d_probe(seed: int = 1, iters: int = 64, ctas: int = 148) -> tuple[int, int]:
+    """(mismatching f16x2 pairs, pairs compared): f16-D MMA vs cvt.rn of the fp32-D MMA."""
+    m, t = C.c_uint64(0), C.c_uint64(0)
+    _check(_lib.ndgi_debug_f16d_probe(int(seed), int(iters), int(ctas), C.byref(m), C.byref(t)),
+           "ndgi_debug_f16d_probe")
+    return int(m.value), int(t.value)

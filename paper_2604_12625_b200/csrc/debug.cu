@@ -312,3 +312,100 @@ cudaError_t tmem_f16_probe(uint32_t* host_out) {
     return e;
 }
 }  // namespace ndgi
+
+// ---------------------------------------------------------------------------
+// Rounding of an f16-D MMA (kind::f16, M128 N16 K16, one instruction) against
+// the fp32-D MMA of the same operands rounded once with cvt.rn.f16x2: random A
+// (TMEM) and B (smem) per iteration and CTA; counts the output pairs that
+// differ.  Zero means the instruction accumulates its K = 16 products at fp32
+// or better and rounds to f16 once, to nearest even -- what the fused kernel's
+// fp32-D layer 1 plus its cvt.rn packing computes.
+// ---------------------------------------------------------------------------
+namespace ndgi {
+namespace {
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+}
+// a float in [-r, r) from a hash, rounded to f16 (and some exact large / tiny values)
+__device__ __forceinline__ float hval(uint32_t h, float r) {
+    const float u = (float)(h >> 8) * (1.0f / 16777216.0f);
+    const uint32_t sel = h & 15u;
+    float v = (2.0f * u - 1.0f) * r;
+    if (sel == 0) v *= 64.0f;            // large magnitudes: cancellation between terms
+    if (sel == 1) v *= 1.0f / 1024.0f;   // small ones
+    return __half2float(__float2half_rn(v));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128, 1) f16d_probe_kernel(uint32_t seed, uint32_t iters,
+                                                            unsigned long long* mism, unsigned long long* total) {
+    __shared__ __align__(1024) __half sB[16 * 16];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t b = ptx::smem_addr(&bar);
+    if (tid == 0) { ptx::mbar_init(b, 1); ptx::fence_mbar_init(); }
+    if (warp == 0) ptx::tmem_alloc<64>(ptx::smem_addr(&tslot));
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tslot, lane = tmem + ((uint32_t)(warp * 32) << 16);
+    unsigned long long bad = 0;
+    for (uint32_t it = 0; it < iters; ++it) {
+        const uint32_t key = hash32(seed ^ hash32(blockIdx.x * 0x9e3779b9u + it));
+        for (int e = tid; e < 256; e += 128) {   // B K-major no-swizzle [n/8][k/8][n%8][k%8]
+            const int n = e >> 4, k = e & 15;
+            const int off = (((n >> 3) * 2 + (k >> 3)) << 6) + ((n & 7) << 3) + (k & 7);
+            sB[off] = __float2half_rn(hval(hash32(key + 7919u * (uint32_t)e), 1.0f));
+        }
+        uint32_t a[8];
+        for (int c = 0; c < 8; ++c)
+            a[c] = pack_f16x2(hval(hash32(key ^ (0x1000u + tid * 16 + 2 * c)), 4.0f),
+                              hval(hash32(key ^ (0x1000u + tid * 16 + 2 * c + 1)), 4.0f));
+        ptx::tmem_st_x8(lane, a);
+        ptx::tmem_wait_st();
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            ptx::tc_fence_after();
+            const uint64_t bd = ptx::smem_desc_kmajor(ptx::smem_addr(sB), 128u, 256u);
+            ptx::mma_f16_ts(tmem + 16, tmem, bd, ptx::idesc_f16_f32(128, 16), 0u);
+            ptx::mma_f16_ts(tmem + 32, tmem, bd, ptx::idesc_f16_f16(128, 16), 0u);
+            ptx::mma_commit(b);
+        }
+        ptx::mbar_wait_fast(b, it & 1u);
+        ptx::tc_fence_after();
+        uint32_t d[16], pk[8];
+        ptx::tmem_ld_x16(lane + 16, d);
+        ptx::tmem_ld_x8_pack16(lane + 32, pk);
+        ptx::tmem_wait_ld();
+        for (int c = 0; c < 8; ++c)
+            bad += pack_f16x2(__uint_as_float(d[2 * c]), __uint_as_float(d[2 * c + 1])) != pk[c];
+        ptx::tc_fence_before();
+        __syncthreads();
+    }
+    atomicAdd(mism, bad);
+    if (tid == 0) atomicAdd(total, (unsigned long long)iters * 128ull * 8ull);
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<64>(tmem);
+}
+
+cudaError_t f16d_probe(uint32_t seed, uint32_t iters, uint32_t ctas, unsigned long long* mism,
+                       unsigned long long* total) {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 2 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    cudaMemset(d, 0, 2 * sizeof(unsigned long long));
+    f16d_probe_kernel<<<ctas, 128>>>(seed, iters, d, d + 1);
+    e = cudaDeviceSynchronize();
+    unsigned long long h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    *mism = h[0];
+    *total = h[1];
+    return e;
+}
+}  // namespace ndgi

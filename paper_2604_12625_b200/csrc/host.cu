@@ -47,6 +47,8 @@ cudaError_t null_launch(cudaStream_t s, int kind);
 int fused_f16acc();
 cudaError_t mma_latency(uint32_t iters, double* cycles_per_iter);
 cudaError_t tmem_f16_probe(uint32_t* host_out);
+cudaError_t f16d_probe(uint32_t seed, uint32_t iters, uint32_t ctas, unsigned long long* mism,
+                       unsigned long long* total);
 }  // namespace ndgi
 
 struct ndgi_ctx {
@@ -872,6 +874,16 @@ ndgi_status ndgi_debug_mma_latency(uint32_t iters, double* cycles_per_iter) {
     if (!cycles_per_iter || !iters) return fail(NDGI_ERR_ARG, "bad arguments");
     cudaError_t e = ndgi::mma_latency(iters, cycles_per_iter);
     return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "mma latency");
+}
+
+ndgi_status ndgi_debug_f16d_probe(uint32_t seed, uint32_t iters, uint32_t ctas, uint64_t* mismatches,
+                                  uint64_t* pairs) {
+    if (!mismatches || !pairs || !iters || !ctas) return fail(NDGI_ERR_ARG, "bad arguments");
+    unsigned long long m = 0, t = 0;
+    cudaError_t e = ndgi::f16d_probe(seed, iters, ctas, &m, &t);
+    *mismatches = m;
+    *pairs = t;
+    return e == cudaSuccess ? NDGI_OK : cuda_fail(e, "f16-D probe");
 }
 
 ndgi_status ndgi_debug_tmem_f16_probe(uint32_t* host_out) {
