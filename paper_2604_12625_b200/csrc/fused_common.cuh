@@ -109,7 +109,7 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
     o = (o + 15) & ~15u;
     s.rowtab = o; o += (uint32_t)(C * 16);            // per core row: y0*R3, y1*R3, fy (f16x2), V_vt (f16x2)
     s.colc = o; o += (uint32_t)(C * 16);              // per core column: x0 / x1 slice byte offsets, fx (f16x2), V_ut
-    s.cnt = o; o += 8 * 4;                            // (unused)
+    s.cnt = o; o += 8 * 4;                            // [0]: the CTA's claimed next unit (KParams::sched)
     s.bars = o; o += 8 * 8;                           // d_ready
     s.tmem_slot = o; o += 8;
     o = (o + 127) & ~127u;

@@ -14,3 +14,11 @@ extern "C" __attribute__((visibility("default"))) int ndgi_debug_timeline(unsign
     return (int)cudaMemcpyFromSymbol(out16, ndgi::g_ndgi_timeline, 16 * sizeof(unsigned long long));
 }
 #endif
+
+#if NDGI_RESIDENCY
+// diagnostic builds only: per-CTA (SM id, entry, after TMEM allocation, exit) of
+// the last (h = 16, C = 128, BC7) fused launch
+extern "C" __attribute__((visibility("default"))) int ndgi_debug_residency(unsigned long long* out, int nblocks) {
+    return (int)cudaMemcpyFromSymbol(out, ndgi::g_ndgi_res, (size_t)(nblocks < 4096 ? nblocks : 4096) * 4 * sizeof(unsigned long long));
+}
+#endif

@@ -53,6 +53,31 @@ __device__ unsigned long long g_ndgi_timeline[16];
 #define NDGI_STAMP(i) do {} while (0)
 #endif
 
+// NDGI_RESIDENCY=1 (diagnostic builds only): per CTA (blockIdx.x < 4096) the SM
+// id and %globaltimer at entry, after the TMEM allocation and at exit ->
+// g_ndgi_res[block][4]
+#ifndef NDGI_RESIDENCY
+#define NDGI_RESIDENCY 0
+#endif
+#if NDGI_RESIDENCY
+__device__ unsigned long long g_ndgi_res[4096][4];
+__device__ __forceinline__ void ndgi_res_stamp(int i) {
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_ndgi_res[blockIdx.x][i] = t;
+        if (i == 1) {
+            unsigned int sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_ndgi_res[blockIdx.x][0] = sm;
+        }
+    }
+}
+#define NDGI_RES(i) ndgi_res_stamp(i)
+#else
+#define NDGI_RES(i) do {} while (0)
+#endif
+
 
 
 // FULL8: decode_full with RGBA8 output (the page-cache hot path): no border,
@@ -74,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     bool tl_on = true;
 #endif
     NDGI_STAMP(0);
+    NDGI_RES(1);
     const FusedSmem L = fused_smem_layout<H>(C, p.R3);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t bars = ptx::smem_addr(smem + L.bars);
@@ -96,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     NDGI_STAMP(1);
+    NDGI_RES(2);
 
     const int B = p.B, P = p.P, R3 = p.R3;
     const float sc3 = (float)R3 * (1.0f / (float)C);   // F_uvt texels per core texel
@@ -120,7 +147,16 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 
     uint32_t dph = 0u;   // d_ready phase
 
-    for (uint32_t unit = blockIdx.x; unit < p.units; unit += gridDim.x) {
+    // unit scheduling: CTA b starts with unit b; with p.sched (launches with
+    // more units than CTAs) thread 0 claims the next unit with one atomic at
+    // the start of the current unit's last chunk (its latency hidden behind
+    // that chunk; the claim is read after the chunk's CTA barriers), else the
+    // static split unit += gridDim.x
+    volatile uint32_t* const s_next = reinterpret_cast<volatile uint32_t*>(smem + L.cnt);
+    auto claim_next = [&]() {
+        if (tid == 0) *s_next = gridDim.x + atomicAdd(p.sched, 1u);
+    };
+    for (uint32_t unit = blockIdx.x; unit < p.units; unit = p.sched ? *s_next : unit + gridDim.x) {
         const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
         const uint32_t rq = unit / (uint32_t)p.strips_per_tile;
         const int ti = (int)(rq / p.n_req);
@@ -140,6 +176,11 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const uint32_t slot = p.slots ? __ldg(p.slots + r) : r;
             if (id >= (uint32_t)p.num_tiles || slot >= p.num_slots) {
                 if (strip == 0 && tid == 0) atomicAdd(p.err, 1u);
+                if (p.sched) {
+                    __syncthreads();   // every thread has read the previous claim
+                    claim_next();
+                    __syncthreads();
+                }
                 continue;  // uniform across the CTA
             }
             k = (int)id;
@@ -554,6 +595,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         const int crows = p.strip_rows < chunk_rows ? p.strip_rows : chunk_rows;
         const int chunk_items = crows * BPR;
         for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
+        if (p.sched && c0 + chunk_items >= nitems) claim_next();
         if constexpr (WIN) stage_ring(j_begin + c0 / BPR, crows);
         NDGI_STAMP(5);
         if (FMT_UV == FMT_BC7 || FMT_UV == FMT_BC1 || FMT_UV == FMT_BC3) decode_chunk(j_begin + c0 / BPR, crows);
@@ -584,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc<Cfg::TM_COLS>(tmem);
+    NDGI_RES(3);
 #if NDGI_TIMELINE
     tl_on = true;
 #endif
@@ -674,6 +717,17 @@ cudaError_t launch_fused_t(const KParams& p, int num_sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const uint32_t cap = (uint32_t)(num_sms * occ);
     const uint32_t grid = p.units < cap ? p.units : cap;
+#ifndef NDGI_STATIC_UNITS   // experiment builds only: 1 = the round-2 static split
+#define NDGI_STATIC_UNITS 0
+#endif
+    if (grid == p.units || !p.sched || NDGI_STATIC_UNITS) {   // one unit per CTA (small VT batches): static, no counter
+        KParams q = p;
+        q.sched = nullptr;
+        kern<<<grid, kThreads, smem, s>>>(q);
+        return cudaGetLastError();
+    }
+    e = cudaMemsetAsync(p.sched, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
     kern<<<grid, kThreads, smem, s>>>(p);
     return cudaGetLastError();
 }

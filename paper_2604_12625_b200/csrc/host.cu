@@ -3,6 +3,7 @@
 // this boundary; every entry point returns an ndgi_status and never throws.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -57,6 +58,11 @@ struct ndgi_ctx {
     int device;
     int num_sms;
     uint32_t* d_err;
+    // dynamic-scheduling counters of the fused kernel (KParams::sched): a ring
+    // of kSchedSlots, one per launch, so launches in flight on different
+    // streams do not share one (each is zeroed on the launch's stream first)
+    uint32_t* d_sched;
+    mutable std::atomic<uint32_t> sched_seq;
     uint8_t* wpack;   // prepacked tcgen05 B operands per tile (FAST layouts), owned
     // NDGI_MODE_FAST_TEXUNIT: per-atlas BC7 F_uv textures, built on first use
     std::mutex tex_mu;
@@ -192,6 +198,7 @@ void fill_common(const ndgi_ctx* ctx, ndgi::KParams& p) {
     p.line_tile_bytes = map2d_bytes(L.fmt_line, L.line_res, L.line_t, 2);
     p.mlp_tile_elems = mlp_elems(L.hidden);
     p.err = ctx->d_err;
+    p.sched = ctx->d_sched + (ctx->sched_seq.fetch_add(1, std::memory_order_relaxed) % ndgi::kSchedSlots);
 }
 
 ndgi_status check_t(float t) {
@@ -348,6 +355,13 @@ ndgi_status ndgi_load(const ndgi_layout* layout, const ndgi_params* params, int 
         return cuda_fail(e, "cudaMalloc(error counter)");
     }
     cudaMemset(c->d_err, 0, sizeof(uint32_t));
+    e = cudaMalloc(&c->d_sched, ndgi::kSchedSlots * sizeof(uint32_t));
+    if (e != cudaSuccess) {
+        cudaFree(c->d_err);
+        delete c;
+        return cuda_fail(e, "cudaMalloc(scheduling counters)");
+    }
+    cudaMemset(c->d_sched, 0, ndgi::kSchedSlots * sizeof(uint32_t));
     int fast = 0;
     validate(layout, &fast);
     if (fast) {
@@ -356,6 +370,7 @@ ndgi_status ndgi_load(const ndgi_layout* layout, const ndgi_params* params, int 
         e = cudaMalloc(&c->wpack, tb * layout->num_tiles);
         if (e != cudaSuccess) {
             cudaFree(c->d_err);
+            cudaFree(c->d_sched);
             delete c;
             return cuda_fail(e, "cudaMalloc(prepacked weights)");
         }
@@ -365,6 +380,7 @@ ndgi_status ndgi_load(const ndgi_layout* layout, const ndgi_params* params, int 
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(c->d_err);
+        cudaFree(c->d_sched);
         if (c->wpack) cudaFree(c->wpack);
         delete c;
         return cuda_fail(e, "ndgi_load prepack / sync");
@@ -821,6 +837,7 @@ ndgi_status ndgi_free(ndgi_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaDeviceSynchronize();
     cudaFree(ctx->d_err);
+    cudaFree(ctx->d_sched);
     if (ctx->wpack) cudaFree(ctx->wpack);
     if (ctx->tex_ready) ndgi::uv_textures_free((int)ctx->L.atlases, ctx->uvarr, ctx->uvtex);
     for (int i = 0; i < 2; ++i) {

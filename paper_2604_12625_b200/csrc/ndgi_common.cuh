@@ -16,6 +16,7 @@ enum : int { GELU_ERF = 0, GELU_TANH = 1 };
 enum : int { BORDER_MIRROR = 0, BORDER_EVAL_CLAMP = 1 };
 
 constexpr int kMaxT = 32;   // query times per launch
+constexpr uint32_t kSchedSlots = 1024;   // dynamic-scheduling counters per context (KParams::sched)
 
 struct TConst {
     float t;
@@ -59,6 +60,12 @@ struct KParams {
     int strip_rows;             // rows of core per work unit
     int strips_per_tile;
     uint32_t units;             // nt * n_req * strips_per_tile
+    // dynamic unit scheduling (fused kernel, units > grid): a zeroed counter of
+    // this launch; CTA b takes unit b, then gridDim.x + atomicAdd(sched, 1)
+    // until the units run out -- co-resident CTAs progress at different rates
+    // (warp-scheduler priority), so a static unit += gridDim.x split leaves the
+    // SMs half-occupied for the second half of the launch
+    uint32_t* sched;
 };
 
 // shading-side sampling (sample_kernel.cu)
