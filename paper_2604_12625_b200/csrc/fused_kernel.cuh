@@ -157,8 +157,18 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         if (tid == 0) *s_next = gridDim.x + atomicAdd(p.sched, 1u);
     };
     for (uint32_t unit = blockIdx.x; unit < p.units; unit = p.sched ? *s_next : unit + gridDim.x) {
-        const int strip = (int)(unit % (uint32_t)p.strips_per_tile);
-        const uint32_t rq = unit / (uint32_t)p.strips_per_tile;
+        int strip, strip_rows;
+        uint32_t rq;
+        if (unit < p.tail_from) {
+            strip = (int)(unit % (uint32_t)p.strips_per_tile);
+            rq = unit / (uint32_t)p.strips_per_tile;
+            strip_rows = p.strip_rows;
+        } else {   // the launch's tail: shorter units (KParams::tail_from)
+            const uint32_t v = unit - p.tail_from;
+            strip = (int)(v % (uint32_t)p.tail_strips);
+            rq = p.tail_from / (uint32_t)p.strips_per_tile + v / (uint32_t)p.tail_strips;
+            strip_rows = C / p.tail_strips;
+        }
         const int ti = (int)(rq / p.n_req);
         const uint32_t r = rq % p.n_req;
         const TConst& tc = p.tc[ti];
@@ -187,8 +197,8 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             row_pitch = (size_t)P;
             out_base = ((size_t)slot * P + B) * P + B;
         }
-        const int nitems = p.strip_rows * BPR;     // 128-texel blocks of this unit (multiple of S)
-        const int j_begin = strip * p.strip_rows;
+        const int nitems = strip_rows * BPR;       // 128-texel blocks of this unit (multiple of S)
+        const int j_begin = strip * strip_rows;
 
         // ---- a2: tile parameters -> shared memory -----------------------------------
         ndgi_jitter(1u);
@@ -592,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
 
         // S items per step; item n = (row j_begin + n / BPR, block n % BPR)
         // strips are whole F_uv chunks, or (small batches) 4..8-row strips
-        const int crows = p.strip_rows < chunk_rows ? p.strip_rows : chunk_rows;
+        const int crows = strip_rows < chunk_rows ? strip_rows : chunk_rows;
         const int chunk_items = crows * BPR;
         for (int c0 = 0; c0 < nitems; c0 += chunk_items) {
         if (p.sched && c0 + chunk_items >= nitems) claim_next();

@@ -227,6 +227,23 @@ void choose_strips(ndgi::KParams& p, int num_sms, int min_rows) {
     p.strips_per_tile = s;
     p.strip_rows = C / s;
     p.units = (uint32_t)((uint64_t)p.nt * p.n_req * s);
+    p.tail_from = p.units;
+    p.tail_strips = 1;
+    // whole-tile units over several rounds of resident CTAs (decode_full, large
+    // batches): the last ~one round of requests as 4 strips each, so the final
+    // dynamically claimed units (KParams::sched) are a quarter as long and the
+    // SMs stay full until closer to the end
+    const uint64_t resident = (uint64_t)num_sms * ndgi::fused_ctas_per_sm(p.H);
+#ifndef NDGI_TAIL_STRIPS   // experiment builds: 1 = no finer tail
+#define NDGI_TAIL_STRIPS 4
+#endif
+    constexpr int kTail = NDGI_TAIL_STRIPS;
+    if (kTail > 1 && s == 1 && req > 2 * resident && (C / kTail) % chunk_rows == 0) {
+        const uint64_t tail = resident;
+        p.tail_from = (uint32_t)(req - tail);
+        p.tail_strips = kTail;
+        p.units = (uint32_t)(req - tail + kTail * tail);
+    }
 }
 
 ndgi_status launch(ndgi_ctx* ctx, ndgi::KParams& p, ndgi_mode mode, cudaStream_t s) {

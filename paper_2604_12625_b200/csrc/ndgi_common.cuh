@@ -59,7 +59,12 @@ struct KParams {
     // work decomposition of the fused kernel
     int strip_rows;             // rows of core per work unit
     int strips_per_tile;
-    uint32_t units;             // nt * n_req * strips_per_tile
+    uint32_t units;             // tail_from + tail_strips * (requests past it)
+    // the launch's last requests are split finer (tail_strips strips each) so
+    // the final dynamically claimed units are short: units >= tail_from are
+    // (request tail_req0 + v / tail_strips, strip v % tail_strips), v = unit - tail_from
+    uint32_t tail_from;
+    int tail_strips;
     // dynamic unit scheduling (fused kernel, units > grid): a zeroed counter of
     // this launch; CTA b takes unit b, then gridDim.x + atomicAdd(sched, 1)
     // until the units run out -- co-resident CTAs progress at different rates

@@ -464,6 +464,20 @@ def test_c2_bench_launch_all_texels_of_one_time():
             assert np.abs(g.astype(int) - e.astype(int)).max() <= 1
 
 
+@pytest.mark.parametrize("cell", ["c2", "c5:H:bc7"])
+def test_dynamic_schedule_and_tail_strips_equal_single_calls(cell):
+    """A 24-t decode_full_batch of 1,024 tiles has more units than resident CTAs:
+    units are claimed dynamically and the last ~1,184 (t, tile) jobs run as
+    4 strips each (KParams::tail_from).  Every byte must equal the single-t
+    calls, which run one whole-tile unit per CTA (static)."""
+    lay, seed = S.config(cell)
+    ctx = _load(lay, S.make_theta(lay, seed))
+    ts = [i / 24 for i in range(24)]
+    q = gpu_full(ctx, ts, "rgba8")
+    for ti in (0, 7, 21, 22, 23):
+        np.testing.assert_array_equal(q[ti], gpu_full(ctx, ts[ti], "rgba8")[0])
+
+
 def test_host_buffer_path():
     lay, seed = S.config("c1")
     th = S.make_theta(lay, seed)
