@@ -119,14 +119,17 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
 }
 
 // ---- GELU epilogue of one layer: D (fp32) -> f16x2 GELU~ -> A23 ---------------
-// NDGI_POLY_PAIRS of every 8 f16x2 GELU pairs run on the FMA pipe
+// Some of every 8 f16x2 GELU pairs run on the FMA pipe
 // (gelu_poly_f16x2) instead of MUFU.TANH: the MUFU queue (mio_throttle) is the
 // hot loop's main stall; 2 + 1 of the step's 16 measured best
-#ifndef NDGI_POLY_PAIRS
-#define NDGI_POLY_PAIRS 1
+#ifndef NDGI_POLY_PAIRS         // h = 16, the second item of a step: 3 of 8 (measured)
+#define NDGI_POLY_PAIRS 3
 #endif
-#ifndef NDGI_POLY_PAIRS_ITEM0   // the first item of a step: 2 of 8 (measured)
-#define NDGI_POLY_PAIRS_ITEM0 2
+#ifndef NDGI_POLY_PAIRS_ITEM0   // h = 16, the first item of a step: 3 of 8
+#define NDGI_POLY_PAIRS_ITEM0 3
+#endif
+#ifndef NDGI_POLY_PAIRS64       // h = 64: 1 of every 8
+#define NDGI_POLY_PAIRS64 1
 #endif
 template <int H>
 __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) {
@@ -138,7 +141,7 @@ __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) 
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const uint32_t x = pack_f16x2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
-            g[q] = q < 8 - NDGI_POLY_PAIRS ? gelu_scaled_f16x2(x) : gelu_poly_f16x2(x);
+            g[q] = q < 8 - NDGI_POLY_PAIRS64 ? gelu_scaled_f16x2(x) : gelu_poly_f16x2(x);
         }
         ptx::tmem_st_x8(a_addr + c0 / 2, g);
     }

@@ -34,9 +34,9 @@ cudaError_t prep_weights(const uint16_t* mlp, size_t tile_elems, int H, int fmt_
 
 // the GELU split compiled into the epilogues: MUFU pairs of every 16 (h = 16:
 // a step's two items take NDGI_POLY_PAIRS_ITEM0 + NDGI_POLY_PAIRS polynomial
-// pairs of their 2 x 8; h = 64: NDGI_POLY_PAIRS of every 8)
+// pairs of their 2 x 8; h = 64: NDGI_POLY_PAIRS64 of every 8)
 int fused_gelu_mufu_pairs(int H) {
-    return H == 16 ? 16 - NDGI_POLY_PAIRS_ITEM0 - NDGI_POLY_PAIRS : 16 - 2 * NDGI_POLY_PAIRS;
+    return H == 16 ? 16 - NDGI_POLY_PAIRS_ITEM0 - NDGI_POLY_PAIRS : 16 - 2 * NDGI_POLY_PAIRS64;
 }
 int fused_f16acc() { return NDGI_F16ACC; }
 

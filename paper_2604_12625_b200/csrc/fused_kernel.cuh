@@ -39,6 +39,10 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
+#ifndef NDGI_OUT_PTR   // experiment builds: 0 = per-item output index arithmetic
+#define NDGI_OUT_PTR 1
+#endif
+
 
 
 // NDGI_TIMELINE=1 (diagnostic builds only): %globaltimer stamps of block 0's
@@ -539,6 +543,10 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
         // FULL8: this thread's texel of core row j_begin in the RGBA8 atlas
         uint32_t* const orow = reinterpret_cast<uint32_t*>(p.out) + out_base + (size_t)j_begin * row_pitch + tid;
         const uint32_t rp32 = (uint32_t)row_pitch;
+        // C = 128 FULL8: a step's two items are rows j, j + 1 of one column --
+        // one running pointer (this thread's texel of row j) instead of 64-bit
+        // index arithmetic per item
+        uint32_t* optr = orow;
 
         // a8: y of block (row j, blk) in slot s -> page cache
         auto output = [&](int j, int blk, int s) {
@@ -549,7 +557,13 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
             if constexpr (FULL8) {
                 NDGI_CHECK(out_base + (size_t)j * row_pitch + i < out_texels);
-                orow[(size_t)((uint32_t)(j - j_begin) * rp32) + blk * kThreads] = rgba8_fma(y0f, y1f, y2f);
+                if constexpr (BPR == 1 && S == 2 && NDGI_OUT_PTR) {
+                    NDGI_CHECK(optr == orow + (size_t)(j - j_begin) * rp32 - (s ? rp32 : 0));
+                    optr[s ? rp32 : 0] = rgba8_fma(y0f, y1f, y2f);
+                    if (s) optr += 2 * (size_t)rp32;
+                } else {
+                    orow[(size_t)((uint32_t)(j - j_begin) * rp32) + blk * kThreads] = rgba8_fma(y0f, y1f, y2f);
+                }
                 return;
             }
             // decode_tiles: core texel (j, i) and its mirrored border copies
