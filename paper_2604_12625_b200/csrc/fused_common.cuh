@@ -128,8 +128,8 @@ __host__ __device__ inline FusedSmem fused_smem_layout(int C, int R3) {
 #ifndef NDGI_POLY_PAIRS_ITEM0   // h = 16, the first item of a step: 3 of 8
 #define NDGI_POLY_PAIRS_ITEM0 3
 #endif
-#ifndef NDGI_POLY_PAIRS64       // h = 64: 1 of every 8
-#define NDGI_POLY_PAIRS64 1
+#ifndef NDGI_POLY_PAIRS64       // h = 64: 3 of every 8 (measured)
+#define NDGI_POLY_PAIRS64 3
 #endif
 template <int H>
 __device__ __forceinline__ void gelu_epilogue(uint32_t d_addr, uint32_t a_addr) {

@@ -604,6 +604,11 @@ struct ndgi_train {
     int* steps;
     uint32_t cap;                  // batch capacity of grad / loss / dtex
     uint32_t last_n;               // batch of the last step (ndgi_train_last_grad)
+    // fine-tuning: the frozen BC7 feature maps decoded once (bit-exact) into
+    // owned u8 copies, [tile][R][R][4] and [tile][D][R3][R3][4], so a step's
+    // taps are plain loads instead of a BC7 block decode each (same values:
+    // both paths dequantise q / 255, R8); nullptr for other formats
+    uint8_t *uv8, *uvt8;
 };
 
 namespace {
@@ -656,12 +661,25 @@ ndgi_status train_create(ndgi_ctx* ctx, bool full, const float* init, ndgi_train
         if (full) e = cudaMemcpy(t->theta, init, n * 4, cudaMemcpyDeviceToDevice);
         else e = ndgi::launch_convert_f16_f32(ctx->P.mlp, t->theta, n, 0);   // fp32 master copy
     }
+    const ndgi_layout& L = ctx->L;
+    if (e == cudaSuccess && !full && L.fmt_uv == NDGI_FMT_BC7) {
+        // tile-major blocks = one image of R_uv x (R_uv * tiles) in block row-major order
+        e = cudaMalloc(&t->uv8, (size_t)L.num_tiles * L.uv_res * L.uv_res * 4);
+        if (e == cudaSuccess) e = ndgi::launch_bc7_map(ctx->P.uv, L.uv_res, L.uv_res * L.num_tiles, t->uv8, 0);
+    }
+    if (e == cudaSuccess && !full && L.fmt_uvt == NDGI_FMT_BC7) {
+        e = cudaMalloc(&t->uvt8, (size_t)L.num_tiles * L.uvt_depth * L.uvt_res * L.uvt_res * 4);
+        if (e == cudaSuccess)
+            e = ndgi::launch_bc7_map(ctx->P.uvt, L.uvt_res, L.uvt_res * L.uvt_depth * L.num_tiles, t->uvt8, 0);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(t->theta);
         cudaFree(t->m);
         cudaFree(t->v);
         cudaFree(t->steps);
+        cudaFree(t->uv8);
+        cudaFree(t->uvt8);
         delete t;
         return cuda_fail(e, "training state allocation");
     }
@@ -714,6 +732,17 @@ ndgi_status train_step(ndgi_train* t, const uint32_t* tile_ids, uint32_t n, cons
     a.line_tile_bytes = map2d_bytes(L.fmt_line, L.line_res, L.line_t, 2);
     a.fmt_uv = (int)L.fmt_uv;
     a.fmt_uvt = (int)L.fmt_uvt;
+    if (t->uv8) {   // the decoded copies (train_create)
+        a.uv = t->uv8;
+        a.fmt_uv = NDGI_FMT_U8;
+        a.uv_tile_bytes = (size_t)L.uv_res * L.uv_res * 4;
+    }
+    if (t->uvt8) {
+        a.uvt = t->uvt8;
+        a.fmt_uvt = NDGI_FMT_U8;
+        a.uvt_slice_bytes = (size_t)L.uvt_res * L.uvt_res * 4;
+        a.uvt_tile_bytes = a.uvt_slice_bytes * L.uvt_depth;
+    }
     a.fmt_line = (int)L.fmt_line;
     a.R_uv = (int)L.uv_res;
     a.R3 = (int)L.uvt_res;
@@ -845,6 +874,8 @@ ndgi_status ndgi_train_free(ndgi_train* t) {
     cudaFree(t->grad);
     cudaFree(t->loss);
     cudaFree(t->dtex);
+    cudaFree(t->uv8);
+    cudaFree(t->uvt8);
     delete t;
     return NDGI_OK;
 }

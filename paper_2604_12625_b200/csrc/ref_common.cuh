@@ -32,8 +32,13 @@ __device__ __forceinline__ void fetch_texel(const Map2D& m, int a, int b, float*
         const uint32_t v = bc7_texel(raw, 4 * (b & 3) + (a & 3));
         for (int c = 0; c < m.nc; ++c) out[c] = (float)((v >> (8 * c)) & 0xffu) / 255.0f;
     } else if (m.fmt == FMT_U8) {
-        const uint8_t* p = m.base + ((size_t)b * m.rx + a) * m.nc;
-        for (int c = 0; c < m.nc; ++c) out[c] = (float)p[c] / 255.0f;
+        if (m.nc == 4) {   // one 32-bit load (U8 maps are 4-byte aligned, include/ndgi.h)
+            const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(m.base) + ((size_t)b * m.rx + a));
+            for (int c = 0; c < 4; ++c) out[c] = (float)((v >> (8 * c)) & 0xffu) / 255.0f;
+        } else {
+            const uint8_t* p = m.base + ((size_t)b * m.rx + a) * m.nc;
+            for (int c = 0; c < m.nc; ++c) out[c] = (float)p[c] / 255.0f;
+        }
     } else if (m.fmt == FMT_F16) {
         const uint16_t* p = reinterpret_cast<const uint16_t*>(m.base) + ((size_t)b * m.rx + a) * m.nc;
         for (int c = 0; c < m.nc; ++c) out[c] = half_bits_to_float(p[c]);
