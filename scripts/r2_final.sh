@@ -7,3 +7,6 @@ timeout 900 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_benc
 timeout 900 python bench.py --workload c4 --steps 5 --warmup 3 --no-cpu --no-vt --no-shading --no-encode --no-finetune --no-texunit > gpurun_out/${T}_c4.json 2> gpurun_out/${T}_c4.err; tail -c 200 gpurun_out/${T}_c4.json
 timeout 1200 python scripts/sweep.py > gpurun_out/${T}_sweep.json 2> gpurun_out/${T}_sweep.err; tail -c 200 gpurun_out/${T}_sweep.json
 bash scripts/round_capture.sh ${T}
+python scripts/residency_probe.py c2 > gpurun_out/${T}_residency.txt 2>&1
+RES_LIB=libndgi_res.so python scripts/residency_probe.py c5:H:bc7 >> gpurun_out/${T}_residency.txt 2>&1
+python scripts/ncu_summary.py gpurun_out/${T}_M.ncu-rep gpurun_out/${T}_launches.csv > gpurun_out/${T}_M.txt 2>&1
