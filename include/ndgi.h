@@ -21,14 +21,20 @@
  * - Decode calls are stream-ordered and asynchronous on the given
  *   cudaStream_t (passed as void*; NULL = legacy default stream) unless
  *   documented otherwise.  They never synchronise.
- * - Outputs are bit-deterministic for identical inputs (no data atomics).
+ * - Outputs are bit-deterministic for identical inputs (no atomics on data).
  * - Host-detectable argument errors are reported synchronously; a tile id
  *   >= num_tiles or a slot >= num_slots is detected on the device: that
  *   request is skipped and the context's error counter is incremented
  *   (read it with ndgi_device_error).
  * - Thread safety: one context may be used from several host threads on
  *   different streams; the context is read-only after ndgi_load except for
- *   its device error counter.
+ *   its device error counter and its work-scheduling counters: a FAST decode
+ *   launch with more work units than resident CTAs takes the next of 1,024
+ *   per-context counters (zeroed by a cudaMemsetAsync on the call's stream
+ *   before the kernel; the CTAs claim units from it with atomics -- the
+ *   claimed order never changes the output).  More than 1,024 such launches
+ *   in flight at once on different streams of one context, or concurrent
+ *   replays of one captured CUDA graph, would share a counter: unsupported.
  */
 #ifndef NDGI_H
 #define NDGI_H
