@@ -23,8 +23,10 @@
 // CTA = 4 warps; thread t owns TMEM lane t, i.e. texel t of each 128-texel
 // item.  A step carries S items (S TMEM slots: 2 for h = 16, 1 for h = 64)
 // through the three layers together: per layer one CTA barrier, S (x K/16)
-// tcgen05.mma issued by one elected lane, one tcgen05.commit -> mbarrier.
-// Several CTAs per SM (6 for h = 16) hide each other's MMA latency.
+// tcgen05.mma issued by one elected lane, one tcgen05.commit -> mbarrier
+// (polled by the issuing warp; the others wait in the next CTA barrier).
+// Several CTAs per SM (8 for h = 16, 4 for h = 64) hide each other's MMA
+// latency; units are claimed dynamically (KParams::sched).
 #include <cuda_runtime.h>
 
 #include <cstdio>
