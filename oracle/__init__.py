@@ -19,7 +19,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ndgi_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# ORACLE_LIB: load another build of the same source (tests/test_oracle_sanitizers.py
+# runs the pins against an ASan + UBSan build)
+_LIB = os.environ.get("ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
 
 FMT = {"bc7": 0, "u8": 1, "f16": 2, "bc1": 3, "bc3": 4, "bc5": 5}
 GELU = {"erf": 0, "tanh": 1}
@@ -28,6 +30,8 @@ BORDER = {"mirror": 0, "eval_clamp": 1}
 
 def build(force: bool = False) -> str:
     """Compile ndgi_oracle.c to liboracle.so (plain gcc, -O2, fp-contract off)."""
+    if os.environ.get("ORACLE_LIB"):
+        return _LIB   # an external build (sanitizer runs), never rebuilt here
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(
             ["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-ffp-contract=off", "-fPIC", "-shared",
