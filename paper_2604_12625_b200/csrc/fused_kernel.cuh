@@ -41,9 +41,6 @@ namespace ndgi {
 
 constexpr int kThreads = 128;
 
-#ifndef NDGI_OUT_PTR   // experiment builds: 0 = per-item output index arithmetic
-#define NDGI_OUT_PTR 1
-#endif
 
 
 
@@ -559,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, FusedCfg<H>::MIN_CTAS) ndgi_fused_ke
             const float y0f = __uint_as_float(yv[0]), y1f = __uint_as_float(yv[1]), y2f = __uint_as_float(yv[2]);
             if constexpr (FULL8) {
                 NDGI_CHECK(out_base + (size_t)j * row_pitch + i < out_texels);
-                if constexpr (BPR == 1 && S == 2 && NDGI_OUT_PTR) {
+                if constexpr (BPR == 1 && S == 2) {
                     NDGI_CHECK(optr == orow + (size_t)(j - j_begin) * rp32 - (s ? rp32 : 0));
                     optr[s ? rp32 : 0] = rgba8_fma(y0f, y1f, y2f);
                     if (s) optr += 2 * (size_t)rp32;

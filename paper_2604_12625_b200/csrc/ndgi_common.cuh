@@ -167,13 +167,9 @@ __device__ __forceinline__ int mirror_core(int i, int C) {
 // RGBA8 texel on the FMA pipe (no F2I on the XU/MUFU pipe): clamp to [0,1],
 // then t*255 + 1.5*2^23 rounds the exact product to the nearest integer, ties
 // to even, into the low mantissa bits (R12); A = 255.
-#ifndef NDGI_RGBA8_NEG
-#define NDGI_RGBA8_NEG 1
-#endif
 __device__ __forceinline__ uint32_t rgba8_fma(float r, float g, float b) {
     const uint32_t qr = __float_as_uint(fmaf(__saturatef(r), 255.0f, 12582912.0f));
     const uint32_t qg = __float_as_uint(fmaf(__saturatef(g), 255.0f, 12582912.0f));
-#if NDGI_RGBA8_NEG
     // blue on the negative side: -(1.5 * 2^23 + RN-even(255 b)) has the same low
     // byte (round-to-nearest-even is symmetric) and a sign byte 0xCB, whose
     // replicated MSB is A = 255 -- two PRMTs, no constant
@@ -182,10 +178,6 @@ __device__ __forceinline__ uint32_t rgba8_fma(float r, float g, float b) {
     uint32_t v;
     asm("prmt.b32 %0, %1, %2, 0xF410;" : "=r"(v) : "r"(__byte_perm(qr, qg, 0x0040u)), "r"(qb));
     return v;
-#else
-    const uint32_t qb = __float_as_uint(fmaf(__saturatef(b), 255.0f, 12582912.0f));
-    return __byte_perm(__byte_perm(qr, qg, 0x0040u), __byte_perm(qb, 0xffu, 0x0040u), 0x5410u);
-#endif
 }
 
 __device__ __forceinline__ void store_texel(void* out, size_t idx, int fmt, float r, float g, float b) {
