@@ -478,6 +478,33 @@ def test_dynamic_schedule_and_tail_strips_equal_single_calls(cell):
         np.testing.assert_array_equal(q[ti], gpu_full(ctx, ts[ti], "rgba8")[0])
 
 
+def test_dynamic_schedule_with_invalid_requests():
+    """A decode_tiles batch with more units than resident CTAs (1,200 requests
+    -> 4 strips each, claimed dynamically) in which every 7th id and every 11th
+    slot is invalid: the skipped units still claim their successors (no unit
+    lost, no hang), the error counter counts each bad request once, and every
+    valid slot is byte-identical to the same tile decoded alone."""
+    lay, seed = S.config("c1")
+    ctx = _load(lay, S.make_theta(lay, seed))
+    n = 1200
+    rng = np.random.default_rng(5)
+    ids = rng.integers(0, 4, n)
+    ids[::7] = 4 + (np.arange(len(ids[::7])) % 3)          # id >= num_tiles
+    slots = np.arange(n)
+    slots[5::11] = n + 3                                     # slot >= num_slots
+    bad = (ids >= 4) | (slots >= n)
+    ndgi.ndgi_device_error(ctx, reset=True)
+    out = gpu_tiles(ctx, ids, 0.45, "rgba8", slots=slots, num_slots=n)
+    assert ndgi.ndgi_device_error(ctx, reset=True) == int(bad.sum())
+    alone = {k: gpu_tiles(ctx, [k], 0.45, "rgba8")[0] for k in range(4)}
+    for r in range(n):
+        if bad[r]:
+            if slots[r] < n:
+                assert (out[slots[r]] == 0).all(), r
+        else:
+            np.testing.assert_array_equal(out[slots[r]], alone[int(ids[r])], err_msg=str(r))
+
+
 def test_host_buffer_path():
     lay, seed = S.config("c1")
     th = S.make_theta(lay, seed)
